@@ -1,0 +1,149 @@
+"""Workload configurations (BASELINE.json `configs`, 0-based) and seeded dataset builder.
+
+Input recipe only (see datagen/sources.py): this module never whitens or runs
+any step of the method.  `make_dataset` returns the RAW mixed signals
+X = A S (+ sensor noise); whitening is the boundary call `whiten` (oracle side:
+oracle.whiten, product side: oica_whiten).
+
+Seeds: data seed 1000 + k, candidate seed 2000 + k for BASELINE config k
+(SURVEY.md §8(d)).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+from typing import List, Optional, Tuple
+
+import torch
+
+from . import sources as S
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    N: int
+    M: int
+    L: int
+    K: int
+    tol: float
+    N_out: int
+    recipe: Tuple[Tuple, ...]          # ((kind, count, params...), ...)
+    noise_sd: float = 0.0
+    data_seed: int = 1000
+    cand_seed: int = 2000
+
+    def with_(self, **kw) -> "Config":
+        return replace(self, **kw)
+
+
+# BASELINE.json configs[0..4] (0-based; SURVEY.md §8c A21/A22 readings).
+CONFIGS = [
+    Config("cfg0_tiny", 8, 2000, 64, 200, 1e-10, 8,
+           (("laplace", 4), ("student_t", 1, 5.0), ("student_t", 1, 7.0),
+            ("student_t", 1, 9.0), ("student_t", 1, 12.0)),
+           data_seed=1000, cand_seed=2000),
+    Config("cfg1_artificial", 32, 20000, 1024, 200, 1e-10, 32,
+           (("laplace", 16), ("gg_uniform", 16, 0.5, 1.5)),
+           data_seed=1001, cand_seed=2001),
+    Config("cfg2_eeg_shaped", 64, 250000, 4096, 200, 1e-10, 32,
+           (("spikes", 12, 0.01, 25.0), ("laplace", 20), ("ar1_uniform", 32, 0.5, 0.95)),
+           noise_sd=0.1, data_seed=1002, cand_seed=2002),
+    Config("cfg3_large", 128, 1000000, 16384, 200, 1e-10, 64,
+           (("gg_uniform", 128, 0.6, 1.8),),
+           data_seed=1003, cand_seed=2003),
+    Config("cfg4_scaling", 256, 4000000, 65536, 200, 1e-10, 32,
+           (("gg_uniform", 256, 0.5, 1.9),),
+           data_seed=1004, cand_seed=2004),
+]
+
+BY_NAME = {c.name: c for c in CONFIGS}
+
+
+def get(name_or_index) -> Config:
+    if isinstance(name_or_index, int):
+        return CONFIGS[name_or_index]
+    if name_or_index in BY_NAME:
+        return BY_NAME[name_or_index]
+    if name_or_index.isdigit():
+        return CONFIGS[int(name_or_index)]
+    raise KeyError(name_or_index)
+
+
+@dataclass
+class Dataset:
+    X: torch.Tensor                      # N x M raw observed signals
+    A: torch.Tensor                      # N x N mixing matrix
+    S: Optional[torch.Tensor]            # N x M sources (None if not kept)
+    kinds: List[str] = field(default_factory=list)
+
+
+def _expand(recipe, g, device) -> List[Tuple[str, tuple]]:
+    rows = []
+    for item in recipe:
+        kind, count, *p = item
+        for _ in range(count):
+            if kind == "gg_uniform":
+                lo, hi = p
+                rho = lo + (hi - lo) * float(torch.rand(1, generator=g, device=device, dtype=torch.float64).item())
+                rows.append(("gg", (rho,)))
+            elif kind == "ar1_uniform":
+                lo, hi = p
+                r = lo + (hi - lo) * float(torch.rand(1, generator=g, device=device, dtype=torch.float64).item())
+                rows.append(("ar1", (r,)))
+            else:
+                rows.append((kind, tuple(p)))
+    return rows
+
+
+def make_sources(cfg: Config, seed: Optional[int] = None, device="cpu", dtype=torch.float64, M: Optional[int] = None):
+    """Seeded N x M source matrix for `cfg` (rows in recipe order)."""
+    g = S._gen(cfg.data_seed if seed is None else seed, device)
+    M = cfg.M if M is None else M
+    rows = _expand(cfg.recipe, g, device)
+    assert len(rows) == cfg.N, (cfg.name, len(rows), cfg.N)
+    out = torch.empty(cfg.N, M, dtype=dtype, device=device)
+    kinds = []
+    for j, (kind, p) in enumerate(rows):
+        if kind == "laplace":
+            out[j] = S.laplace(M, g, device, dtype)
+        elif kind == "student_t":
+            out[j] = S.student_t(p[0], M, g, device, dtype)
+        elif kind == "gg":
+            out[j] = S.gen_gaussian(p[0], M, g, device, dtype)
+        elif kind == "spikes":
+            out[j] = S.spikes(p[0], p[1], M, g, device, dtype)
+        elif kind == "ar1":
+            out[j] = S.ar1(p[0], M, g, device, dtype)
+        elif kind == "gaussian":
+            out[j] = S.gaussian(M, g, device, dtype)
+        elif kind == "uniform":
+            out[j] = S.uniform(M, g, device, dtype)
+        else:
+            raise ValueError(kind)
+        kinds.append(f"{kind}{p}")
+    return out, kinds, g
+
+
+def make_dataset(cfg: Config, seed: Optional[int] = None, device="cpu", dtype=torch.float64,
+                 keep_sources: bool = True, M: Optional[int] = None) -> Dataset:
+    """X = A S (+ N(0, noise_sd^2) sensor noise), A ~ iid N(0,1) with cond(A) < 1e6."""
+    Ssrc, kinds, g = make_sources(cfg, seed, device, dtype, M)
+    A = S.mixing_matrix(cfg.N, g, device, dtype)
+    X = A @ Ssrc
+    if cfg.noise_sd > 0:
+        X += cfg.noise_sd * torch.randn(X.shape, dtype=dtype, device=device, generator=g)
+    return Dataset(X=X, A=A, S=Ssrc if keep_sources else None, kinds=kinds)
+
+
+# Small parity workloads: oracle finishes in seconds, several tiles + ragged tails.
+PARITY = {
+    "p_tiny": CONFIGS[0],
+    "p_ragged": Config("p_ragged", 12, 5003, 300, 200, 1e-10, 5,
+                       (("laplace", 6), ("gg_uniform", 6, 0.5, 1.5)),
+                       data_seed=3001, cand_seed=4001),
+    "p_cfg1_reducedL": CONFIGS[1].with_(name="p_cfg1_reducedL", L=160, N_out=6),
+    "p_n40": Config("p_n40", 40, 12000, 257, 200, 1e-10, 4,
+                    (("laplace", 20), ("gg_uniform", 20, 0.6, 1.8)),
+                    data_seed=3003, cand_seed=4003),
+}
