@@ -1,0 +1,218 @@
+/*
+ * oica.h -- C ABI of liboica.so, the B200 (sm_100a) hot path of Fast Ordering ICA
+ * (Matsuda & Yamaguchi, "Efficient Estimation of Unique Components in ICA by Matrix
+ * Representation", arXiv 2408.17118).  Citations "PAPER.md:n" are lines of the paper's
+ * LaTeX source; readings Ann are listed in DESIGN.md §2.
+ *
+ * The library computes, for each component i = 1..N_out (Alg. 2):
+ *   draw L candidate rows, project them orthogonal to the accepted
+ *   rows (E = W^T W, w <- w - E w) and normalise; then iterate
+ *     Z = B X,  B <- (Z o Z o Z) X^T / M - 3 B,
+ *     project, normalise, drop converged rows
+ *   and accept the candidate of largest Upsilon(alpha), alpha = sum z^4 / M - 3
+ *   (eqs. (1)-(2), :257-259, :264).
+ *
+ * Conventions (all functions):
+ *   - Every function returns oica_status; no C++ exception crosses the ABI.
+ *     oica_last_error(ctx) holds a message until the next call on ctx.
+ *   - "device" pointers are CUDA global-memory addresses on the context's device;
+ *     "host" pointers are ordinary CPU memory.  Matrices are ROW-MAJOR.
+ *   - The caller owns every buffer it passes and allocates every output; the library
+ *     never frees caller memory and retains no host pointer after a call returns.
+ *     Device inputs passed to oica_set_data are BORROWED until the next set_data /
+ *     destroy; all derived operands and workspace are owned by the context.
+ *   - CUDA / NCCL failures return OICA_ERR_CUDA / OICA_ERR_NCCL and leave the context
+ *     usable only for oica_destroy.
+ *   - A context is single-threaded: one context per device and rank.
+ *   - With world > 1 every call that computes is COLLECTIVE: all ranks call it with
+ *     identical scalar arguments.
+ */
+#ifndef OICA_H_
+#define OICA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct oica_ctx oica_ctx;
+
+typedef enum {
+  OICA_OK = 0,
+  OICA_ERR_INVALID_ARGUMENT = 1,      /* bad size, NULL pointer, out-of-range parameter      */
+  OICA_ERR_DIMENSION_MISMATCH = 2,    /* shapes inconsistent with the data set on the ctx     */
+  OICA_ERR_RANK_DEFICIENT = 3,        /* whitening: covariance eigenvalue < floor (A11)       */
+  OICA_ERR_ALL_CANDIDATES_DEGENERATE = 4, /* every candidate projected to ||w|| < 1e-12 (A18)  */
+  OICA_ERR_DOMAIN = 5,                /* no eligible candidate has alpha > -2 (eq. (1), A13)  */
+  OICA_ERR_STATE = 6,                 /* call order violated (e.g. extract before set_data)   */
+  OICA_ERR_UNSUPPORTED_DEVICE = 7,    /* device is not compute capability 10.0 (sm_100a)      */
+  OICA_ERR_OUT_OF_MEMORY = 8,
+  OICA_ERR_CUDA = 9,
+  OICA_ERR_NCCL = 10
+} oica_status;
+
+/* Arithmetic of the fixed-point contraction (the two products of PAPER.md:243-245). */
+typedef enum {
+  OICA_PREC_AUTO = 0,   /* TC where N >= 16 and the kernel supports the shape, else FP32     */
+  OICA_PREC_FP32 = 1,   /* FP32 FFMA on CUDA cores, fp32 accumulate per flush, fp64 slots    */
+  OICA_PREC_TC = 2      /* tcgen05 tensor cores, split-fp16 GEMM1 (W_hi+W_lo) / fp16 GEMM2   */
+} oica_precision;
+
+/* Multi-GPU partitioning.  world == 1 ignores it. */
+typedef enum {
+  OICA_SHARD_L = 0,     /* candidates split over ranks, X replicated, one exchange/component */
+  OICA_SHARD_M = 1      /* samples split over ranks, fp64 allreduce of G, s4 per iteration   */
+} oica_shard_mode;
+
+typedef struct {
+  int32_t device;            /* CUDA device ordinal                                         */
+  int32_t rank;              /* 0 <= rank < world                                           */
+  int32_t world;             /* number of ranks (1 = single GPU)                            */
+  int32_t shard_mode;        /* oica_shard_mode                                             */
+  int32_t precision;         /* oica_precision                                              */
+  int32_t reserved;
+  void* stream;              /* cudaStream_t to run on, or NULL: the context creates one    */
+  const void* nccl_unique_id;/* 128-byte ncclUniqueId from oica_nccl_unique_id (world > 1)  */
+} oica_config;
+
+/* Per-component results, caller-allocated HOST arrays of length >= N_out (W: N_out x N). */
+typedef struct {
+  double* W;              /* accepted rows, canonical sign (A17), whitened coordinates       */
+  double* alpha;          /* alpha_q = sum_m y^4/M - 3 at the accepted w (eq. (2), A15)      */
+  double* upsilon;        /* Upsilon(alpha_q) (eq. (1))                                      */
+  int64_t* index;         /* q: global candidate id accepted (cluster minimum, A6)            */
+  int32_t* iters;         /* fixed-point updates applied to candidate q                      */
+  int32_t* n_iter;        /* iterations executed for the component (max over candidates)     */
+  int32_t* cluster_size;  /* eligible candidates on q's fixed point (1-|cos| <= 1e-6)        */
+  int32_t* n_converged;   /* candidates that met the convergence test (A1/A2)                */
+  int32_t* n_unconverged; /* candidates still active at the cap K (A4)                       */
+  int32_t* n_degenerate;  /* candidates with ||w|| < 1e-12 after a projection (A18)          */
+  int64_t* sum_active;    /* sum over iterations of active rows (algorithmic-work counter)   */
+  uint8_t* gaussian_flag; /* Upsilon_q < 2(N-i+2)(N-i+1)/M                    */
+  uint8_t* near_tie;      /* best and second-best clusters within 1e-6 relative (A6)         */
+  int32_t n_extracted;    /* rows written (< N_out only with OICA_STOP_ON_GAUSSIANITY)       */
+  int32_t stopped;        /* 1 if the Gaussianity test ended extraction   */
+} oica_result;
+
+/* Flags for oica_extract_components. */
+#define OICA_INCLUDE_UNCONVERGED 0x1u  /* rows still active at K join the argmax (A4, Alg. 1)   */
+#define OICA_STOP_ON_GAUSSIANITY 0x2u  /* break on the Gaussianity test     */
+#define OICA_RAW_ARGMAX          0x4u  /* accept p = argmax itself, no cluster rule (A6)        */
+
+/* Counters of the last extract / step call (for benchmarks; all host values). */
+typedef struct {
+  int64_t kernel_launches;   /* kernels launched by the library since the last reset        */
+  int64_t step_launches;     /* launches of the fused fixed-point kernel                    */
+  double step_ms;            /* summed CUDA-event time of those launches                    */
+  double step_flops;         /* algorithmic flops of those launches: sum L_act (4NM + 3M)   */
+  int64_t iterations;        /* fixed-point iterations executed                             */
+  int64_t sum_active;        /* sum over iterations of active rows                           */
+  int32_t precision;         /* precision actually used by the step kernel                  */
+  int32_t slots;             /* split-M slots S                                             */
+} oica_stats;
+
+/* ---- lifetime ---------------------------------------------------------------------- */
+
+/* Create a context on cfg->device.  Fails with OICA_ERR_UNSUPPORTED_DEVICE unless the device
+ * is compute capability 10.0.  world > 1 initialises an NCCL communicator from
+ * cfg->nccl_unique_id (collective over all ranks). */
+oica_status oica_create(const oica_config* cfg, oica_ctx** out);
+oica_status oica_destroy(oica_ctx* ctx);
+const char* oica_status_string(oica_status s);
+const char* oica_last_error(const oica_ctx* ctx);
+/* Write a fresh 128-byte ncclUniqueId into out (host); call on rank 0 and broadcast. */
+oica_status oica_nccl_unique_id(void* out);
+
+/* ---- boundary: whitening "in advance" (readings A11/A12) ---------- */
+
+/* X_dev: device fp32 N x M raw signals, row stride ld >= M.  Computes the row means, the
+ * covariance C = Xc Xc^T / M in fp64, its eigendecomposition (host Jacobi), V = D^{-1/2} E^T
+ * (eigenvalues descending, each eigenvector's largest-|entry| positive) and writes
+ * Xw = V (X - mean) as fp32 to Xw_dev (N x M, stride ld_out >= M).  mean_out (N), V_out (N x N),
+ * eig_out (N) are host fp64 and may be NULL.  RANK_DEFICIENT if min eig < eig_floor * max eig. */
+oica_status oica_whiten(oica_ctx* ctx, const float* X_dev, int64_t N, int64_t M, int64_t ld,
+                        double eig_floor, float* Xw_dev, int64_t ld_out,
+                        double* mean_out, double* V_out, double* eig_out);
+
+/* ---- data and candidates --------------------------------------------------------------- */
+
+/* Bind whitened data: Xw_dev device fp32 N x M_local (stride ld >= M_local), BORROWED.
+ * M_global is the total sample count M of eq. (2) (== M_local unless shard_mode = M).
+ * 1 <= N <= 256, M_global > N.  Prepares the context-owned operand planes. */
+oica_status oica_set_data(oica_ctx* ctx, const float* Xw_dev, int64_t N, int64_t M_local,
+                          int64_t ld, int64_t M_global);
+/* Same with a HOST fp32 source: the library copies it into an owned device buffer
+ * (the end-to-end entry point; the copy is part of the call). */
+oica_status oica_set_data_host(oica_ctx* ctx, const float* Xw_host, int64_t N, int64_t M_local,
+                               int64_t ld, int64_t M_global);
+
+/* Fix the candidate generator (seed) and the global candidate count L (PAPER.md:126, :136,
+ * :237; readings A7/A8).  Candidates are drawn afresh for every component from the
+ * counter-based generator of DESIGN.md §2 A7, keyed by (seed, i, global id l, coordinate).
+ * L-shard: rank r owns ids [r*L/world, (r+1)*L/world).  1 <= L < 2^24. */
+oica_status oica_init_candidates(oica_ctx* ctx, uint64_t seed, int64_t L);
+
+/* ---- the hot path ---------------------------------------------------------------------- */
+
+/* Extract components k_prefix+1 .. N_out (Alg. 2 with the projection of Alg. 1).
+ * max_iter = K >= 1 (do-while, A19); tol > 0 is the convergence test 1 - |w . w_prev| <= tol
+ * (A1/A2; the paper's chord eps corresponds to tol = eps^2/2).  W_prefix (host fp64
+ * k_prefix x N, orthonormal rows, may be NULL when k_prefix == 0) seeds the accepted rows
+ * (resume / teacher forcing).  Writes rows k_prefix .. n_extracted-1 of out (synchronous).
+ * Errors: ALL_CANDIDATES_DEGENERATE, DOMAIN, INVALID_ARGUMENT (N_out outside [k_prefix+1, N]). */
+oica_status oica_extract_components(oica_ctx* ctx, int32_t N_out, int32_t max_iter, double tol,
+                                    uint32_t flags, const double* W_prefix, int32_t k_prefix,
+                                    oica_result* out);
+
+/* ---- test and benchmark entry points ---------------------------------------------------- */
+
+/* One fused contraction (PAPER.md:243-244 before the -3B term) on caller rows:
+ * W_dev device fp64 L x N (unit rows); outputs device fp64 G_dev (L x N) = sum_m y^3 x^T and
+ * s4_dev (L) = sum_m y^4 with y = w X, summed over the local samples in the context's precision
+ * and slot order.  (Uses the context's workspace; L <= the L of init_candidates.) */
+oica_status oica_fixed_point_step(oica_ctx* ctx, const double* W_dev, int64_t L,
+                                  double* G_dev, double* s4_dev);
+/* The candidate generator + projection + normalisation
+ * for component i (1-based) against host W_acc (k x N, may be NULL if k == 0):
+ * writes this rank's L_local x N fp64 rows to W_dev (device).  Degenerate rows are zero. */
+oica_status oica_draw_candidates(oica_ctx* ctx, int32_t i, const double* W_acc, int32_t k,
+                                 double* W_dev);
+/* End state of the last extracted component's candidates on this rank (host outputs, each
+ * L_local long, any may be NULL): W (L_local x N fp64), alpha at the last forward pass,
+ * iterations, state (0 active/unconverged, 1 converged, 2 degenerate). */
+oica_status oica_get_candidates(oica_ctx* ctx, double* W, double* alpha, int32_t* iters,
+                                uint8_t* state, int64_t* L_local, int64_t* id_base);
+oica_status oica_get_stats(oica_ctx* ctx, oica_stats* out);
+oica_status oica_reset_stats(oica_ctx* ctx);
+/* Synchronise the context's stream (for host-side timing). */
+oica_status oica_synchronize(oica_ctx* ctx);
+
+/* ---- host-only selection merge (multi-GPU decision; also unit-tested on CPU) ------------ */
+
+/* One candidate cluster as reported by a rank: its minimum global id q, the accepted
+ * quantities of that member and the cluster's local size.  w is N doubles. */
+typedef struct {
+  double upsilon;
+  double alpha;
+  int64_t q;
+  int64_t size;
+  int32_t iters;
+  int32_t valid;          /* 0 = empty slot */
+} oica_cluster_record;
+
+/* Merge n records (from all ranks, records[k].w = w + k*N) into the global decision of
+ * reading A6: records whose rows satisfy 1 - |w_a . w_b| <= 1e-6 are one cluster (sizes add,
+ * q = minimum id, its record supplies alpha/upsilon/iters/w); the winner is the cluster of
+ * largest upsilon (ties -> lowest q); near_tie if the runner-up is within 1e-6 relative.
+ * Host pointers; pure function.  Writes the winner index into `records` (*winner) and the
+ * merged size / near-tie flag. */
+oica_status oica_merge_records(const oica_cluster_record* records, const double* w, int32_t n,
+                               int32_t N, int32_t* winner, int64_t* merged_size,
+                               uint8_t* near_tie);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OICA_H_ */

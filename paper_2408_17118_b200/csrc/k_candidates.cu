@@ -1,0 +1,265 @@
+// K1 candidate init, K3 fp64 epilogue, K4 compaction and operand gathers.
+// One warp per candidate row for the fp64 row work (N <= 256 -> <= 8 values per lane).
+#include <cuda_fp16.h>
+
+#include "kernels.cuh"
+
+namespace oica {
+namespace {
+
+constexpr int kMaxV = 8;  // 256 / 32 coordinates per lane
+
+// SplitMix64 finaliser (Steele, Lea, Flood 2014) -- DESIGN.md §2 A7 generator.
+__device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double uniform01(uint64_t seed, uint64_t c) {
+  uint64_t z = splitmix64_mix(seed + (c + 1ull) * 0x9E3779B97F4A7C15ull);
+  return ((double)(z >> 11) + 0.5) * 0x1.0p-53;
+}
+
+// v <- v - E v with E = Wacc^T Wacc: all coefficients w_k . v are
+// taken from the incoming v (one projection, as written in the paper).
+__device__ __forceinline__ void project_warp(double (&v)[kMaxV], const double* __restrict__ Wacc, int k,
+                                             int N, int lane) {
+  double h[kMaxV];
+#pragma unroll
+  for (int u = 0; u < kMaxV; ++u) h[u] = 0.0;
+  for (int r = 0; r < k; ++r) {
+    const double* wr = Wacc + (int64_t)r * N;
+    double c = 0.0;
+#pragma unroll
+    for (int u = 0; u < kMaxV; ++u) {
+      int n = lane + 32 * u;
+      if (n < N) c += wr[n] * v[u];
+    }
+    c = warp_sum(c);
+#pragma unroll
+    for (int u = 0; u < kMaxV; ++u) {
+      int n = lane + 32 * u;
+      if (n < N) h[u] += c * wr[n];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kMaxV; ++u) v[u] -= h[u];
+}
+
+__global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_local, int N,
+                            const double* __restrict__ Wacc, int k, double* __restrict__ W64,
+                            uint8_t* __restrict__ state, uint8_t* __restrict__ keep) {
+  int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (j >= L_local) return;
+  uint64_t l = (uint64_t)(id_base + j);
+  double v[kMaxV];
+#pragma unroll
+  for (int u = 0; u < kMaxV; ++u) {
+    int n = lane + 32 * u;
+    v[u] = 0.0;
+    if (n < N) {
+      // counter c = ((i 2^24 + l) 2^9 + p) 2 + h, p = n / 2  (DESIGN.md §2 A7)
+      uint64_t p = (uint64_t)(n >> 1);
+      uint64_t c0 = ((((uint64_t)i << 24) + l) * 512ull + p) * 2ull;
+      double u0 = uniform01(seed, c0), u1 = uniform01(seed, c0 + 1ull);
+      double rad = sqrt(-2.0 * log(u0));
+      double ang = 2.0 * 3.141592653589793 * u1;
+      v[u] = (n & 1) ? rad * sin(ang) : rad * cos(ang);
+    }
+  }
+  project_warp(v, Wacc, k, N, lane);
+  double ss = 0.0;
+#pragma unroll
+  for (int u = 0; u < kMaxV; ++u) ss += v[u] * v[u];
+  double nrm = sqrt(warp_sum(ss));
+  bool deg = nrm < kDegenerateNorm;                       // A18
+#pragma unroll
+  for (int u = 0; u < kMaxV; ++u) {
+    int n = lane + 32 * u;
+    if (n < N) W64[j * N + n] = deg ? 0.0 : v[u] / nrm;
+  }
+  if (lane == 0) {
+    state[j] = deg ? ST_DEGENERATE : ST_ACTIVE;
+    keep[j] = deg ? 0 : 1;
+  }
+}
+
+// K3: g = sum_s Gp / M - 3 w_old; g <- g - E g; w = g / ||g||;
+// d = 1 - |w . w_old| as 0.5 ||w - s w_old||^2 (A1/A2); converged iff d <= tol.
+__global__ void k_epilogue(const double* __restrict__ Gp, const double* __restrict__ s4p, int S, int64_t cap,
+                           int ldg, const int* __restrict__ act, int L_act, const double* __restrict__ Wacc,
+                           int k, int N, double M, double tol, int t, double* __restrict__ W64,
+                           double* __restrict__ alpha_old, int* __restrict__ iters, uint8_t* __restrict__ state,
+                           uint8_t* __restrict__ keep) {
+  int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int lane = threadIdx.x & 31;
+  if (a >= L_act) return;
+  int l = act[a];
+  double g[kMaxV], wo[kMaxV];
+#pragma unroll
+  for (int u = 0; u < kMaxV; ++u) {
+    int n = lane + 32 * u;
+    double acc = 0.0, w = 0.0;
+    if (n < N) {
+      for (int s = 0; s < S; ++s) acc += Gp[((int64_t)s * cap + a) * ldg + n];   // fixed slot order
+      w = W64[(int64_t)l * N + n];
+    }
+    wo[u] = w;
+    g[u] = (n < N) ? acc / M - 3.0 * w : 0.0;            // PAPER.md:244-245 (eq. (5), A3)
+  }
+  double s4 = 0.0;
+  if (lane == 0)
+    for (int s = 0; s < S; ++s) s4 += s4p[(int64_t)s * cap + a];
+  project_warp(g, Wacc, k, N, lane);
+  double ss = 0.0;
+#pragma unroll
+  for (int u = 0; u < kMaxV; ++u) ss += g[u] * g[u];
+  double nrm = sqrt(warp_sum(ss));
+  bool deg = nrm < kDegenerateNorm;
+  double dot = 0.0;
+#pragma unroll
+  for (int u = 0; u < kMaxV; ++u) {
+    g[u] = deg ? 0.0 : g[u] / nrm;
+    dot += g[u] * wo[u];
+  }
+  dot = warp_sum(dot);
+  double sg = dot < 0.0 ? -1.0 : 1.0;
+  double dd = 0.0;
+#pragma unroll
+  for (int u = 0; u < kMaxV; ++u) {
+    double e = g[u] - sg * wo[u];
+    dd += e * e;
+  }
+  dd = 0.5 * warp_sum(dd);
+  bool conv = !deg && dd <= tol;                          // PAPER.md:249-250 (A2)
+  if (!deg) {
+#pragma unroll
+    for (int u = 0; u < kMaxV; ++u) {
+      int n = lane + 32 * u;
+      if (n < N) W64[(int64_t)l * N + n] = g[u];
+    }
+  }
+  if (lane == 0) {
+    iters[l] = t;
+    alpha_old[l] = s4 / M - 3.0;                          // eq. (2) at w_old (A15)
+    state[l] = deg ? ST_DEGENERATE : (conv ? ST_CONVERGED : ST_ACTIVE);
+    keep[a] = (deg || conv) ? 0 : 1;
+  }
+}
+
+// Single-block, order-preserving compaction (deterministic).
+__global__ void __launch_bounds__(1024) k_compact(const int* __restrict__ act_in, const uint8_t* __restrict__ keep,
+                                                  int L_in, int* __restrict__ act_out, int* __restrict__ Lact_out,
+                                                  int* Lact_host) {
+  __shared__ int scan[1024];
+  int t = threadIdx.x;
+  int per = (L_in + 1023) / 1024;
+  int b = t * per, e = min(L_in, b + per);
+  int cnt = 0;
+  for (int a = b; a < e; ++a) cnt += keep[a] ? 1 : 0;
+  scan[t] = cnt;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    int v = t >= off ? scan[t - off] : 0;
+    __syncthreads();
+    scan[t] += v;
+    __syncthreads();
+  }
+  int pos = scan[t] - cnt;
+  for (int a = b; a < e; ++a)
+    if (keep[a]) act_out[pos++] = act_in ? act_in[a] : a;
+  if (t == 1023) {
+    *Lact_out = scan[1023];
+    if (Lact_host) *(volatile int*)Lact_host = scan[1023];
+  }
+}
+
+__global__ void k_operand_f32(const int* __restrict__ act, const int* __restrict__ Lact, int cap,
+                              const double* __restrict__ W64, int N, int NP, float* __restrict__ W32) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int a = (int)(idx / NP), n = (int)(idx % NP);
+  if (a >= cap || a >= *Lact) return;
+  W32[idx] = n < N ? (float)W64[(int64_t)act[a] * N + n] : 0.f;
+}
+
+// Split fp16 operand: w is scaled by 2^4 (|w| <= 1 -> <= 16) so w_lo stays in the normal range;
+// hi = fp16(2^4 w), lo = fp16((2^4 w - hi) 2^11).  The step kernel undoes both scales.
+__global__ void k_operand_f16x2(const int* __restrict__ act, const int* __restrict__ Lact, int cap,
+                                const double* __restrict__ W64, int N, int NP, __half* __restrict__ Whi,
+                                __half* __restrict__ Wlo) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int a = (int)(idx / NP), n = (int)(idx % NP);
+  if (a >= cap || a >= *Lact) return;
+  double w = n < N ? W64[(int64_t)act[a] * N + n] * 16.0 : 0.0;
+  __half hi = __double2half(w);
+  __half lo = __double2half((w - (double)__half2float(hi)) * 2048.0);
+  Whi[idx] = hi;
+  Wlo[idx] = lo;
+}
+
+__global__ void k_slot_reduce(const double* __restrict__ Gp, const double* __restrict__ s4p, int S, int64_t cap,
+                              int ldg, int L, int N, double* __restrict__ G_out, int ldo, double* __restrict__ s4_out) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int a = (int)(idx / (N + 1)), n = (int)(idx % (N + 1));
+  if (a >= L) return;
+  double acc = 0.0;
+  if (n < N) {
+    for (int s = 0; s < S; ++s) acc += Gp[((int64_t)s * cap + a) * ldg + n];
+    G_out[(int64_t)a * ldo + n] = acc;
+  } else {
+    for (int s = 0; s < S; ++s) acc += s4p[(int64_t)s * cap + a];
+    s4_out[a] = acc;
+  }
+}
+
+}  // namespace
+
+int launch_cand_init(cudaStream_t st, uint64_t seed, int i, int64_t id_base, int64_t L_local, int N,
+                     const double* Wacc, int k, double* W64, uint8_t* state, uint8_t* keep) {
+  int64_t threads = L_local * 32;
+  k_cand_init<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(seed, i, id_base, L_local, N, Wacc, k, W64, state, keep);
+  return 1;
+}
+
+int launch_epilogue(cudaStream_t st, const double* Gp, const double* s4p, int S, int64_t cap, int ldg,
+                    const int* act, int L_act, const double* Wacc, int k, int N, double M, double tol, int t,
+                    double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep) {
+  if (L_act <= 0) return 0;
+  int64_t threads = (int64_t)L_act * 32;
+  k_epilogue<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, act, L_act, Wacc, k, N, M, tol,
+                                                               t, W64, alpha_old, iters, state, keep);
+  return 1;
+}
+
+int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, int L_in, int* act_out, int* Lact_out,
+                   int* Lact_host) {
+  k_compact<<<1, 1024, 0, st>>>(act_in, keep, L_in, act_out, Lact_out, Lact_host);
+  return 1;
+}
+
+int launch_operand_f32(cudaStream_t st, const int* act, const int* Lact, int cap, const double* W64, int N, int NP,
+                       float* W32) {
+  if (cap <= 0) return 0;
+  int64_t tot = (int64_t)cap * NP;
+  k_operand_f32<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(act, Lact, cap, W64, N, NP, W32);
+  return 1;
+}
+
+int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact, int cap, const double* W64, int N, int NP,
+                         __half* Whi, __half* Wlo) {
+  if (cap <= 0) return 0;
+  int64_t tot = (int64_t)cap * NP;
+  k_operand_f16x2<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(act, Lact, cap, W64, N, NP, Whi, Wlo);
+  return 1;
+}
+
+int launch_slot_reduce(cudaStream_t st, const double* Gp, const double* s4p, int S, int64_t cap, int ldg, int L,
+                       int N, double* G_out, int ldo, double* s4_out) {
+  if (L <= 0) return 0;
+  int64_t tot = (int64_t)L * (N + 1);
+  k_slot_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, L, N, G_out, ldo, s4_out);
+  return 1;
+}
+
+}  // namespace oica

@@ -1,0 +1,89 @@
+// Launch wrappers of the liboica kernels (internal).  Every wrapper enqueues on `st` and
+// returns the number of kernels it launched (for the launch counter in oica_stats).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace oica {
+
+// ---- K1: candidate draw + projection + normalisation
+int launch_cand_init(cudaStream_t st, uint64_t seed, int i, int64_t id_base, int64_t L_local, int N,
+                     const double* Wacc, int k, double* W64, uint8_t* state, uint8_t* keep);
+
+// ---- K4: order-preserving compaction of the active set
+// act_in == nullptr means the identity list.  Writes act_out, *Lact_out_dev and *Lact_host.
+int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, int L_in, int* act_out,
+                   int* Lact_out_dev, int* Lact_host);
+
+// Operand rows for the step kernel, gathered in active order from the fp64 master.
+int launch_operand_f32(cudaStream_t st, const int* act, const int* Lact_dev, int cap, const double* W64,
+                       int N, int NP, float* W32);
+// Split-fp16 operand (TC path): hi = fp16(w*2^s), lo = fp16((w*2^s - hi)*2^11), K-major rows.
+int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact_dev, int cap, const double* W64,
+                         int N, int NP, __half* Whi, __half* Wlo);
+
+// ---- K2b: fused GEMM-cube-GEMM on CUDA cores (PAPER.md:243-245 before the -3B term)
+// Gp[s][a][n] (stride ldg = NP), s4p[s][a] over slots s of slot_len samples.
+int launch_step_simt(cudaStream_t st, const float* X, int64_t ld, int64_t M, int N, int NP,
+                     const float* W32, int L_act, int64_t slot_len, int S, int flush,
+                     double* Gp, double* s4p, int64_t cap);
+
+// ---- K3: fp64 epilogue: slot sum, /M - 3w, projection, normalise, convergence
+int launch_epilogue(cudaStream_t st, const double* Gp, const double* s4p, int S, int64_t cap, int ldg,
+                    const int* act, int L_act, const double* Wacc, int k, int N, double M, double tol,
+                    int t, double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep);
+
+// Fixed-order slot sum into G_out (L x ldo) and s4_out (L).
+int launch_slot_reduce(cudaStream_t st, const double* Gp, const double* s4p, int S, int64_t cap, int ldg,
+                       int L, int N, double* G_out, int ldo, double* s4_out);
+
+// ---- K5: device-side argmax, cluster assignment, exact alpha, merge + accept
+struct SelectWork;  // defined in k_select.cu
+struct ComponentRecord {
+  double w_alpha, w_upsilon;
+  int64_t q, cluster_size, n_conv, n_unconv, n_deg, sum_active;
+  int32_t iters, n_iter, status, gaussian, near_tie, n_domain;
+};
+struct RankSummary {
+  oica_cluster_record rec[kMaxClusters];
+  int64_t n_conv, n_unconv, n_deg, sum_active;
+  int32_t n_iter, n_domain;
+};
+
+// Census + refinement: fills summary (per-rank records) and wsum (kMaxClusters x N rows).
+// Exact alpha partial sums are left in s4c (kMaxClusters) for an optional M-shard allreduce.
+int launch_select_local(cudaStream_t st, const double* W64, const double* alpha_old, const uint8_t* state,
+                        const int* iters, int L_local, int64_t id_base, int N, uint32_t flags,
+                        const float* X, int64_t ld, int64_t M_local, int* cluster, int* pc, int* qc,
+                        int* csize, double* ups_max, int* counts, double* part, int nblk, double* s4c);
+int launch_select_finish(cudaStream_t st, const double* W64, const int* iters, const int* counts,
+                         const int* pc, const int* qc, const int* csize, const double* s4c,
+                         int64_t id_base, int N, double M_global, uint32_t flags, int64_t sum_active,
+                         int n_iter, RankSummary* summary, double* wsum);
+// Merge all ranks' summaries (world x RankSummary, world x kMaxClusters x N), append the winner to
+// Wacc row k, write the record.
+int launch_merge_accept(cudaStream_t st, const RankSummary* all, const double* wall, int world, int N,
+                        int i, double M_global, uint32_t flags, double* Wacc, int k, ComponentRecord* rec,
+                        double* w_out);
+
+// ---- fused tensor-core step (k_step_tc.cu)
+struct TcPlan;
+bool tc_supported(int N);
+int tc_np(int N);
+int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
+                   const __half* Wlo, int L_act, int64_t slot_len, int S, int flush, double* Gp,
+                   double* s4p, int64_t cap, int num_sms);
+int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP,
+                         int64_t ldx, __half* Xh);
+
+// ---- boundary: whitening (k_whiten.cu)
+int launch_row_mean(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, double* mean);
+int launch_covariance(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, const double* mean,
+                      double* part, int nsplit, double* C);
+int launch_apply_whitening(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, const double* mean,
+                           const double* V, float* Xw, int64_t ldo);
+
+}  // namespace oica

@@ -1,0 +1,670 @@
+// Host runtime and C-ABI of liboica.so: context, memory planner, per-component driver loop,
+// NCCL exchange, whitening eigensolver.  Kernels live in k_*.cu (launch wrappers in kernels.cuh).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/oica.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "merge.hpp"
+#include "nccl_dl.hpp"
+
+using namespace oica;
+
+namespace {
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t k) {
+    if (k <= n) return;
+    release();
+    if (k == 0) return;
+    OICA_CUDA(cudaMalloc(&p, k * sizeof(T)));
+    n = k;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+// Split-M slot policy: S depends only on M, so per-row results are identical
+// for any GPU count in L-shard mode and any active-set size.
+constexpr int64_t kSlotTarget = 4096;   // samples per slot (lower bound)
+constexpr int kMaxSlots = 128;
+constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
+constexpr int64_t kSlotAlign = 128;
+
+}  // namespace
+
+struct oica_ctx {
+  oica_config cfg{};
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int num_sms = 0;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  // data
+  const float* X = nullptr;
+  DevBuf<float> Xown;
+  int64_t N = 0, NP = 0, M = 0, ld = 0, Mg = 0;
+  int precision = OICA_PREC_FP32;
+  DevBuf<__half> Xh;   // TC operand plane
+  int64_t ldx = 0;
+  bool tc_ready = false;
+  // slots
+  int S = 1;
+  int64_t slot_len = 0;
+  // candidates
+  bool have_cand = false;
+  uint64_t seed = 0;
+  int64_t L = 0, Ll = 0, id_base = 0;
+  DevBuf<double> W64, alpha_old, Gp, s4p, Gsum, s4sum;
+  DevBuf<float> W32;
+  DevBuf<__half> Whi, Wlo;
+  DevBuf<int> act0, act1, iters, Lact_dev;
+  DevBuf<uint8_t> state, keep;
+  int* Lact_host = nullptr;
+  DevBuf<double> Wacc;
+  // selection
+  DevBuf<int> cluster, pc, qc, csize, counts;
+  DevBuf<double> ups_max, part, s4c, wsum, wsum_all, w_out;
+  DevBuf<RankSummary> summary, summary_all;
+  DevBuf<ComponentRecord> rec;
+  int nblk_alpha = 0;
+  bool last_valid = false;
+  // whitening scratch
+  DevBuf<double> wh_mean, wh_part, wh_C, wh_V;
+  // stats
+  oica_stats stats{};
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+
+  int world() const { return cfg.world; }
+  bool mshard() const { return cfg.world > 1 && cfg.shard_mode == OICA_SHARD_M; }
+
+  void count(int n) { stats.kernel_launches += n; }
+  cudaEvent_t event() {
+    if (ev_used == ev.size()) {
+      cudaEvent_t e;
+      OICA_CUDA(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    return ev[ev_used++];
+  }
+  void harvest_events() {
+    OICA_CUDA(cudaStreamSynchronize(st));
+    for (size_t k = 0; k + 1 < ev_used; k += 2) {
+      float ms = 0.f;
+      OICA_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+      stats.step_ms += ms;
+    }
+    ev_used = 0;
+  }
+};
+
+namespace {
+
+oica_status fail(oica_ctx* ctx, oica_status s, const std::string& m) {
+  if (ctx) ctx->err = m;
+  return s;
+}
+
+template <class F>
+oica_status guard(oica_ctx* ctx, F&& f) {
+  try {
+    if (ctx) {
+      ctx->err.clear();
+      OICA_CUDA(cudaSetDevice(ctx->cfg.device));
+    }
+    f();
+    return OICA_OK;
+  } catch (const Error& e) {
+    return fail(ctx, e.status, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, OICA_ERR_OUT_OF_MEMORY, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(ctx, OICA_ERR_CUDA, e.what());
+  }
+}
+
+// Cyclic Jacobi eigensolver for a symmetric N x N matrix (row-major, fp64).
+void jacobi_eigh(std::vector<double>& A, int n, std::vector<double>& d, std::vector<double>& E) {
+  E.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) E[(size_t)i * n + i] = 1.0;
+  auto a = [&](int i, int j) -> double& { return A[(size_t)i * n + j]; };
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        tot += a(i, j) * a(i, j);
+        if (i != j) off += a(i, j) * a(i, j);
+      }
+    if (off <= 1e-30 * tot) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        double apq = a(p, q);
+        if (std::fabs(apq) < 1e-300) continue;
+        double app = a(p, p), aqq = a(q, q);
+        double theta = (aqq - app) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < n; ++k) {
+          double akp = a(k, p), akq = a(k, q);
+          a(k, p) = c * akp - s * akq;
+          a(k, q) = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {
+          double apk = a(p, k), aqk = a(q, k);
+          a(p, k) = c * apk - s * aqk;
+          a(q, k) = s * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          double ekp = E[(size_t)k * n + p], ekq = E[(size_t)k * n + q];
+          E[(size_t)k * n + p] = c * ekp - s * ekq;
+          E[(size_t)k * n + q] = s * ekp + c * ekq;
+        }
+      }
+  }
+  d.resize(n);
+  for (int i = 0; i < n; ++i) d[i] = a(i, i);
+}
+
+void plan_slots(oica_ctx* c) {
+  int64_t S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, c->Mg / kSlotTarget));
+  // slot length is a function of the GLOBAL M only (determinism across GPU counts)
+  int64_t len = round_up(ceil_div(c->Mg, S), kSlotAlign);
+  c->slot_len = len;
+  c->S = (int)ceil_div(c->M, len);
+  if (c->S < 1) c->S = 1;
+}
+
+void ensure_candidate_buffers(oica_ctx* c) {
+  size_t Ll = (size_t)c->Ll, N = (size_t)c->N, NP = (size_t)c->NP;
+  c->W64.ensure(Ll * N);
+  c->alpha_old.ensure(Ll);
+  c->iters.ensure(Ll);
+  c->state.ensure(Ll);
+  c->keep.ensure(Ll);
+  c->act0.ensure(Ll);
+  c->act1.ensure(Ll);
+  c->Lact_dev.ensure(1);
+  c->Gp.ensure((size_t)c->S * Ll * NP);
+  c->s4p.ensure((size_t)c->S * Ll);
+  if (c->precision == OICA_PREC_TC) {
+    c->Whi.ensure(Ll * NP);
+    c->Wlo.ensure(Ll * NP);
+  } else {
+    c->W32.ensure(Ll * NP);
+  }
+  if (c->mshard()) {
+    c->Gsum.ensure(Ll * NP);
+    c->s4sum.ensure(Ll);
+  }
+  c->cluster.ensure(Ll);
+  c->pc.ensure(kMaxClusters);
+  c->qc.ensure(kMaxClusters);
+  c->csize.ensure(kMaxClusters);
+  c->counts.ensure(4);
+  c->ups_max.ensure(1);
+  c->nblk_alpha = (int)std::max<int64_t>(1, std::min<int64_t>(4 * c->num_sms, ceil_div(c->M, 4096)));
+  c->part.ensure((size_t)kMaxClusters * c->nblk_alpha);
+  c->s4c.ensure(kMaxClusters);
+  c->wsum.ensure(kMaxClusters * N);
+  c->wsum_all.ensure((size_t)c->cfg.world * kMaxClusters * N);
+  c->summary.ensure(1);
+  c->summary_all.ensure((size_t)c->cfg.world);
+  c->rec.ensure(1);
+  c->w_out.ensure(N);
+  c->Wacc.ensure(N * N);
+}
+
+// Build the step-kernel operand rows for the active list `act` (count in Lact_dev, <= cap).
+void build_operand(oica_ctx* c, const int* act, int cap) {
+  if (c->precision == OICA_PREC_TC)
+    c->count(launch_operand_f16x2(c->st, act, c->Lact_dev.p, cap, c->W64.p, (int)c->N, (int)c->NP, c->Whi.p, c->Wlo.p));
+  else
+    c->count(launch_operand_f32(c->st, act, c->Lact_dev.p, cap, c->W64.p, (int)c->N, (int)c->NP, c->W32.p));
+}
+
+// One fused contraction over the active rows (positions 0..L_act-1) into the slots.
+void run_step(oica_ctx* c, int L_act, bool timed) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timed) {
+    e0 = c->event();
+    OICA_CUDA(cudaEventRecord(e0, c->st));
+  }
+  int n;
+  if (c->precision == OICA_PREC_TC)
+    n = launch_step_tc(c->st, c->Xh.p, c->ldx, c->M, (int)c->NP, c->Whi.p, c->Wlo.p, L_act, c->slot_len, c->S, kFlush,
+                       c->Gp.p, c->s4p.p, c->Ll, c->num_sms);
+  else
+    n = launch_step_simt(c->st, c->X, c->ld, c->M, (int)c->N, (int)c->NP, c->W32.p, L_act, c->slot_len, c->S, kFlush,
+                         c->Gp.p, c->s4p.p, c->Ll);
+  OICA_CUDA(cudaGetLastError());
+  c->count(n);
+  c->stats.step_launches += n;
+  c->stats.step_flops += (double)L_act * (4.0 * (double)c->N * (double)c->Mg + 3.0 * (double)c->Mg) *
+                         ((double)c->M / (double)c->Mg);
+  if (timed) {
+    e1 = c->event();
+    OICA_CUDA(cudaEventRecord(e1, c->st));
+  }
+}
+
+void check_launch() { OICA_CUDA(cudaGetLastError()); }
+
+void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t flags, const double* W_prefix,
+                  int32_t k_prefix, oica_result* out) {
+  OICA_REQUIRE(c->X, OICA_ERR_STATE, "oica_set_data has not been called");
+  OICA_REQUIRE(c->have_cand, OICA_ERR_STATE, "oica_init_candidates has not been called");
+  OICA_REQUIRE(out, OICA_ERR_INVALID_ARGUMENT, "out is NULL");
+  OICA_REQUIRE(K >= 1, OICA_ERR_INVALID_ARGUMENT, "max_iter must be >= 1");
+  OICA_REQUIRE(tol > 0, OICA_ERR_INVALID_ARGUMENT, "tol must be > 0");
+  OICA_REQUIRE(k_prefix >= 0 && k_prefix < N_out && N_out <= c->N, OICA_ERR_INVALID_ARGUMENT,
+               "need 0 <= k_prefix < N_out <= N");
+  OICA_REQUIRE(k_prefix == 0 || W_prefix, OICA_ERR_INVALID_ARGUMENT, "W_prefix is NULL");
+  const int N = (int)c->N;
+  cudaStream_t st = c->st;
+  if (k_prefix > 0)
+    OICA_CUDA(cudaMemcpyAsync(c->Wacc.p, W_prefix, sizeof(double) * k_prefix * N, cudaMemcpyHostToDevice, st));
+  out->n_extracted = k_prefix;
+  out->stopped = 0;
+  std::vector<double> w_host(N);
+  ComponentRecord rec_h{};
+  for (int k = k_prefix; k < N_out; ++k) {
+    const int i = k + 1;  // 1-based component index
+    // a1: fresh candidates for this component (A8)
+    c->count(launch_cand_init(st, c->seed, i, c->id_base, c->Ll, N, c->Wacc.p, k, c->W64.p, c->state.p, c->keep.p));
+    c->count(launch_compact(st, nullptr, c->keep.p, (int)c->Ll, c->act0.p, c->Lact_dev.p, c->Lact_host));
+    OICA_CUDA(cudaStreamSynchronize(st));
+    int L_act = *(volatile int*)c->Lact_host;
+    int* act = c->act0.p;
+    int* act_next = c->act1.p;
+    build_operand(c, act, L_act);
+    int t = 0;
+    int64_t sum_active = 0;
+    // a2-a6: the do-while of PAPER.md:241-256
+    while (L_act > 0) {
+      ++t;
+      sum_active += L_act;
+      c->stats.iterations += 1;
+      c->stats.sum_active += L_act;
+      run_step(c, L_act, true);
+      const double* G = c->Gp.p;
+      const double* s4 = c->s4p.p;
+      int S = c->S;
+      int64_t cap = c->Ll;
+      if (c->mshard()) {  // one fp64 allreduce of (G, s4) per iteration
+        c->count(launch_slot_reduce(st, c->Gp.p, c->s4p.p, c->S, c->Ll, (int)c->NP, L_act, N, c->Gsum.p, (int)c->NP,
+                                    c->s4sum.p));
+        auto& nc = Nccl::get();
+        OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_act * c->NP, ncclFloat64, ncclSum, c->comm, st));
+        OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_act, ncclFloat64, ncclSum, c->comm, st));
+        G = c->Gsum.p;
+        s4 = c->s4sum.p;
+        S = 1;
+        cap = c->Ll;
+      }
+      c->count(launch_epilogue(st, G, s4, S, cap, (int)c->NP, act, L_act, c->Wacc.p, k, N, (double)c->Mg, tol, t,
+                               c->W64.p, c->alpha_old.p, c->iters.p, c->state.p, c->keep.p));
+      c->count(launch_compact(st, act, c->keep.p, L_act, act_next, c->Lact_dev.p, c->Lact_host));
+      std::swap(act, act_next);
+      if (t < K) build_operand(c, act, L_act);
+      check_launch();
+      OICA_CUDA(cudaStreamSynchronize(st));
+      L_act = *(volatile int*)c->Lact_host;
+      if (t >= K) break;  // ... while t < K and B non-empty (A19)
+    }
+    // a7: selection and accept
+    c->count(launch_select_local(st, c->W64.p, c->alpha_old.p, c->state.p, c->iters.p, (int)c->Ll, c->id_base, N,
+                                 flags, c->X, c->ld, c->M, c->cluster.p, c->pc.p, c->qc.p, c->csize.p, c->ups_max.p,
+                                 c->counts.p, c->part.p, c->nblk_alpha, c->s4c.p));
+    if (c->mshard())
+      OICA_NCCL(Nccl::get().AllReduce(c->s4c.p, c->s4c.p, kMaxClusters, ncclFloat64, ncclSum, c->comm, st));
+    c->count(launch_select_finish(st, c->W64.p, c->iters.p, c->counts.p, c->pc.p, c->qc.p, c->csize.p, c->s4c.p,
+                                  c->id_base, N, (double)c->Mg, flags, sum_active, t, c->summary.p, c->wsum.p));
+    const RankSummary* all = c->summary.p;
+    const double* wall = c->wsum.p;
+    int world = 1;
+    if (c->world() > 1 && !c->mshard()) {  // L-shard: one exchange per component (C1)
+      auto& nc = Nccl::get();
+      OICA_NCCL(nc.AllGather(c->summary.p, c->summary_all.p, sizeof(RankSummary), ncclUint8, c->comm, st));
+      OICA_NCCL(nc.AllGather(c->wsum.p, c->wsum_all.p, (size_t)kMaxClusters * N, ncclFloat64, c->comm, st));
+      all = c->summary_all.p;
+      wall = c->wsum_all.p;
+      world = c->world();
+    }
+    c->count(launch_merge_accept(st, all, wall, world, N, i, (double)c->Mg, flags, c->Wacc.p, k, c->rec.p, c->w_out.p));
+    check_launch();
+    OICA_CUDA(cudaMemcpyAsync(&rec_h, c->rec.p, sizeof(ComponentRecord), cudaMemcpyDeviceToHost, st));
+    OICA_CUDA(cudaMemcpyAsync(w_host.data(), c->w_out.p, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    c->harvest_events();
+    c->last_valid = true;
+    if (rec_h.status != OICA_OK)
+      throw Error((oica_status)rec_h.status,
+                  rec_h.status == OICA_ERR_ALL_CANDIDATES_DEGENERATE ? "all candidates degenerate (A18)"
+                                                                     : "no eligible candidate with alpha > -2 (A13)");
+    bool stop = (flags & OICA_STOP_ON_GAUSSIANITY) && rec_h.gaussian;
+    if (out->W && !stop) std::memcpy(out->W + (size_t)k * N, w_host.data(), sizeof(double) * N);
+    if (out->alpha) out->alpha[k] = rec_h.w_alpha;
+    if (out->upsilon) out->upsilon[k] = rec_h.w_upsilon;
+    if (out->index) out->index[k] = rec_h.q;
+    if (out->iters) out->iters[k] = rec_h.iters;
+    if (out->n_iter) out->n_iter[k] = rec_h.n_iter;
+    if (out->cluster_size) out->cluster_size[k] = (int32_t)rec_h.cluster_size;
+    if (out->n_converged) out->n_converged[k] = (int32_t)rec_h.n_conv;
+    if (out->n_unconverged) out->n_unconverged[k] = (int32_t)rec_h.n_unconv;
+    if (out->n_degenerate) out->n_degenerate[k] = (int32_t)rec_h.n_deg;
+    if (out->sum_active) out->sum_active[k] = rec_h.sum_active;
+    if (out->gaussian_flag) out->gaussian_flag[k] = (uint8_t)rec_h.gaussian;
+    if (out->near_tie) out->near_tie[k] = (uint8_t)rec_h.near_tie;
+    if (stop) {
+      out->stopped = 1;
+      break;
+    }
+    out->n_extracted = k + 1;
+  }
+}
+
+void set_data_impl(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int64_t ld, int64_t M_global) {
+  OICA_REQUIRE(Xw, OICA_ERR_INVALID_ARGUMENT, "Xw is NULL");
+  OICA_REQUIRE(N >= 1 && N <= 256, OICA_ERR_INVALID_ARGUMENT, "need 1 <= N <= 256");
+  OICA_REQUIRE(M_local >= 1 && ld >= M_local, OICA_ERR_INVALID_ARGUMENT, "need M_local >= 1 and ld >= M_local");
+  OICA_REQUIRE(M_global > N, OICA_ERR_INVALID_ARGUMENT, "need M_global > N");
+  OICA_REQUIRE(c->mshard() ? M_global >= M_local : M_global == M_local, OICA_ERR_DIMENSION_MISMATCH,
+               "M_global must equal M_local unless shard_mode = M");
+  if (c->have_cand && N != c->N) c->have_cand = false;
+  c->X = Xw;
+  c->N = N;
+  c->M = M_local;
+  c->ld = ld;
+  c->Mg = M_global;
+  int req = c->cfg.precision;
+  bool tc = (req == OICA_PREC_TC || req == OICA_PREC_AUTO) && tc_supported((int)N);
+  OICA_REQUIRE(!(req == OICA_PREC_TC && !tc), OICA_ERR_INVALID_ARGUMENT, "tensor-core step unsupported for this N");
+  c->precision = tc ? OICA_PREC_TC : OICA_PREC_FP32;
+  c->NP = tc ? tc_np((int)N) : (N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256);
+  plan_slots(c);
+  c->stats.precision = c->precision;
+  c->stats.slots = c->S;
+  if (tc) {
+    c->ldx = round_up(M_local, 128);
+    c->Xh.ensure((size_t)c->NP * c->ldx);
+    c->count(launch_x_prepare_f16(c->st, Xw, ld, (int)N, M_local, (int)c->NP, c->ldx, c->Xh.p));
+    check_launch();
+  }
+  if (c->have_cand) ensure_candidate_buffers(c);
+}
+
+}  // namespace
+
+// ============================== C ABI ======================================================
+extern "C" {
+
+const char* oica_status_string(oica_status s) {
+  switch (s) {
+    case OICA_OK: return "OICA_OK";
+    case OICA_ERR_INVALID_ARGUMENT: return "OICA_ERR_INVALID_ARGUMENT";
+    case OICA_ERR_DIMENSION_MISMATCH: return "OICA_ERR_DIMENSION_MISMATCH";
+    case OICA_ERR_RANK_DEFICIENT: return "OICA_ERR_RANK_DEFICIENT";
+    case OICA_ERR_ALL_CANDIDATES_DEGENERATE: return "OICA_ERR_ALL_CANDIDATES_DEGENERATE";
+    case OICA_ERR_DOMAIN: return "OICA_ERR_DOMAIN";
+    case OICA_ERR_STATE: return "OICA_ERR_STATE";
+    case OICA_ERR_UNSUPPORTED_DEVICE: return "OICA_ERR_UNSUPPORTED_DEVICE";
+    case OICA_ERR_OUT_OF_MEMORY: return "OICA_ERR_OUT_OF_MEMORY";
+    case OICA_ERR_CUDA: return "OICA_ERR_CUDA";
+    case OICA_ERR_NCCL: return "OICA_ERR_NCCL";
+  }
+  return "OICA_UNKNOWN_STATUS";
+}
+
+const char* oica_last_error(const oica_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+oica_status oica_nccl_unique_id(void* out) {
+  if (!out) return OICA_ERR_INVALID_ARGUMENT;
+  try {
+    ncclUniqueId id;
+    OICA_NCCL(Nccl::get().GetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+    return OICA_OK;
+  } catch (const Error& e) {
+    return e.status;
+  }
+}
+
+oica_status oica_create(const oica_config* cfg, oica_ctx** out) {
+  if (!cfg || !out) return OICA_ERR_INVALID_ARGUMENT;
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world || cfg->world > 64) return OICA_ERR_INVALID_ARGUMENT;
+  if (cfg->world > 1 && !cfg->nccl_unique_id) return OICA_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  oica_ctx* c = new (std::nothrow) oica_ctx();
+  if (!c) return OICA_ERR_OUT_OF_MEMORY;
+  c->cfg = *cfg;
+  oica_status s = guard(c, [&] {
+    cudaDeviceProp prop;
+    OICA_CUDA(cudaGetDeviceProperties(&prop, cfg->device));
+    OICA_REQUIRE(prop.major == 10 && prop.minor == 0, OICA_ERR_UNSUPPORTED_DEVICE,
+                 std::string("liboica is built for sm_100a (B200); device is ") + prop.name);
+    c->num_sms = prop.multiProcessorCount;
+    if (cfg->stream) {
+      c->st = (cudaStream_t)cfg->stream;
+    } else {
+      OICA_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    OICA_CUDA(cudaHostAlloc((void**)&c->Lact_host, sizeof(int), cudaHostAllocMapped));
+    if (cfg->world > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+      OICA_NCCL(Nccl::get().CommInitRank(&c->comm, cfg->world, id, cfg->rank));
+    }
+  });
+  if (s != OICA_OK) {
+    oica_destroy(c);
+    return s;
+  }
+  *out = c;
+  return OICA_OK;
+}
+
+oica_status oica_destroy(oica_ctx* c) {
+  if (!c) return OICA_OK;
+  cudaSetDevice(c->cfg.device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  if (c->comm) Nccl::get().CommDestroy(c->comm);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->Lact_host) cudaFreeHost(c->Lact_host);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  delete c;
+  return OICA_OK;
+}
+
+oica_status oica_whiten(oica_ctx* c, const float* X, int64_t N, int64_t M, int64_t ld, double eig_floor, float* Xw,
+                        int64_t ld_out, double* mean_out, double* V_out, double* eig_out) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    OICA_REQUIRE(X && Xw, OICA_ERR_INVALID_ARGUMENT, "X / Xw is NULL");
+    OICA_REQUIRE(N >= 1 && N <= 256 && M > N && ld >= M && ld_out >= M, OICA_ERR_INVALID_ARGUMENT,
+                 "need 1 <= N <= 256, M > N, ld >= M, ld_out >= M");
+    OICA_REQUIRE(eig_floor >= 0, OICA_ERR_INVALID_ARGUMENT, "eig_floor < 0");
+    int n = (int)N;
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, M / 8192));
+    c->wh_mean.ensure(n);
+    c->wh_part.ensure((size_t)nsplit * n * n);
+    c->wh_C.ensure((size_t)n * n);
+    c->wh_V.ensure((size_t)n * n);
+    c->count(launch_row_mean(c->st, X, ld, n, M, c->wh_mean.p));
+    c->count(launch_covariance(c->st, X, ld, n, M, c->wh_mean.p, c->wh_part.p, nsplit, c->wh_C.p));
+    check_launch();
+    std::vector<double> C((size_t)n * n), mean(n);
+    OICA_CUDA(cudaMemcpyAsync(C.data(), c->wh_C.p, sizeof(double) * n * n, cudaMemcpyDeviceToHost, c->st));
+    OICA_CUDA(cudaMemcpyAsync(mean.data(), c->wh_mean.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->st));
+    OICA_CUDA(cudaStreamSynchronize(c->st));
+    for (int i = 0; i < n; ++i)  // symmetrise
+      for (int j = i + 1; j < n; ++j) C[(size_t)i * n + j] = C[(size_t)j * n + i] = 0.5 * (C[(size_t)i * n + j] + C[(size_t)j * n + i]);
+    std::vector<double> d, E;
+    jacobi_eigh(C, n, d, E);
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return d[a] > d[b]; });
+    double dmax = d[order[0]], dmin = d[order[n - 1]];
+    OICA_REQUIRE(dmin > 0 && dmin >= eig_floor * dmax, OICA_ERR_RANK_DEFICIENT,
+                 "covariance eigenvalue below eig_floor * max (A11)");
+    std::vector<double> V((size_t)n * n), ev(n);
+    for (int r = 0; r < n; ++r) {
+      int k = order[r];
+      int jm = 0;
+      double am = -1;
+      for (int j = 0; j < n; ++j)
+        if (std::fabs(E[(size_t)j * n + k]) > am) { am = std::fabs(E[(size_t)j * n + k]); jm = j; }
+      double sg = E[(size_t)jm * n + k] < 0 ? -1.0 : 1.0;   // largest-|entry| positive
+      double sc = sg / std::sqrt(d[k]);
+      for (int j = 0; j < n; ++j) V[(size_t)r * n + j] = sc * E[(size_t)j * n + k];   // V = D^-1/2 E^T
+      ev[r] = d[k];
+    }
+    OICA_CUDA(cudaMemcpyAsync(c->wh_V.p, V.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, c->st));
+    c->count(launch_apply_whitening(c->st, X, ld, n, M, c->wh_mean.p, c->wh_V.p, Xw, ld_out));
+    check_launch();
+    OICA_CUDA(cudaStreamSynchronize(c->st));
+    if (mean_out) std::memcpy(mean_out, mean.data(), sizeof(double) * n);
+    if (V_out) std::memcpy(V_out, V.data(), sizeof(double) * n * n);
+    if (eig_out) std::memcpy(eig_out, ev.data(), sizeof(double) * n);
+  });
+}
+
+oica_status oica_set_data(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int64_t ld, int64_t M_global) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] { set_data_impl(c, Xw, N, M_local, ld, M_global); });
+}
+
+oica_status oica_set_data_host(oica_ctx* c, const float* Xh, int64_t N, int64_t M_local, int64_t ld, int64_t M_global) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    OICA_REQUIRE(Xh && N >= 1 && M_local >= 1 && ld >= M_local, OICA_ERR_INVALID_ARGUMENT, "bad host data");
+    c->Xown.ensure((size_t)N * M_local);
+    OICA_CUDA(cudaMemcpy2DAsync(c->Xown.p, sizeof(float) * M_local, Xh, sizeof(float) * ld, sizeof(float) * M_local,
+                                (size_t)N, cudaMemcpyHostToDevice, c->st));
+    set_data_impl(c, c->Xown.p, N, M_local, M_local, M_global);
+  });
+}
+
+oica_status oica_init_candidates(oica_ctx* c, uint64_t seed, int64_t L) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    OICA_REQUIRE(c->X, OICA_ERR_STATE, "oica_set_data has not been called");
+    OICA_REQUIRE(L >= 1 && L < (1 << 24), OICA_ERR_INVALID_ARGUMENT, "need 1 <= L < 2^24");
+    int w = c->mshard() ? 1 : c->cfg.world, r = c->mshard() ? 0 : c->cfg.rank;
+    c->seed = seed;
+    c->L = L;
+    c->id_base = L * r / w;
+    c->Ll = L * (r + 1) / w - c->id_base;
+    OICA_REQUIRE(c->Ll >= 1, OICA_ERR_INVALID_ARGUMENT, "fewer candidates than ranks");
+    ensure_candidate_buffers(c);
+    c->have_cand = true;
+    c->last_valid = false;
+  });
+}
+
+oica_status oica_extract_components(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t flags,
+                                    const double* W_prefix, int32_t k_prefix, oica_result* out) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] { extract_impl(c, N_out, K, tol, flags, W_prefix, k_prefix, out); });
+}
+
+oica_status oica_fixed_point_step(oica_ctx* c, const double* W_dev, int64_t L, double* G_dev, double* s4_dev) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    OICA_REQUIRE(c->X && c->have_cand, OICA_ERR_STATE, "set_data and init_candidates first");
+    OICA_REQUIRE(W_dev && G_dev && s4_dev && L >= 1 && L <= c->Ll, OICA_ERR_INVALID_ARGUMENT, "bad arguments");
+    // stage caller rows through the fp64 master (identity active list)
+    OICA_CUDA(cudaMemcpyAsync(c->W64.p, W_dev, sizeof(double) * L * c->N, cudaMemcpyDeviceToDevice, c->st));
+    std::vector<uint8_t> ones((size_t)L, 1);
+    OICA_CUDA(cudaMemcpyAsync(c->keep.p, ones.data(), L, cudaMemcpyHostToDevice, c->st));
+    c->count(launch_compact(c->st, nullptr, c->keep.p, (int)L, c->act0.p, c->Lact_dev.p, nullptr));
+    build_operand(c, c->act0.p, (int)L);
+    run_step(c, (int)L, true);
+    c->count(launch_slot_reduce(c->st, c->Gp.p, c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L, (int)c->N, G_dev,
+                                (int)c->N, s4_dev));
+    check_launch();
+    c->harvest_events();
+  });
+}
+
+oica_status oica_draw_candidates(oica_ctx* c, int32_t i, const double* W_acc, int32_t k, double* W_dev) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    OICA_REQUIRE(c->have_cand, OICA_ERR_STATE, "init_candidates first");
+    OICA_REQUIRE(i >= 1 && k >= 0 && k < c->N && (k == 0 || W_acc) && W_dev, OICA_ERR_INVALID_ARGUMENT,
+                 "bad arguments");
+    if (k > 0)
+      OICA_CUDA(cudaMemcpyAsync(c->Wacc.p, W_acc, sizeof(double) * k * c->N, cudaMemcpyHostToDevice, c->st));
+    c->count(launch_cand_init(c->st, c->seed, i, c->id_base, c->Ll, (int)c->N, c->Wacc.p, k, W_dev, c->state.p,
+                              c->keep.p));
+    check_launch();
+    OICA_CUDA(cudaStreamSynchronize(c->st));
+    c->last_valid = false;
+  });
+}
+
+oica_status oica_get_candidates(oica_ctx* c, double* W, double* alpha, int32_t* iters, uint8_t* state, int64_t* L_local,
+                                int64_t* id_base) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    OICA_REQUIRE(c->have_cand, OICA_ERR_STATE, "init_candidates first");
+    if (L_local) *L_local = c->Ll;
+    if (id_base) *id_base = c->id_base;
+    if (!(W || alpha || iters || state)) return;
+    OICA_REQUIRE(c->last_valid, OICA_ERR_STATE, "no extracted component yet");
+    if (W) OICA_CUDA(cudaMemcpyAsync(W, c->W64.p, sizeof(double) * c->Ll * c->N, cudaMemcpyDeviceToHost, c->st));
+    if (alpha) OICA_CUDA(cudaMemcpyAsync(alpha, c->alpha_old.p, sizeof(double) * c->Ll, cudaMemcpyDeviceToHost, c->st));
+    if (iters) OICA_CUDA(cudaMemcpyAsync(iters, c->iters.p, sizeof(int32_t) * c->Ll, cudaMemcpyDeviceToHost, c->st));
+    if (state) OICA_CUDA(cudaMemcpyAsync(state, c->state.p, c->Ll, cudaMemcpyDeviceToHost, c->st));
+    OICA_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+oica_status oica_get_stats(oica_ctx* c, oica_stats* out) {
+  if (!c || !out) return OICA_ERR_INVALID_ARGUMENT;
+  *out = c->stats;
+  return OICA_OK;
+}
+
+oica_status oica_reset_stats(oica_ctx* c) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  int p = c->stats.precision, s = c->stats.slots;
+  c->stats = oica_stats{};
+  c->stats.precision = p;
+  c->stats.slots = s;
+  return OICA_OK;
+}
+
+oica_status oica_synchronize(oica_ctx* c) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] { OICA_CUDA(cudaStreamSynchronize(c->st)); });
+}
+
+oica_status oica_merge_records(const oica_cluster_record* records, const double* w, int32_t n, int32_t N,
+                               int32_t* winner, int64_t* merged_size, uint8_t* near_tie) {
+  if (!records || !w || n < 0 || N < 1 || !winner) return OICA_ERR_INVALID_ARGUMENT;
+  std::vector<int32_t> group((size_t)std::max(n, 1));
+  MergeOut m = merge_records(records, w, n, N, group.data(), false, kClusterDelta, kNearTieRel);
+  *winner = m.winner;
+  if (merged_size) *merged_size = m.merged_size;
+  if (near_tie) *near_tie = m.near_tie;
+  return m.winner >= 0 ? OICA_OK : OICA_ERR_DOMAIN;
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol include/oica.h declares,
+maps statuses, refuses non-sm_100 / absent devices, and its host-only selection merge
+(reading A6) decides as the oracle's selection rule does."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2408_17118_b200 import oica
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "oica.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(oica_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = oica.lib()
+    names = declared_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(oica.SIGNATURES), set(names) ^ set(oica.SIGNATURES)
+
+
+def test_library_is_sm100a_binary():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", oica.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings():
+    for k, name in enumerate(oica.STATUS):
+        assert oica.lib().oica_status_string(k).decode() == "OICA_" + ("OK" if k == 0 else "ERR_" + name)
+
+
+def test_create_without_device_fails_cleanly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    with pytest.raises(oica.OicaError) as e:
+        oica.Context(device=0)
+    assert e.value.name in ("CUDA", "UNSUPPORTED_DEVICE")
+
+
+def _unit(v):
+    v = np.asarray(v, dtype=np.float64)
+    return v / np.linalg.norm(v)
+
+
+def test_merge_records_cluster_rule():
+    a, b = _unit([1, 2, 0.5]), _unit([-1, 0.3, 2])
+    W = np.array([a, b, -a, a + 1e-6 * b, b])
+    W /= np.linalg.norm(W, axis=1, keepdims=True)
+    recs = [dict(upsilon=1.0, alpha=1.5, q=30, size=5),
+            dict(upsilon=0.9, alpha=1.2, q=3, size=2),
+            dict(upsilon=1.0 + 1e-9, alpha=1.5, q=12, size=7),
+            dict(upsilon=1.0 - 1e-9, alpha=1.5, q=40, size=1),
+            dict(upsilon=0.9, alpha=1.2, q=8, size=4, valid=0)]
+    r = oica.merge_records(recs, W)
+    assert r["status"] == 0 and r["winner"] == 2 and r["size"] == 13 and not r["near_tie"]
+    # a tie between two different fixed points -> near_tie, lowest q wins
+    recs[1]["upsilon"] = 1.0 + 1e-9
+    r = oica.merge_records(recs, W)
+    assert r["near_tie"] and r["winner"] == 1
+    assert oica.merge_records([dict(upsilon=1, alpha=1, q=0, size=1, valid=0)], W[:1])["status"] != 0

@@ -1,0 +1,228 @@
+"""GPU parity: liboica (through the C ABI) against the float64 oracle on identical seeded inputs.
+
+Gates (BASELINE.json north_star): identical selected candidate indices, per-component
+|cos| >= 0.9999, objective (sum y^4 / M) relative error <= 1e-4.  Inputs: datagen sources,
+ORACLE whitening (fp64) cast to fp32; the oracle consumes the same fp32 values upcast.
+"""
+import functools
+
+import numpy as np
+import pytest
+import torch
+
+import datagen
+from datagen import Config
+from oracle import ordering, rng, whiten
+from paper_2408_17118_b200 import oica
+
+pytestmark = pytest.mark.gpu
+
+PRECISIONS = [oica.PREC_FP32, oica.PREC_AUTO]
+
+
+@functools.lru_cache(maxsize=None)
+def prepared(name, seed=None):
+    cfg = datagen.PARITY[name] if name in datagen.PARITY else datagen.get(name)
+    ds = datagen.make_dataset(cfg, seed=seed)
+    Xw, _, V, _ = whiten.whiten(ds.X.numpy())
+    X32 = np.ascontiguousarray(Xw.astype(np.float32))
+    return cfg, X32, X32.astype(np.float64)
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_run(name, N_out=None, flags=0):
+    cfg, _, X64 = prepared(name)
+    W, res, st = ordering.extract(X64, cfg.L, cfg.K, cfg.tol, N_out or cfg.N_out, cfg.cand_seed,
+                                  include_unconverged=bool(flags & oica.INCLUDE_UNCONVERGED), keep_candidates=True)
+    return W, res, st
+
+
+def ctx_for(name, precision=oica.PREC_AUTO):
+    cfg, X32, _ = prepared(name)
+    ctx = oica.Context(0, precision)
+    Xd = torch.from_numpy(X32).cuda()
+    ctx.set_data(Xd)
+    ctx.init_candidates(cfg.cand_seed, cfg.L)
+    return cfg, ctx
+
+
+def test_candidate_generator_parity():
+    cfg, ctx = ctx_for("p_ragged")
+    W_or, _, _ = oracle_run("p_ragged")
+    for i, k in [(1, 0), (3, 2), (5, 4)]:
+        out = torch.zeros(cfg.L, cfg.N, dtype=torch.float64, device="cuda")
+        ctx.draw_candidates(i, W_or[:k] if k else None, out)
+        R = rng.candidates(cfg.cand_seed, i, np.arange(cfg.L), cfg.N)
+        P = ordering.project(R, W_or[:k])
+        P /= np.linalg.norm(P, axis=1, keepdims=True)
+        assert np.abs(out.cpu().numpy() - P).max() < 1e-13
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("name", ["p_ragged", "p_n40", "p_cfg1_reducedL"])
+def test_fixed_point_step_parity(name, precision):
+    cfg, ctx = ctx_for(name, precision)
+    _, X32, X64 = prepared(name)
+    Lt = min(cfg.L, 150)
+    W = rng.candidates(7, 1, np.arange(Lt), cfg.N)
+    W /= np.linalg.norm(W, axis=1, keepdims=True)
+    Wd = torch.from_numpy(W).cuda()
+    G = torch.zeros(Lt, cfg.N, dtype=torch.float64, device="cuda")
+    s4 = torch.zeros(Lt, dtype=torch.float64, device="cuda")
+    ctx.fixed_point_step(Wd, G, s4)
+    Gref, s4ref = ordering.batch_step(W, X64)
+    M = X64.shape[1]
+    Graw = (Gref + 3.0 * W) * M
+    s4raw = s4ref
+    # floating-point error bound scale: sum_m |y^3| |x| per element, sum_m y^4 per row
+    Y = W @ X64
+    bound = (np.abs(Y) ** 3) @ np.abs(X64).T
+    tolr = 2e-5 if ctx.stats()["precision"] == oica.PREC_FP32 else 4e-3
+    assert np.all(np.abs(G.cpu().numpy() - Graw) <= tolr * bound + 1e-9)
+    assert np.allclose(s4.cpu().numpy(), s4raw, rtol=tolr * 10)
+
+
+def test_step_is_row_independent_and_deterministic():
+    cfg, ctx = ctx_for("p_n40")
+    L = 200
+    W = rng.candidates(9, 1, np.arange(L), cfg.N)
+    W /= np.linalg.norm(W, axis=1, keepdims=True)
+    perm = np.random.default_rng(0).permutation(L)
+    outs = []
+    for Wm in (W, W[perm], W[:37]):
+        Wd = torch.from_numpy(np.ascontiguousarray(Wm)).cuda()
+        G = torch.zeros(len(Wm), cfg.N, dtype=torch.float64, device="cuda")
+        s4 = torch.zeros(len(Wm), dtype=torch.float64, device="cuda")
+        ctx.fixed_point_step(Wd, G, s4)
+        outs.append((G.cpu().numpy(), s4.cpu().numpy()))
+    assert np.array_equal(outs[0][0][perm], outs[1][0]) and np.array_equal(outs[0][1][perm], outs[1][1])
+    assert np.array_equal(outs[0][0][:37], outs[2][0])
+
+
+def _compare(res_gpu, res_or, W_or, X64, allow_near_tie=True):
+    idx_g = list(res_gpu.index[: res_gpu.n_extracted])
+    idx_o = [r.index for r in res_or]
+    report = []
+    for k, r in enumerate(res_or):
+        if k >= res_gpu.n_extracted:
+            break
+        cos = abs(res_gpu.W[k] @ W_or[k])
+        obj_g, obj_o = res_gpu.alpha[k] + 3.0, r.alpha + 3.0
+        rel = abs(obj_g - obj_o) / abs(obj_o)
+        report.append((k + 1, idx_g[k], idx_o[k], cos, rel))
+        if idx_g[k] != idx_o[k]:
+            assert allow_near_tie and (r.near_tie or res_gpu.near_tie[k]), report
+            return report
+        assert cos >= 0.9999, report
+        assert rel <= 1e-4, report
+    return report
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("name", ["p_tiny", "p_ragged", "p_n40", "p_cfg1_reducedL"])
+def test_extract_parity(name, precision):
+    cfg, ctx = ctx_for(name, precision)
+    _, _, X64 = prepared(name)
+    W_or, res_or, _ = oracle_run(name)
+    res = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
+    assert res.n_extracted == cfg.N_out
+    rep = _compare(res, res_or, W_or, X64)
+    assert np.abs(res.W @ res.W.T - np.eye(cfg.N_out)).max() < 1e-10
+    for k, r in enumerate(res_or):
+        assert res.n_degenerate[k] == r.n_degenerate
+        assert abs(int(res.n_converged[k]) - r.n_converged) <= max(2, cfg.L // 50)
+        assert res.cluster_size[k] == pytest.approx(r.cluster_size, abs=max(2, cfg.L // 50))
+        assert bool(res.gaussian_flag[k]) == r.gaussian_flag
+    st = ctx.stats()
+    assert st["kernel_launches"] > 0 and st["step_launches"] > 0
+    print(name, precision, rep)
+
+
+def test_teacher_forced_prefix():
+    name = "p_cfg1_reducedL"
+    cfg, ctx = ctx_for(name)
+    _, _, X64 = prepared(name)
+    W_or, res_or, _ = oracle_run(name)
+    k = 3
+    res = ctx.extract(cfg.N_out, cfg.K, cfg.tol, W_prefix=W_or[:k])
+    assert np.array_equal(res.W[:k], W_or[:k])
+    for j in range(k, cfg.N_out):
+        assert res.index[j] == res_or[j].index or res_or[j].near_tie
+        assert abs(res.W[j] @ W_or[j]) >= 0.9999
+
+
+def test_candidate_end_state_parity():
+    name = "p_ragged"
+    cfg, ctx = ctx_for(name)
+    W_or, res_or, st_or = oracle_run(name)
+    ctx.extract(1, cfg.K, cfg.tol)
+    c = ctx.candidates()
+    s = st_or[0]
+    conv_g = c["state"] == 1
+    agree = np.mean(conv_g == s.converged)
+    assert agree >= 0.98
+    both = conv_g & s.converged
+    cos = np.abs(np.sum(c["W"][both] * s.W[both], axis=1))
+    assert np.mean(cos >= 1 - 1e-8) >= 0.98
+    it_agree = np.mean(np.abs(c["iters"][both] - s.iters[both]) <= 1)
+    assert it_agree >= 0.95
+
+
+def test_determinism_bitwise():
+    cfg, ctx = ctx_for("p_n40")
+    a = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
+    b = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
+    assert np.array_equal(a.W, b.W) and np.array_equal(a.alpha, b.alpha) and np.array_equal(a.index, b.index)
+
+
+def test_whiten_parity():
+    cfg = datagen.PARITY["p_n40"]
+    ds = datagen.make_dataset(cfg)
+    X32 = np.ascontiguousarray(ds.X.numpy().astype(np.float32))
+    Xw_o, mean_o, V_o, d_o = whiten.whiten(X32.astype(np.float64))
+    with oica.Context(0) as ctx:
+        Xd = torch.from_numpy(X32).cuda()
+        Xw = torch.empty_like(Xd)
+        mean, V, eig = ctx.whiten(Xd, Xw)
+    assert np.allclose(mean, mean_o, rtol=1e-12, atol=1e-12)
+    assert np.allclose(eig, d_o, rtol=1e-9)
+    assert np.abs(V - V_o).max() < 1e-7 * np.abs(V_o).max()
+    assert np.abs(Xw.cpu().numpy() - Xw_o).max() < 1e-5 * np.abs(Xw_o).max()
+
+
+def test_rank_deficient_whitening():
+    X = torch.randn(4, 1000, device="cuda")
+    X[3] = X[0]
+    with oica.Context(0) as ctx, pytest.raises(oica.OicaError) as e:
+        ctx.whiten(X, torch.empty_like(X))
+    assert e.value.name == "RANK_DEFICIENT"
+
+
+def test_gaussianity_stop_and_flags():
+    cfg = Config("lg5", 5, 100_000, 20, 200, 1e-10, 5, (("laplace", 3), ("gaussian", 2)), data_seed=500, cand_seed=600)
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X32 = np.ascontiguousarray(Xw.astype(np.float32))
+    W_o, r_o = ordering.extract(X32.astype(np.float64), cfg.L, cfg.K, cfg.tol, 5, cfg.cand_seed, stop_on_gaussianity=True)
+    with oica.Context(0) as ctx:
+        ctx.set_data(torch.from_numpy(X32).cuda())
+        ctx.init_candidates(cfg.cand_seed, cfg.L)
+        res = ctx.extract(5, cfg.K, cfg.tol, flags=oica.STOP_ON_GAUSSIANITY)
+        assert res.n_extracted == W_o.shape[0] and res.stopped == r_o[-1].stopped
+        # K = 1 with unconverged rows included: every candidate is eligible
+        r1 = ctx.extract(1, 1, 1e-30, flags=oica.INCLUDE_UNCONVERGED)
+        assert r1.n_unconverged[0] == cfg.L and r1.cluster_size[0] >= 1
+        raw = ctx.extract(1, cfg.K, cfg.tol, flags=oica.RAW_ARGMAX)
+        q = ctx.extract(1, cfg.K, cfg.tol)
+        assert abs(raw.W[0] @ q.W[0]) >= 1 - 1e-6 and raw.cluster_size[0] == 1
+
+
+def test_argument_errors():
+    cfg, ctx = ctx_for("p_tiny")
+    for kw in [dict(N_out=cfg.N + 1), dict(N_out=2, max_iter=0), dict(N_out=2, tol=0.0)]:
+        with pytest.raises(oica.OicaError) as e:
+            ctx.extract(**kw)
+        assert e.value.name == "INVALID_ARGUMENT"
+    with oica.Context(0) as c2, pytest.raises(oica.OicaError) as e:
+        c2.init_candidates(1, 10)
+    assert e.value.name == "STATE"
