@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the Fast Ordering ICA hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4_scaling] [--impl oica|reference]
+
+A STEP is one pass of the whole hot path for one component:
+candidate draw + projection, the fixed-point do-while over the active set (fused
+GEMM-cube-GEMM + fp64 epilogue + compaction) and the device-side selection/accept.  Warm-up
+steps extract components 1..W, timed steps W+1..W+K (each step is the next component, as in
+the paper's outer loop).  value = algorithmic TFLOP/s of the timed steps,
+sum_i sum_t L_act(i,t) (4 N M + 3 M) / device time (max over ranks); inputs (X, 4 N M bytes)
+are larger than L2, so no flush is needed between steps.
+
+--impl reference times the float64 CPU oracle (the reference arm for this tier) on a bounded
+sample of the same workload.  Multi-GPU: launch under torchrun; L-shard (candidates split,
+one NCCL exchange per component).  One JSON line is printed by rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ordering-ICA fixed-point TFLOP/s (% tensor peak) and seconds to extract all N"
+DEFAULT_CONFIG = "cfg4_scaling"
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active"
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            p = [s.strip() for s in line.split(",")]
+            if len(p) >= 4:
+                try:
+                    self.rows.append((float(p[0]), float(p[1]), float(p[2]), int(p[3], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        load = [r for r in self.rows if not (r[3] & 0x1)] or self.rows
+        reasons = set()
+        for r in load:
+            for bit, name in REASONS.items():
+                if r[3] & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in load),
+                "power_w_max": max(r[2] for r in load), "samples": len(load), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def load_traffic(workload: str, precision: str):
+    """dram bytes per launch of the step kernel from the committed ncu summary (or None)."""
+    import glob
+    best = None
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_step_summary.json"))):
+        try:
+            d = json.load(open(p))
+        except Exception:
+            continue
+        e = d.get(f"{workload}:{precision}")
+        if e:
+            best = e
+    return best
+
+
+def cpu_baseline(cfg, n_steps: int = 1, M_sample: int = 200_000, L_sample: int = 64):
+    """Time the float64 oracle (as it stands) on a bounded sample of the workload."""
+    import numpy as np
+
+    import datagen
+    from oracle import ordering, whiten
+
+    M_s = min(cfg.M, M_sample)
+    L_s = min(cfg.L, L_sample)
+    ds = datagen.make_dataset(cfg, M=M_s, keep_sources=False)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X = Xw.astype(np.float32).astype(np.float64)
+    W = np.zeros((0, cfg.N))
+    flops, secs = 0.0, 0.0
+    per = []
+    for k in range(n_steps):
+        t0 = time.perf_counter()
+        Wk, res = ordering.extract(X, L_s, cfg.K, cfg.tol, k + 1, cfg.cand_seed, W_prefix=W if k else None)
+        dt = time.perf_counter() - t0
+        f = ordering.algorithmic_flops(res, cfg.N, M_s)
+        per.append((f, dt))
+        W = Wk
+        flops += f
+        secs += dt
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [(i.get("internal_api"), i.get("num_threads")) for i in threadpool_info()]
+    except Exception:
+        blas = []
+    cores = len(os.sched_getaffinity(0))
+    return dict(value=flops / secs / 1e12, unit="TFLOP/s", cores=cores, kind="oracle",
+                sample=f"{cfg.name} N={cfg.N} with M'={M_s} samples, L'={L_s} candidates (ids 0..{L_s - 1}), "
+                       f"{n_steps} component(s), float64 numpy (BLAS {blas})",
+                seconds=secs, per_step=per)
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    n = args.warmup + args.steps
+    cb = cpu_baseline(cfg, n_steps=n, M_sample=args.ref_M, L_sample=args.ref_L)
+    per = cb.pop("per_step")
+    timed = per[args.warmup:]
+    f = sum(p[0] for p in timed)
+    t = sum(p[1] for p in timed)
+    val = f / t / 1e12
+    cb["value"] = val
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg.name, "N": cfg.N, "M": cfg.M, "L": cfg.L, "sample_M": min(cfg.M, args.ref_M),
+                      "sample_L": min(cfg.L, args.ref_L), "parallelism": "cpu oracle"},
+           "cpu_baseline": cb, "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_oica(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import datagen
+    from paper_2408_17118_b200 import oica
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("gloo")
+    nid = None
+    if world > 1:
+        box = [oica.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        nid = box[0]
+    stream = torch.cuda.Stream(device=dev)
+    prec = {"auto": oica.PREC_AUTO, "fp32": oica.PREC_FP32, "tc": oica.PREC_TC}[args.precision]
+    shard = oica.SHARD_M if args.shard == "m" else oica.SHARD_L
+    ctx = oica.Context(local, prec, rank, world, shard, stream=stream, nccl_id=nid)
+
+    # synthetic inputs of the config's recipe, generated and whitened on the device (not timed)
+    t0 = time.perf_counter()
+    ds = datagen.make_dataset(cfg, device=dev, dtype=torch.float32, keep_sources=False)
+    X = ds.X.contiguous()
+    del ds
+    Xw = torch.empty_like(X)
+    ctx.whiten(X, Xw)
+    del X
+    torch.cuda.synchronize()
+    M_local = cfg.M
+    if shard == oica.SHARD_M and world > 1:
+        lo, hi = cfg.M * rank // world, cfg.M * (rank + 1) // world
+        Xw = Xw[:, lo:hi].contiguous()
+        M_local = hi - lo
+    ctx.set_data(Xw, M_global=cfg.M)
+    ctx.init_candidates(cfg.cand_seed, cfg.L)
+    setup_s = time.perf_counter() - t0
+
+    N_out = args.warmup + args.steps
+    assert N_out <= cfg.N_out, "warmup + steps exceeds the config's N_out"
+    Wacc = np.zeros((cfg.N_out, cfg.N))
+    recs = []
+
+    def step(k):
+        r = ctx.extract(k + 1, cfg.K, cfg.tol, W_prefix=Wacc[:k] if k else None)
+        Wacc[k] = r.W[k]
+        recs.append(dict(i=k + 1, index=int(r.index[k]), alpha=float(r.alpha[k]), upsilon=float(r.upsilon[k]),
+                         sum_active=int(r.sum_active[k]), n_iter=int(r.n_iter[k]), cluster=int(r.cluster_size[k]),
+                         n_conv=int(r.n_converged[k]), n_unconv=int(r.n_unconverged[k]), near_tie=int(r.near_tie[k])))
+        return r
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ctx.reset_stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for k in range(args.warmup, N_out):
+            step(k)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    st = ctx.stats()
+    timed = recs[args.warmup:]
+    M = cfg.M
+    flops = sum(r["sum_active"] for r in timed) * (4.0 * cfg.N * M + 3.0 * M)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = flops / (ms / 1e3) / 1e12
+
+    # end-to-end leg: the same components re-extracted through host buffers each step
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.empty(Xw.shape, dtype=torch.float32, pin_memory=True)
+        Xh.copy_(Xw)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        d2h = 0
+        for k in range(args.warmup, N_out):
+            ctx.set_data_host_ptr(Xh.data_ptr(), cfg.N, M_local, M_local, M_global=cfg.M)
+            r = ctx.extract(k + 1, cfg.K, cfg.tol, W_prefix=Wacc[:k])
+            d2h += 8 * cfg.N + 112 + 4 * int(r.n_iter[k])
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": flops / (ems / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 4 * cfg.N * M_local,
+               "d2h_bytes_per_step": d2h // max(1, args.steps), "ms_per_step": ems / args.steps}
+        ctx.set_data(Xw, M_global=cfg.M)
+
+    if rank != 0:
+        ctx.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    clocks = clk.summary()
+    precision = "tc" if st["precision"] == oica.PREC_TC else "fp32"
+    kern_tflops = st["step_flops"] / (st["step_ms"] / 1e3) / 1e12 if st["step_ms"] > 0 else None
+    if precision == "tc":
+        peak = peaks.get("bf16_tflops_sustained") or 1404.1
+        roof = {"bound": "tensor", "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (fp16 dense = bf16 rate); "
+                                                  "3 fp16 passes per 2 algorithmic GEMMs -> precision roofline = peak*2/3"}
+    else:
+        mhz = clocks.get("sm_mhz") or peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1357.0)
+        peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+        roof = {"bound": "alu", "peak_source": f"148 SMs x 128 FP32 lanes x 2 flop x {mhz:.0f} MHz (median SM clock under load)"}
+    tr = load_traffic(cfg.name, precision)
+    roof.update({"achieved": kern_tflops, "peak": peak, "unit": "TFLOP/s",
+                 "frac": (kern_tflops / peak) if kern_tflops else None,
+                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                 "traffic_launch": tr if tr else None,
+                 "kernel": "fused fixed-point step (GEMM-cube-GEMM)", "launches": st["step_launches"],
+                 "kernel_ms": st["step_ms"], "share_of_step": st["step_ms"] / ms if ms else None})
+    cb = None
+    if not args.no_cpu_baseline and world == 1:
+        cb = cpu_baseline(cfg, 1, args.ref_M, args.ref_L)
+        cb.pop("per_step", None)
+    sec_per_comp = ms / 1e3 / args.steps
+    out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f16" if precision == "tc" else "f32", "data": "synthetic",
+           "config": {"workload": cfg.name, "N": cfg.N, "M": cfg.M, "L": cfg.L, "K": cfg.K, "tol": cfg.tol,
+                      "N_out": cfg.N_out, "components_timed": [r["i"] for r in timed],
+                      "parallelism": f"{'m' if shard == oica.SHARD_M else 'l'}shard{world}",
+                      "l2": f"inputs larger than L2 (X = {4 * cfg.N * cfg.M / 1e9:.2f} GB fp32), no flush",
+                      "precision": precision, "slots": st["slots"]},
+           "seconds_per_component": sec_per_comp,
+           "gpu_launches": st["kernel_launches"], "roofline": roof, "e2e": e2e, "cpu_baseline": cb,
+           "clocks": clocks, "components": timed, "setup_s": setup_s}
+    print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="oica", choices=["oica", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tc"])
+    ap.add_argument("--shard", default="l", choices=["l", "m"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-M", type=int, default=200_000)
+    ap.add_argument("--ref-L", type=int, default=64)
+    args = ap.parse_args()
+    import datagen
+    cfg = datagen.get(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_oica(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

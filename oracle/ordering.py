@@ -91,7 +91,7 @@ def batch_step(B: np.ndarray, X: np.ndarray, block: int = 8192):
         Z = B @ Xb                      # eq. (4)
         Z2 = Z * Z
         s4 += np.sum(Z2 * Z2, axis=1)
-        G += (Z2 * Z) @ Xb.T            # eq. (5), accumulated over M
+        G += (Xb @ (Z2 * Z).T).T        # eq. (5), accumulated over M ((X Z^3^T)^T: same product)
     return G / M - 3.0 * B, s4
 
 

@@ -95,7 +95,7 @@ def ordering_ica_fast_reduced(X, L, K, tol, N_out, seed, include_unconverged=Fal
             for m0 in range(0, M, block):
                 Xb = Xr[:, m0:m0 + block]
                 Zb = Bp @ Xb                                # :243
-                Z += (Zb * Zb * Zb) @ Xb.T                  # :244
+                Z += (Xb @ (Zb * Zb * Zb).T).T              # :244
             Bn = Z / M - 3.0 * Bp                           # :245
             n = np.linalg.norm(Bn, axis=1)
             dg = n < DEGENERATE_NORM
