@@ -97,6 +97,7 @@ __global__ void k_epilogue(const double* __restrict__ Gp, const double* __restri
   if (a >= L_act) return;
   int l = act[a];
   double g[kMaxV], wo[kMaxV];
+  double s4g = 0.0;
 #pragma unroll
   for (int u = 0; u < kMaxV; ++u) {
     int n = lane + 32 * u;
@@ -106,11 +107,16 @@ __global__ void k_epilogue(const double* __restrict__ Gp, const double* __restri
       w = W64[(int64_t)l * N + n];
     }
     wo[u] = w;
+    s4g += w * acc;
     g[u] = (n < N) ? acc / M - 3.0 * w : 0.0;            // PAPER.md:244-245 (eq. (5), A3)
   }
   double s4 = 0.0;
-  if (lane == 0)
-    for (int s = 0; s < S; ++s) s4 += s4p[(int64_t)s * cap + a];
+  if (s4p) {
+    if (lane == 0)
+      for (int s = 0; s < S; ++s) s4 += s4p[(int64_t)s * cap + a];
+  } else {
+    s4 = warp_sum(s4g);   // identity w . sum_m y^3 x = sum_m y^4 (tensor-core path: approximate alpha)
+  }
   project_warp(g, Wacc, k, N, lane);
   double ss = 0.0;
 #pragma unroll
@@ -183,8 +189,9 @@ __global__ void k_operand_f32(const int* __restrict__ act, const int* __restrict
   W32[idx] = n < N ? (float)W64[(int64_t)act[a] * N + n] : 0.f;
 }
 
-// Split fp16 operand: w is scaled by 2^4 (|w| <= 1 -> <= 16) so w_lo stays in the normal range;
-// hi = fp16(2^4 w), lo = fp16((2^4 w - hi) 2^11).  The step kernel undoes both scales.
+// Split fp16 operand: w is scaled by 2^4 (|w| <= 1 -> <= 16) so most w_lo stay normal fp16;
+// hi = fp16(2^4 w), lo = fp16(2^4 w - hi).  hi + lo = 2^4 w to ~2^-22 relative (absolute error
+// <= 3e-8 / 16 per coordinate from lo subnormals); both GEMM1 passes share one accumulator.
 __global__ void k_operand_f16x2(const int* __restrict__ act, const int* __restrict__ Lact, int cap,
                                 const double* __restrict__ W64, int N, int NP, __half* __restrict__ Whi,
                                 __half* __restrict__ Wlo) {
@@ -193,7 +200,7 @@ __global__ void k_operand_f16x2(const int* __restrict__ act, const int* __restri
   if (a >= cap || a >= *Lact) return;
   double w = n < N ? W64[(int64_t)act[a] * N + n] * 16.0 : 0.0;
   __half hi = __double2half(w);
-  __half lo = __double2half((w - (double)__half2float(hi)) * 2048.0);
+  __half lo = __double2half(w - (double)__half2float(hi));
   Whi[idx] = hi;
   Wlo[idx] = lo;
 }
@@ -207,10 +214,22 @@ __global__ void k_slot_reduce(const double* __restrict__ Gp, const double* __res
   if (n < N) {
     for (int s = 0; s < S; ++s) acc += Gp[((int64_t)s * cap + a) * ldg + n];
     G_out[(int64_t)a * ldo + n] = acc;
-  } else {
+  } else if (s4p && s4_out) {
     for (int s = 0; s < S; ++s) acc += s4p[(int64_t)s * cap + a];
     s4_out[a] = acc;
   }
+}
+
+// s4 = w . G_raw (identity sum_m y^3 (w.x) = sum_m y^4), rows by position; one warp per row.
+__global__ void k_s4_from_g(const double* __restrict__ W, const double* __restrict__ G, int ldg, int L, int N,
+                            double* __restrict__ s4) {
+  int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int lane = threadIdx.x & 31;
+  if (a >= L) return;
+  double v = 0.0;
+  for (int n = lane; n < N; n += 32) v += W[(int64_t)a * N + n] * G[(int64_t)a * ldg + n];
+  v = warp_sum(v);
+  if (lane == 0) s4[a] = v;
 }
 
 }  // namespace
@@ -259,6 +278,12 @@ int launch_slot_reduce(cudaStream_t st, const double* Gp, const double* s4p, int
   if (L <= 0) return 0;
   int64_t tot = (int64_t)L * (N + 1);
   k_slot_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, L, N, G_out, ldo, s4_out);
+  return 1;
+}
+
+int launch_s4_from_g(cudaStream_t st, const double* W, const double* G, int ldg, int L, int N, double* s4) {
+  if (L <= 0) return 0;
+  k_s4_from_g<<<(unsigned)ceil_div((int64_t)L * 32, 256), 256, 0, st>>>(W, G, ldg, L, N, s4);
   return 1;
 }
 

@@ -1,17 +1,439 @@
-// K2a: fused GEMM-cube-GEMM on tcgen05 tensor cores (placeholder until the kernel lands).
+// K2a: fused GEMM-cube-GEMM on tcgen05 tensor cores (sm_100a), Y never leaves the SM.
+//
+// For one work unit = (128-row tile of active candidates, split-M slot s) the CTA computes
+//   Y   = W X_chunk                 GEMM1  (eq. (4))   -> TMEM, fp32
+//   Y3  = y o y o y                  epilogue warps, fp16 A operand written back into TMEM
+//   G  += Y3 X_chunk^T               GEMM2  (eq. (5))   -> TMEM, fp32 accumulator
+// streaming X through shared memory in TMA-loaded chunks, and finally stores G (x 2^6) as the
+// unit's fp64 slot partial Gp[s][row][n].  No atomics: each unit owns its slot region, so the
+// result of a row is independent of the tile it shares (bitwise-deterministic).
+//
+// Arithmetic (DESIGN.md §5 "precision"): X is rounded once to fp16 (11-bit significand, same
+// as TF32); W is split into hi + lo fp16 planes of 2^4 w (GEMM1 = 2 passes: hi X + lo X, so w is
+// represented to ~2^-22 and the fixed-point map stays smooth at the 1e-10 convergence level);
+// y^3 2^-6 is rounded to fp16 for GEMM2 (1 pass).  Accumulation fp32 in TMEM per slot, fp64
+// across slots (K3).  Issued tensor work = 3 fp16 passes per 2 algorithmic GEMMs.
+//
+// Layout (variant A, NP <= 128):  TMEM  [W_hi NP/2 | W_lo NP/2 | G NP | Y0 128 | Y1 128]
+//                                  SMEM  X stages [NP][128] fp16, 128B-swizzled (2 TMA boxes)
+// Layout (variant B, NP = 256):   TMEM  [W_hi 128 | G 256 | Y0 64 | Y1 64]
+//                                  SMEM  W_lo [128][256] (4 K-major SW128 boxes) + X stages [256][64]
+// Warp roles: 0 = TMA producer + TMEM allocator, 1 = MMA issuer (one thread), 2..5 = epilogue
+// (warp w reaches TMEM lanes 32*(w%4)..+31 = rows of the tile).
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "kernels.cuh"
 
 namespace oica {
+namespace {
 
-bool tc_supported(int N) { (void)N; return false; }
-int tc_np(int N) { return (int)round_up(N < 16 ? 16 : N, 16); }
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-int launch_step_tc(cudaStream_t, const __half*, int64_t, int64_t, int, const __half*, const __half*, int, int64_t, int,
-                   int, double*, double*, int64_t, int) {
-  throw Error(OICA_ERR_INVALID_ARGUMENT, "tensor-core step not built");
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-int launch_x_prepare_f16(cudaStream_t, const float*, int64_t, int, int64_t, int, int64_t, __half*) {
-  throw Error(OICA_ERR_INVALID_ARGUMENT, "tensor-core step not built");
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[smem desc] * B[smem desc]
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem desc]
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+#define OICA_R8(i) "=r"(v[i + 0]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
+#define OICA_W8(i) "r"(v[i + 0]), "r"(v[i + 1]), "r"(v[i + 2]), "r"(v[i + 3]), "r"(v[i + 4]), "r"(v[i + 5]), "r"(v[i + 6]), "r"(v[i + 7])
+
+// 32 lanes x 32 consecutive 32-bit columns: thread i of the warp gets lane (base+i), columns c..c+31
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : OICA_R8(0), OICA_R8(8), OICA_R8(16), OICA_R8(24)
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      OICA_W8(0), OICA_W8(8), OICA_W8(16), OICA_W8(24)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      OICA_W8(0), OICA_W8(8)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// ------------------------------------------------------------------ descriptors
+// shared-memory matrix descriptor (tcgen05): start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
+// version 1 [46,48), layout SWIZZLE_128B = 2 [61,64).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor, kind::f16: F16 x F16 -> F32, M = 128
+__host__ __device__ constexpr uint32_t idesc_f16(int N, int b_mn_major) {
+  return (1u << 4) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+template <int NP, bool WLO_TMEM>
+struct Cfg {
+  static constexpr int MT = WLO_TMEM ? 128 : 64;                 // samples per chunk (GEMM1 N)
+  static constexpr int XB = NP * 128;                            // bytes of one [NP][64] swizzled box
+  static constexpr int X_STAGE = NP * MT * 2;                    // bytes per X stage
+  static constexpr int WLO_BYTES = WLO_TMEM ? 0 : 128 * NP * 2;  // W_lo in SMEM (variant B)
+  static constexpr int STAGES = (WLO_TMEM ? 196608 : 131072) / X_STAGE >= 8 ? 8 : (WLO_TMEM ? 196608 : 131072) / X_STAGE;
+  static constexpr int C_WHI = 0;
+  static constexpr int C_WLO = NP / 2;                           // variant A only
+  static constexpr int C_G = WLO_TMEM ? NP : NP / 2;
+  static constexpr int C_Y0 = C_G + NP;
+  static constexpr int C_Y1 = C_Y0 + MT;
+  static_assert(C_Y1 + MT <= 512, "TMEM budget");
+  static constexpr int SMEM = 1024 + WLO_BYTES + STAGES * X_STAGE + 1024;
+};
+
+template <int NP, bool WLO_TMEM>
+__global__ void __launch_bounds__(192, 1)
+k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
+          const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_act, int64_t M, int64_t slot_len,
+          double* __restrict__ Gp, int64_t cap, int n_tiles) {
+  using C = Cfg<NP, WLO_TMEM>;
+  constexpr int MT = C::MT;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* s_wlo = smem;
+  uint8_t* s_x = smem + C::WLO_BYTES;
+  uint64_t* bars = (uint64_t*)(s_x + C::STAGES * C::X_STAGE);
+  uint64_t* full = bars;                     // [STAGES]
+  uint64_t* empty = full + C::STAGES;        // [STAGES]
+  uint64_t* wlo_full = empty + C::STAGES;    // 1
+  uint64_t* w_ready = wlo_full + 1;          // 1
+  uint64_t* yfull = w_ready + 1;             // [2]
+  uint64_t* y3ready = yfull + 2;             // [2]
+  uint64_t* gdone = y3ready + 2;             // 1
+  uint32_t* tmem_slot = (uint32_t*)(gdone + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x % n_tiles, s = blockIdx.x / n_tiles;
+  const int row0 = tile * 128;
+  const int64_t m_begin = (int64_t)s * slot_len;
+  const int64_t m_end = min(M, m_begin + slot_len);
+  const int nchunk = (int)ceil_div(m_end - m_begin, MT);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(wlo_full, 1);
+    mbar_init(w_ready, 128);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&yfull[b], 1);
+      mbar_init(&y3ready[b], 128);
+    }
+    mbar_init(gdone, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      if (!WLO_TMEM) {
+        mbar_expect_tx(wlo_full, C::WLO_BYTES);
+        for (int kb = 0; kb < NP / 64; ++kb) tma_load_2d(s_wlo + kb * 16384, &tmWlo, wlo_full, kb * 64, row0);
+      }
+      for (int j = 0; j < nchunk; ++j) {
+        int st = j % C::STAGES;
+        if (j >= C::STAGES) mbar_wait(&empty[st], ((j / C::STAGES) - 1) & 1);
+        mbar_expect_tx(&full[st], C::X_STAGE);
+        int m0 = (int)(m_begin + (int64_t)j * MT);
+        uint8_t* dst = s_x + st * C::X_STAGE;
+        for (int h = 0; h < MT / 64; ++h) tma_load_2d(dst + h * C::XB, &tmX, &full[st], m0 + 64 * h, 0);
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      constexpr uint32_t id1 = idesc_f16(MT, 1);   // GEMM1: B = X, MN-major (m contiguous)
+      constexpr uint32_t id2 = idesc_f16(NP, 0);   // GEMM2: B = X, K-major (K = m)
+      const uint32_t t_g = tmem + C::C_G;
+      mbar_wait(w_ready, 0);
+      if (!WLO_TMEM) mbar_wait(wlo_full, 0);
+      tc_fence_after();
+      auto gemm1 = [&](int j) {
+        int st = j % C::STAGES, b = j & 1;
+        mbar_wait(&full[st], (j / C::STAGES) & 1);
+        tc_fence_after();
+        uint32_t xs = smem_u32(s_x + st * C::X_STAGE);
+        uint32_t t_y = tmem + (b ? C::C_Y1 : C::C_Y0);
+#pragma unroll 1
+        for (int kb = 0; kb < NP / 16; ++kb) {   // pass 1: W_hi (TMEM) x X
+          uint64_t bd = sdesc(xs + kb * 2048, C::XB, 1024);
+          mma_ts(t_y, tmem + C::C_WHI + kb * 8, bd, id1, kb > 0);
+        }
+#pragma unroll 1
+        for (int kb = 0; kb < NP / 16; ++kb) {   // pass 2: W_lo x X
+          uint64_t bd = sdesc(xs + kb * 2048, C::XB, 1024);
+          if (WLO_TMEM) {
+            mma_ts(t_y, tmem + C::C_WLO + kb * 8, bd, id1, 1u);
+          } else {
+            uint32_t ws = smem_u32(s_wlo) + (kb >> 2) * 16384 + (kb & 3) * 32;
+            mma_ss(t_y, sdesc(ws, 16, 1024), bd, id1, 1u);
+          }
+        }
+        tc_commit(&yfull[b]);
+      };
+      auto gemm2 = [&](int j) {
+        int st = j % C::STAGES, b = j & 1;
+        mbar_wait(&y3ready[b], (j >> 1) & 1);
+        tc_fence_after();
+        uint32_t xs = smem_u32(s_x + st * C::X_STAGE);
+        uint32_t t_y3 = tmem + (b ? C::C_Y1 : C::C_Y0);
+#pragma unroll 1
+        for (int kk = 0; kk < MT / 16; ++kk) {
+          uint64_t bd = sdesc(xs + (kk >> 2) * C::XB + (kk & 3) * 32, 16, 1024);
+          mma_ts(t_g, t_y3 + kk * 8, bd, id2, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(&empty[st]);
+      };
+      if (nchunk > 0) gemm1(0);
+      for (int j = 0; j < nchunk; ++j) {
+        if (j + 1 < nchunk) gemm1(j + 1);
+        gemm2(j);
+      }
+      tc_commit(gdone);
+    }
+  } else {
+    // ===== epilogue warps (128 threads, thread <-> TMEM lane <-> tile row) =====
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int row = row0 + r;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    // W operand rows -> TMEM (A operand of GEMM1, fp16 pairs per 32-bit column)
+    {
+      const uint32_t* wh = (const uint32_t*)(Whi + (int64_t)row * NP);
+      const uint32_t* wl = (const uint32_t*)(Wlo + (int64_t)row * NP);
+      bool ok = row < L_act;
+#pragma unroll 1
+      for (int c = 0; c < NP / 2; c += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = ok ? __ldg(wh + c + k) : 0u;
+        tmem_st16(tmem + lane_off + C::C_WHI + c, v);
+        if (WLO_TMEM) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = ok ? __ldg(wl + c + k) : 0u;
+          tmem_st16(tmem + lane_off + C::C_WLO + c, v);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(w_ready);
+    }
+    for (int j = 0; j < nchunk; ++j) {
+      const int b = j & 1;
+      const uint32_t t_y = tmem + lane_off + (b ? C::C_Y1 : C::C_Y0);
+      mbar_wait(&yfull[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t packed[MT / 2];
+#pragma unroll
+      for (int c = 0; c < MT; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(t_y + c, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          // accumulator = 2^4 y  ->  2^-6 y^3 = acc^3 2^-18
+          float a0 = __uint_as_float(v[k]), a1 = __uint_as_float(v[k + 1]);
+          float c0 = a0 * a0 * a0 * 0x1.0p-18f, c1 = a1 * a1 * a1 * 0x1.0p-18f;
+          __half2 h = __floats2half2_rn(c0, c1);
+          packed[(c + k) / 2] = *reinterpret_cast<uint32_t*>(&h);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < MT / 2; c += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = packed[c + k];
+        tmem_st16(t_y + c, v);   // Y^3 (fp16 pairs) in place: A operand of GEMM2
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&y3ready[b]);
+    }
+    // G (fp32, scaled 2^-6) -> fp64 slot partial
+    mbar_wait(gdone, 0);
+    tc_fence_after();
+    double* out = Gp + ((int64_t)s * cap + row) * NP;
+    bool ok = row < L_act && nchunk > 0;
+#pragma unroll 1
+    for (int c = 0; c < NP; c += 32) {
+      uint32_t v[32];
+      tmem_ld32(tmem + lane_off + C::C_G + c, v);
+      tmem_wait_ld();
+      if (ok) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) out[c + k] = (double)__uint_as_float(v[k]) * 64.0;
+      }
+    }
+    if (row < L_act && nchunk == 0)
+      for (int c = 0; c < NP; ++c) out[c] = 0.0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  });
+  if (!fn) throw Error(OICA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2D fp16 tensor [rows][cols] (row stride ld elements), box [box_rows][64], 128B swizzle
+CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)base, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(OICA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+template <int NP, bool A>
+void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
+                    int L_act, int64_t slot_len, int S, double* Gp, int64_t cap) {
+  using C = Cfg<NP, A>;
+  static bool attr = false;
+  if (!attr) {
+    OICA_CUDA(cudaFuncSetAttribute(k_step_tc<NP, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  CUtensorMap tx = make_map(Xh, NP, ldx, ldx, NP);
+  CUtensorMap tw = make_map(Wlo, cap, NP, NP, 128);
+  int n_tiles = (int)ceil_div(L_act, 128);
+  k_step_tc<NP, A><<<(unsigned)(n_tiles * S), 192, C::SMEM, st>>>(tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_tiles);
+}
+
+__global__ void k_x_prepare_f16(const float* __restrict__ X, int64_t ld, int N, int64_t M, int NP, int64_t ldx,
+                                __half* __restrict__ Xh) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t n = idx / ldx, m = idx % ldx;
+  if (n >= NP) return;
+  float v = (n < N && m < M) ? X[n * ld + m] : 0.f;
+  Xh[idx] = __float2half_rn(v);
+}
+
+}  // namespace
+
+bool tc_supported(int N) { return N >= 1 && N <= 256; }
+int tc_np(int N) { return N <= 128 ? (int)round_up(N < 16 ? 16 : N, 16) : 256; }
+
+int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
+                   const __half* Wlo, int L_act, int64_t slot_len, int S, int flush, double* Gp, double* s4p,
+                   int64_t cap, int num_sms) {
+  (void)flush; (void)s4p; (void)num_sms;
+  if (L_act <= 0) return 0;
+  switch (NP) {
+    case 16: launch_variant<16, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
+    case 32: launch_variant<32, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
+    case 48: launch_variant<48, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
+    case 64: launch_variant<64, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
+    case 80: launch_variant<80, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
+    case 96: launch_variant<96, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
+    case 112: launch_variant<112, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
+    case 128: launch_variant<128, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
+    case 256: launch_variant<256, false>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
+    default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
+  }
+  return 1;
+}
+
+int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP, int64_t ldx,
+                         __half* Xh) {
+  int64_t tot = (int64_t)NP * ldx;
+  k_x_prepare_f16<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(X, ld, N, M, NP, ldx, Xh);
+  return 1;
 }
 
 }  // namespace oica

@@ -40,6 +40,8 @@ int launch_epilogue(cudaStream_t st, const double* Gp, const double* s4p, int S,
 int launch_slot_reduce(cudaStream_t st, const double* Gp, const double* s4p, int S, int64_t cap, int ldg,
                        int L, int N, double* G_out, int ldo, double* s4_out);
 
+int launch_s4_from_g(cudaStream_t st, const double* W, const double* G, int ldg, int L, int N, double* s4);
+
 // ---- K5: device-side argmax, cluster assignment, exact alpha, merge + accept
 struct SelectWork;  // defined in k_select.cu
 struct ComponentRecord {

@@ -41,7 +41,7 @@ struct DevBuf {
 
 // Split-M slot policy: S depends only on M, so per-row results are identical
 // for any GPU count in L-shard mode and any active-set size.
-constexpr int64_t kSlotTarget = 4096;   // samples per slot (lower bound)
+constexpr int64_t kSlotTarget = 8192;   // samples per slot (lower bound)
 constexpr int kMaxSlots = 128;
 constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
 constexpr int64_t kSlotAlign = 128;
@@ -303,18 +303,19 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
       c->stats.iterations += 1;
       c->stats.sum_active += L_act;
       run_step(c, L_act, true);
+      const bool tc = c->precision == OICA_PREC_TC;
       const double* G = c->Gp.p;
-      const double* s4 = c->s4p.p;
+      const double* s4 = tc ? nullptr : c->s4p.p;   // TC: alpha~ from the identity w . G (K3)
       int S = c->S;
       int64_t cap = c->Ll;
       if (c->mshard()) {  // one fp64 allreduce of (G, s4) per iteration
-        c->count(launch_slot_reduce(st, c->Gp.p, c->s4p.p, c->S, c->Ll, (int)c->NP, L_act, N, c->Gsum.p, (int)c->NP,
-                                    c->s4sum.p));
+        c->count(launch_slot_reduce(st, c->Gp.p, tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, L_act, N, c->Gsum.p,
+                                    (int)c->NP, c->s4sum.p));
         auto& nc = Nccl::get();
         OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_act * c->NP, ncclFloat64, ncclSum, c->comm, st));
-        OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_act, ncclFloat64, ncclSum, c->comm, st));
+        if (!tc) OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_act, ncclFloat64, ncclSum, c->comm, st));
         G = c->Gsum.p;
-        s4 = c->s4sum.p;
+        s4 = tc ? nullptr : c->s4sum.p;
         S = 1;
         cap = c->Ll;
       }
@@ -596,8 +597,10 @@ oica_status oica_fixed_point_step(oica_ctx* c, const double* W_dev, int64_t L, d
     c->count(launch_compact(c->st, nullptr, c->keep.p, (int)L, c->act0.p, c->Lact_dev.p, nullptr));
     build_operand(c, c->act0.p, (int)L);
     run_step(c, (int)L, true);
-    c->count(launch_slot_reduce(c->st, c->Gp.p, c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L, (int)c->N, G_dev,
-                                (int)c->N, s4_dev));
+    bool tc = c->precision == OICA_PREC_TC;
+    c->count(launch_slot_reduce(c->st, c->Gp.p, tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L, (int)c->N,
+                                G_dev, (int)c->N, s4_dev));
+    if (tc) c->count(launch_s4_from_g(c->st, c->W64.p, G_dev, (int)c->N, (int)L, (int)c->N, s4_dev));
     check_launch();
     c->harvest_events();
   });
