@@ -111,38 +111,44 @@ def load_traffic(workload: str, precision: str):
 
 
 def cpu_baseline(cfg, n_steps: int = 1, M_sample: int = 200_000, L_sample: int = 64):
-    """Time the float64 oracle (as it stands) on a bounded sample of the workload."""
+    """Time the float64 oracle (as it stands) on a bounded sample of the workload.
+
+    The sample's raw signals come from the seeded generator (on the GPU when present, only for
+    speed); whitening and the extraction are the oracle's.  BLAS threads: half the host cores
+    (OpenBLAS with one thread per logical core hits threading pathologies on skinny products)."""
     import numpy as np
+    import torch
+    from threadpoolctl import threadpool_info, threadpool_limits
 
     import datagen
     from oracle import ordering, whiten
 
     M_s = min(cfg.M, M_sample)
     L_s = min(cfg.L, L_sample)
-    ds = datagen.make_dataset(cfg, M=M_s, keep_sources=False)
-    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
-    X = Xw.astype(np.float32).astype(np.float64)
-    W = np.zeros((0, cfg.N))
-    flops, secs = 0.0, 0.0
-    per = []
-    for k in range(n_steps):
-        t0 = time.perf_counter()
-        Wk, res = ordering.extract(X, L_s, cfg.K, cfg.tol, k + 1, cfg.cand_seed, W_prefix=W if k else None)
-        dt = time.perf_counter() - t0
-        f = ordering.algorithmic_flops(res, cfg.N, M_s)
-        per.append((f, dt))
-        W = Wk
-        flops += f
-        secs += dt
-    try:
-        from threadpoolctl import threadpool_info
-        blas = [(i.get("internal_api"), i.get("num_threads")) for i in threadpool_info()]
-    except Exception:
-        blas = []
-    cores = len(os.sched_getaffinity(0))
-    return dict(value=flops / secs / 1e12, unit="TFLOP/s", cores=cores, kind="oracle",
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    ds = datagen.make_dataset(cfg, M=M_s, keep_sources=False, device=dev)
+    Xraw = ds.X.cpu().numpy()
+    threads = max(1, len(os.sched_getaffinity(0)) // 2)
+    with threadpool_limits(threads, user_api="blas"):
+        Xw, _, _, _ = whiten.whiten(Xraw)
+        X = Xw.astype(np.float32).astype(np.float64)
+        W = np.zeros((0, cfg.N))
+        flops, secs = 0.0, 0.0
+        per = []
+        for k in range(n_steps):
+            t0 = time.perf_counter()
+            Wk, res = ordering.extract(X, L_s, cfg.K, cfg.tol, k + 1, cfg.cand_seed, W_prefix=W if k else None)
+            dt = time.perf_counter() - t0
+            f = ordering.algorithmic_flops(res[-1:], cfg.N, M_s)
+            per.append((f, dt))
+            W = Wk
+            flops += f
+            secs += dt
+        blas = [(i.get("internal_api"), i.get("num_threads")) for i in threadpool_info() if i.get("user_api") == "blas"]
+    return dict(value=flops / secs / 1e12, unit="TFLOP/s", cores=threads, kind="oracle",
                 sample=f"{cfg.name} N={cfg.N} with M'={M_s} samples, L'={L_s} candidates (ids 0..{L_s - 1}), "
-                       f"{n_steps} component(s), float64 numpy (BLAS {blas})",
+                       f"{n_steps} component(s), float64 numpy, BLAS {blas}, host has "
+                       f"{len(os.sched_getaffinity(0))} cores",
                 seconds=secs, per_step=per)
 
 

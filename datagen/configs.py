@@ -146,4 +146,14 @@ PARITY = {
     "p_n40": Config("p_n40", 40, 12000, 257, 200, 1e-10, 4,
                     (("laplace", 20), ("gg_uniform", 20, 0.6, 1.8)),
                     data_seed=3003, cand_seed=4003),
+    # M >= 131072: OICA_PREC_AUTO runs the tensor-core kernel (variant A: NP <= 128, B: NP = 256)
+    "p_tc_n32": Config("p_tc_n32", 32, 150_001, 300, 200, 1e-10, 4,
+                       (("laplace", 16), ("gg_uniform", 16, 0.5, 1.5)),
+                       data_seed=3004, cand_seed=4004),
+    "p_tc_n128": Config("p_tc_n128", 128, 200_000, 200, 200, 1e-10, 3,
+                        (("gg_uniform", 128, 0.6, 1.8),),
+                        data_seed=3005, cand_seed=4005),
+    "p_tc_n256": Config("p_tc_n256", 256, 150_000, 160, 200, 1e-10, 2,
+                        (("gg_uniform", 256, 0.5, 1.9),),
+                        data_seed=3006, cand_seed=4006),
 }

@@ -99,12 +99,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : OICA_R8(0), OICA_R8(8), OICA_R8(16), OICA_R8(24)
       : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      OICA_W8(0), OICA_W8(8), OICA_W8(16), OICA_W8(24)
-      : "memory");
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), OICA_W8(0)
+               : "memory");
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
@@ -277,15 +274,15 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const uint32_t* wl = (const uint32_t*)(Wlo + (int64_t)row * NP);
       bool ok = row < L_act;
 #pragma unroll 1
-      for (int c = 0; c < NP / 2; c += 16) {
-        uint32_t v[16];
+      for (int c = 0; c < NP / 2; c += 8) {   // NP/2 is a multiple of 8 columns
+        uint32_t v[8];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = ok ? __ldg(wh + c + k) : 0u;
-        tmem_st16(tmem + lane_off + C::C_WHI + c, v);
+        for (int k = 0; k < 8; ++k) v[k] = ok ? __ldg(wh + c + k) : 0u;
+        tmem_st8(tmem + lane_off + C::C_WHI + c, v);
         if (WLO_TMEM) {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] = ok ? __ldg(wl + c + k) : 0u;
-          tmem_st16(tmem + lane_off + C::C_WLO + c, v);
+          for (int k = 0; k < 8; ++k) v[k] = ok ? __ldg(wl + c + k) : 0u;
+          tmem_st8(tmem + lane_off + C::C_WLO + c, v);
         }
       }
       tmem_wait_st();
@@ -335,7 +332,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       tmem_wait_ld();
       if (ok) {
 #pragma unroll
-        for (int k = 0; k < 32; ++k) out[c + k] = (double)__uint_as_float(v[k]) * 64.0;
+        for (int k = 0; k < 32; ++k)
+          if (NP % 32 == 0 || c + k < NP) out[c + k] = (double)__uint_as_float(v[k]) * 64.0;
       }
     }
     if (row < L_act && nchunk == 0)

@@ -45,6 +45,7 @@ constexpr int64_t kSlotTarget = 8192;   // samples per slot (lower bound)
 constexpr int kMaxSlots = 128;
 constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
 constexpr int64_t kSlotAlign = 128;
+constexpr int64_t kTcMinSamples = 131072;   // OICA_PREC_AUTO switches to tensor cores at this M
 
 }  // namespace
 
@@ -394,7 +395,9 @@ void set_data_impl(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int
   c->ld = ld;
   c->Mg = M_global;
   int req = c->cfg.precision;
-  bool tc = (req == OICA_PREC_TC || req == OICA_PREC_AUTO) && tc_supported((int)N);
+  // AUTO: tensor cores once M is large enough that the fp16 rounding noise of the contraction
+  // (~2^-12 / sqrt(M) relative in G) sits well below the 1e-10 convergence test.
+  bool tc = (req == OICA_PREC_TC || (req == OICA_PREC_AUTO && M_global >= kTcMinSamples)) && tc_supported((int)N);
   OICA_REQUIRE(!(req == OICA_PREC_TC && !tc), OICA_ERR_INVALID_ARGUMENT, "tensor-core step unsupported for this N");
   c->precision = tc ? OICA_PREC_TC : OICA_PREC_FP32;
   c->NP = tc ? tc_np((int)N) : (N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256);
