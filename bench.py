@@ -338,8 +338,8 @@ def main():
     ap.add_argument("--shard", default="l", choices=["l", "m"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-M", type=int, default=200_000)
-    ap.add_argument("--ref-L", type=int, default=64)
+    ap.add_argument("--ref-M", type=int, default=1_000_000)
+    ap.add_argument("--ref-L", type=int, default=256)
     args = ap.parse_args()
     import datagen
     cfg = datagen.get(args.config)
