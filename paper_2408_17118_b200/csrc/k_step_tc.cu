@@ -64,6 +64,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, %1;\n\t"
+      "@px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -211,57 +222,61 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
-      constexpr uint32_t id1 = idesc_f16(MT, 1);   // GEMM1: B = X, MN-major (m contiguous)
-      constexpr uint32_t id2 = idesc_f16(NP, 0);   // GEMM2: B = X, K-major (K = m)
-      const uint32_t t_g = tmem + C::C_G;
-      mbar_wait(w_ready, 0);
-      if (!WLO_TMEM) mbar_wait(wlo_full, 0);
+    // ===== MMA issuer: the whole warp follows the schedule, one elected lane issues =====
+    // (warp-uniform operands keep the descriptors in uniform registers: one UTCHMMA + an
+    // add per MMA, no per-instruction lane waterfall)
+    constexpr uint32_t id1 = idesc_f16(MT, 1);   // GEMM1: B = X, MN-major (m contiguous)
+    constexpr uint32_t id2 = idesc_f16(NP, 0);   // GEMM2: B = X, K-major (K = m)
+    const uint32_t t_g = tmem + C::C_G;
+    const uint64_t dx0 = sdesc(smem_u32(s_x), C::XB, 1024);   // X as MN-major B (GEMM1)
+    const uint64_t dk0 = sdesc(smem_u32(s_x), 16, 1024);      // X as K-major B (GEMM2)
+    const uint64_t dw0 = sdesc(smem_u32(s_wlo), 16, 1024);    // W_lo as K-major A (variant B)
+    mbar_wait(w_ready, 0);
+    if (!WLO_TMEM) mbar_wait(wlo_full, 0);
+    tc_fence_after();
+    auto gemm1 = [&](int j) {
+      const int st = j % C::STAGES, b = j & 1;
+      mbar_wait(&full[st], (j / C::STAGES) & 1);
       tc_fence_after();
-      auto gemm1 = [&](int j) {
-        int st = j % C::STAGES, b = j & 1;
-        mbar_wait(&full[st], (j / C::STAGES) & 1);
-        tc_fence_after();
-        uint32_t xs = smem_u32(s_x + st * C::X_STAGE);
-        uint32_t t_y = tmem + (b ? C::C_Y1 : C::C_Y0);
-#pragma unroll 1
-        for (int kb = 0; kb < NP / 16; ++kb) {   // pass 1: W_hi (TMEM) x X
-          uint64_t bd = sdesc(xs + kb * 2048, C::XB, 1024);
-          mma_ts(t_y, tmem + C::C_WHI + kb * 8, bd, id1, kb > 0);
-        }
-#pragma unroll 1
+      if (elect_one()) {
+        const uint64_t bx = dx0 + (uint64_t)((st * C::X_STAGE) >> 4);
+        const uint32_t t_y = tmem + (b ? C::C_Y1 : C::C_Y0);
+#pragma unroll
+        for (int kb = 0; kb < NP / 16; ++kb)   // pass 1: W_hi (TMEM) x X
+          mma_ts(t_y, tmem + C::C_WHI + kb * 8, bx + (uint64_t)(kb * 128), id1, kb > 0 ? 1u : 0u);
+#pragma unroll
         for (int kb = 0; kb < NP / 16; ++kb) {   // pass 2: W_lo x X
-          uint64_t bd = sdesc(xs + kb * 2048, C::XB, 1024);
-          if (WLO_TMEM) {
-            mma_ts(t_y, tmem + C::C_WLO + kb * 8, bd, id1, 1u);
-          } else {
-            uint32_t ws = smem_u32(s_wlo) + (kb >> 2) * 16384 + (kb & 3) * 32;
-            mma_ss(t_y, sdesc(ws, 16, 1024), bd, id1, 1u);
-          }
+          if (WLO_TMEM)
+            mma_ts(t_y, tmem + C::C_WLO + kb * 8, bx + (uint64_t)(kb * 128), id1, 1u);
+          else
+            mma_ss(t_y, dw0 + (uint64_t)(((kb >> 2) * 16384 + (kb & 3) * 32) >> 4), bx + (uint64_t)(kb * 128), id1, 1u);
         }
         tc_commit(&yfull[b]);
-      };
-      auto gemm2 = [&](int j) {
-        int st = j % C::STAGES, b = j & 1;
-        mbar_wait(&y3ready[b], (j >> 1) & 1);
-        tc_fence_after();
-        uint32_t xs = smem_u32(s_x + st * C::X_STAGE);
-        uint32_t t_y3 = tmem + (b ? C::C_Y1 : C::C_Y0);
-#pragma unroll 1
-        for (int kk = 0; kk < MT / 16; ++kk) {
-          uint64_t bd = sdesc(xs + (kk >> 2) * C::XB + (kk & 3) * 32, 16, 1024);
-          mma_ts(t_g, t_y3 + kk * 8, bd, id2, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc_commit(&empty[st]);
-      };
-      if (nchunk > 0) gemm1(0);
-      for (int j = 0; j < nchunk; ++j) {
-        if (j + 1 < nchunk) gemm1(j + 1);
-        gemm2(j);
       }
-      tc_commit(gdone);
+      __syncwarp();
+    };
+    auto gemm2 = [&](int j) {
+      const int st = j % C::STAGES, b = j & 1;
+      mbar_wait(&y3ready[b], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t bk = dk0 + (uint64_t)((st * C::X_STAGE) >> 4);
+        const uint32_t t_y3 = tmem + (b ? C::C_Y1 : C::C_Y0);
+#pragma unroll
+        for (int kk = 0; kk < MT / 16; ++kk)
+          mma_ts(t_g, t_y3 + kk * 8, bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2,
+                 (j > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(&empty[st]);
+      }
+      __syncwarp();
+    };
+    if (nchunk > 0) gemm1(0);
+    for (int j = 0; j < nchunk; ++j) {
+      if (j + 1 < nchunk) gemm1(j + 1);
+      gemm2(j);
     }
+    if (elect_one()) tc_commit(gdone);
+    __syncwarp();
   } else {
     // ===== epilogue warps (128 threads, thread <-> TMEM lane <-> tile row) =====
     const int q = warp & 3;

@@ -125,7 +125,23 @@ def _np_ptr(a, ctype):
     return a.ctypes.data_as(_P(ctype)) if a is not None else None
 
 
+def _point_to_torch_nccl():
+    """liboica dlopens libnccl.so.2; prefer the copy torch ships (same process, same version)."""
+    if os.environ.get("OICA_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl
+        for d in nvidia.nccl.__path__:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                os.environ["OICA_NCCL_LIB"] = p
+                return
+    except Exception:
+        pass
+
+
 def nccl_unique_id() -> bytes:
+    _point_to_torch_nccl()
     buf = C.create_string_buffer(128)
     _check(lib().oica_nccl_unique_id(buf))
     return buf.raw
@@ -172,6 +188,8 @@ class Context:
 
     def __init__(self, device: int = 0, precision: int = PREC_AUTO, rank: int = 0, world: int = 1,
                  shard_mode: int = SHARD_L, stream=None, nccl_id: Optional[bytes] = None):
+        if world > 1:
+            _point_to_torch_nccl()
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         cfg = Config(device, rank, world, shard_mode, precision, 0,
                      C.c_void_p(stream.cuda_stream if stream is not None else 0),

@@ -47,6 +47,12 @@ def test_create_without_device_fails_cleanly():
     assert e.value.name in ("CUDA", "UNSUPPORTED_DEVICE")
 
 
+def test_nccl_is_loadable_and_makes_unique_ids():
+    """The L/M-shard exchange dlopens NCCL; ncclGetUniqueId needs no GPU."""
+    a, b = oica.nccl_unique_id(), oica.nccl_unique_id()
+    assert len(a) == 128 and a != b
+
+
 def _unit(v):
     v = np.asarray(v, dtype=np.float64)
     return v / np.linalg.norm(v)
