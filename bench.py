@@ -192,7 +192,8 @@ def run_oica(args, cfg):
         dist.broadcast_object_list(box, src=0)
         nid = box[0]
     stream = torch.cuda.Stream(device=dev)
-    prec = {"auto": oica.PREC_AUTO, "fp32": oica.PREC_FP32, "tc": oica.PREC_TC}[args.precision]
+    prec = {"auto": oica.PREC_AUTO, "fp32": oica.PREC_FP32, "tc": oica.PREC_TC,
+            "tc_split": oica.PREC_TC_SPLIT}[args.precision]
     shard = oica.SHARD_M if args.shard == "m" else oica.SHARD_L
     ctx = oica.Context(local, prec, rank, world, shard, stream=stream, nccl_id=nid)
 
@@ -288,12 +289,16 @@ def run_oica(args, cfg):
 
     peaks = measured_peaks()
     clocks = clk.summary()
-    precision = "tc" if st["precision"] == oica.PREC_TC else "fp32"
+    precision = {oica.PREC_TC: "tc", oica.PREC_TC_SPLIT: "tc_split"}.get(st["precision"], "fp32")
     kern_tflops = st["step_flops"] / (st["step_ms"] / 1e3) / 1e12 if st["step_ms"] > 0 else None
-    if precision == "tc":
+    issued_tflops = st["step_issued_flops"] / (st["step_ms"] / 1e3) / 1e12 if st["step_ms"] > 0 else None
+    if precision.startswith("tc"):
         peak = peaks.get("bf16_tflops_sustained") or 1404.1
-        roof = {"bound": "tensor", "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (fp16 dense = bf16 rate); "
-                                                  "3 fp16 passes per 2 algorithmic GEMMs -> precision roofline = peak*2/3"}
+        passes = 3 if precision == "tc_split" else 2
+        roof = {"bound": "tensor",
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kind::f16 fp16 dense = bf16 rate); "
+                               f"{passes} fp16 MMA passes per 2 algorithmic GEMMs; frac = algorithmic / peak, "
+                               "issued_frac = issued (128-row tiles x padded N, all passes) / peak"}
     else:
         mhz = clocks.get("sm_mhz") or peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1357.0)
         peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
@@ -301,6 +306,8 @@ def run_oica(args, cfg):
     tr = load_traffic(cfg.name, precision)
     roof.update({"achieved": kern_tflops, "peak": peak, "unit": "TFLOP/s",
                  "frac": (kern_tflops / peak) if kern_tflops else None,
+                 "issued": issued_tflops, "issued_frac": (issued_tflops / peak) if issued_tflops else None,
+                 "fine_row_frac": st["fine_rows"] / st["sum_active"] if st["sum_active"] else None,
                  "traffic": tr.get("dram_bytes_per_launch") if tr else None,
                  "traffic_launch": tr if tr else None,
                  "kernel": "fused fixed-point step (GEMM-cube-GEMM)", "launches": st["step_launches"],
@@ -312,7 +319,7 @@ def run_oica(args, cfg):
     sec_per_comp = ms / 1e3 / args.steps
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-           "vs_baseline": None, "dtype": "f16" if precision == "tc" else "f32", "data": "synthetic",
+           "vs_baseline": None, "dtype": "f16" if precision.startswith("tc") else "f32", "data": "synthetic",
            "config": {"workload": cfg.name, "N": cfg.N, "M": cfg.M, "L": cfg.L, "K": cfg.K, "tol": cfg.tol,
                       "N_out": cfg.N_out, "components_timed": [r["i"] for r in timed],
                       "parallelism": f"{'m' if shard == oica.SHARD_M else 'l'}shard{world}",
@@ -334,7 +341,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="oica", choices=["oica", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tc"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tc", "tc_split"])
     ap.add_argument("--shard", default="l", choices=["l", "m"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -55,9 +55,14 @@ typedef enum {
 
 /* Arithmetic of the fixed-point contraction (the two products of PAPER.md:243-245). */
 typedef enum {
-  OICA_PREC_AUTO = 0,   /* TC where N >= 16 and the kernel supports the shape, else FP32     */
+  OICA_PREC_AUTO = 0,   /* TC when M_global >= 131072, else FP32              */
   OICA_PREC_FP32 = 1,   /* FP32 FFMA on CUDA cores, fp32 accumulate per flush, fp64 slots    */
-  OICA_PREC_TC = 2      /* tcgen05 tensor cores, split-fp16 GEMM1 (W_hi+W_lo) / fp16 GEMM2   */
+  OICA_PREC_TC = 2,     /* tcgen05 tensor cores: fp16 X, one-pass fp16 GEMM1 on w_h =        */
+                        /* fp16(2^4 w)/2^4 with eq. (5)'s -3w evaluated at w_h (consistent),  */
+                        /* rows whose step stagnates near the fp16 floor promoted to the      */
+                        /* two-pass w_h + w_l operand; fp16 GEMM2; fp32 TMEM accumulation,    */
+                        /* fp64 across slots                                   */
+  OICA_PREC_TC_SPLIT = 3 /* as TC with every row two-pass from the start (w to ~2^-22)        */
 } oica_precision;
 
 /* Multi-GPU partitioning.  world == 1 ignores it. */
@@ -111,6 +116,9 @@ typedef struct {
   int64_t sum_active;        /* sum over iterations of active rows                           */
   int32_t precision;         /* precision actually used by the step kernel                  */
   int32_t slots;             /* split-M slots S                                             */
+  double step_issued_flops;  /* flops the step launches issued to the tensor pipe / FMA units,*/
+                             /* padding and second passes included (row tiles x NP)         */
+  int64_t fine_rows;         /* sum over step launches of rows run with the two-pass GEMM1   */
 } oica_stats;
 
 /* ---- lifetime ---------------------------------------------------------------------- */

@@ -48,7 +48,8 @@ __device__ __forceinline__ void project_warp(double (&v)[kMaxV], const double* _
 
 __global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_local, int N,
                             const double* __restrict__ Wacc, int k, double* __restrict__ W64,
-                            uint8_t* __restrict__ state, uint8_t* __restrict__ keep) {
+                            uint8_t* __restrict__ state, uint8_t* __restrict__ keep, uint8_t* __restrict__ fine,
+                            uint8_t fine_init, double* __restrict__ dprev) {
   int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (j >= L_local) return;
@@ -82,16 +83,41 @@ __global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_loc
   if (lane == 0) {
     state[j] = deg ? ST_DEGENERATE : ST_ACTIVE;
     keep[j] = deg ? 0 : 1;
+    if (fine) fine[j] = fine_init;
+    if (dprev) dprev[j] = INFINITY;
   }
 }
 
-// K3: g = sum_s Gp / M - 3 w_old; g <- g - E g; w = g / ||g||;
+__device__ __forceinline__ double slot_sum(SlotPartials Gp, int S, int64_t cap, int ldg, int a, int n) {
+  double acc = 0.0;   // fixed slot order
+  if (Gp.f32) {
+    const float* g = (const float*)Gp.p;
+    for (int s = 0; s < S; ++s) acc += (double)g[((int64_t)s * cap + a) * ldg + n];
+  } else {
+    const double* g = (const double*)Gp.p;
+    for (int s = 0; s < S; ++s) acc += g[((int64_t)s * cap + a) * ldg + n];
+  }
+  return acc;
+}
+
+// coordinate n of the point the contraction used for active row a (master value w64 if none)
+__device__ __forceinline__ double eval_coord(EvalPoint ev, int a, int n, double w64) {
+  int64_t i = (int64_t)a * ev.ld + n;
+  if (ev.hi) return ((double)__half2float(ev.hi[i]) + (ev.lo ? (double)__half2float(ev.lo[i]) : 0.0)) * 0.0625;
+  if (ev.f32) return (double)ev.f32[i];
+  return w64;
+}
+
+// K3: g = sum_s Gp / M - 3 w_e; g <- g - E g; w = g / ||g||;
 // d = 1 - |w . w_old| as 0.5 ||w - s w_old||^2 (A1/A2); converged iff d <= tol.
-__global__ void k_epilogue(const double* __restrict__ Gp, const double* __restrict__ s4p, int S, int64_t cap,
-                           int ldg, const int* __restrict__ act, int L_act, const double* __restrict__ Wacc,
+// w_e is the operand the contraction was evaluated at (the whole of eq. (5) at
+// one point, so the map keeps its vanishing tangent Jacobian at the fixed points); w_old is
+// the fp64 master row.
+__global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int S, int64_t cap, int ldg,
+                           EvalPoint ev, const int* __restrict__ act, int L_act, const double* __restrict__ Wacc,
                            int k, int N, double M, double tol, int t, double* __restrict__ W64,
                            double* __restrict__ alpha_old, int* __restrict__ iters, uint8_t* __restrict__ state,
-                           uint8_t* __restrict__ keep) {
+                           uint8_t* __restrict__ keep, Promotion pr) {
   int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   int lane = threadIdx.x & 31;
   if (a >= L_act) return;
@@ -101,14 +127,15 @@ __global__ void k_epilogue(const double* __restrict__ Gp, const double* __restri
 #pragma unroll
   for (int u = 0; u < kMaxV; ++u) {
     int n = lane + 32 * u;
-    double acc = 0.0, w = 0.0;
+    double acc = 0.0, w = 0.0, we = 0.0;
     if (n < N) {
-      for (int s = 0; s < S; ++s) acc += Gp[((int64_t)s * cap + a) * ldg + n];   // fixed slot order
+      acc = slot_sum(Gp, S, cap, ldg, a, n);
       w = W64[(int64_t)l * N + n];
+      we = eval_coord(ev, a, n, w);
     }
     wo[u] = w;
-    s4g += w * acc;
-    g[u] = (n < N) ? acc / M - 3.0 * w : 0.0;            // PAPER.md:244-245 (eq. (5), A3)
+    s4g += we * acc;
+    g[u] = (n < N) ? acc / M - 3.0 * we : 0.0;           // PAPER.md:244-245 (eq. (5), A3)
   }
   double s4 = 0.0;
   if (s4p) {
@@ -151,33 +178,52 @@ __global__ void k_epilogue(const double* __restrict__ Gp, const double* __restri
     alpha_old[l] = s4 / M - 3.0;                          // eq. (2) at w_old (A15)
     state[l] = deg ? ST_DEGENERATE : (conv ? ST_CONVERGED : ST_ACTIVE);
     keep[a] = (deg || conv) ? 0 : 1;
+    if (pr.fine && !deg && !conv) {                       // DESIGN.md §5 precision promotion
+      if (!pr.fine[l] && ((dd <= pr.d_promote && dd > 1e-3 * pr.dprev[l]) || t >= pr.t_force)) pr.fine[l] = 1;
+      pr.dprev[l] = dd;
+    }
   }
 }
 
-// Single-block, order-preserving compaction (deterministic).
+// Single-block, order-preserving compaction (deterministic), stably partitioned into coarse
+// rows followed by fine rows.
 __global__ void __launch_bounds__(1024) k_compact(const int* __restrict__ act_in, const uint8_t* __restrict__ keep,
-                                                  int L_in, int* __restrict__ act_out, int* __restrict__ Lact_out,
-                                                  int* Lact_host) {
-  __shared__ int scan[1024];
+                                                  const uint8_t* __restrict__ fine, int L_in, int* __restrict__ act_out,
+                                                  int* __restrict__ out_dev, int* host_mapped) {
+  __shared__ int sc[1024], sf[1024];
   int t = threadIdx.x;
   int per = (L_in + 1023) / 1024;
   int b = t * per, e = min(L_in, b + per);
-  int cnt = 0;
-  for (int a = b; a < e; ++a) cnt += keep[a] ? 1 : 0;
-  scan[t] = cnt;
+  int cc = 0, cf = 0;
+  for (int a = b; a < e; ++a) {
+    if (!keep[a]) continue;
+    int id = act_in ? act_in[a] : a;
+    if (fine && fine[id]) ++cf; else ++cc;
+  }
+  sc[t] = cc;
+  sf[t] = cf;
   __syncthreads();
   for (int off = 1; off < 1024; off <<= 1) {
-    int v = t >= off ? scan[t - off] : 0;
+    int vc = t >= off ? sc[t - off] : 0, vf = t >= off ? sf[t - off] : 0;
     __syncthreads();
-    scan[t] += v;
+    sc[t] += vc;
+    sf[t] += vf;
     __syncthreads();
   }
-  int pos = scan[t] - cnt;
-  for (int a = b; a < e; ++a)
-    if (keep[a]) act_out[pos++] = act_in ? act_in[a] : a;
+  const int n_coarse = sc[1023];
+  int pc = sc[t] - cc, pf = n_coarse + sf[t] - cf;
+  for (int a = b; a < e; ++a) {
+    if (!keep[a]) continue;
+    int id = act_in ? act_in[a] : a;
+    if (fine && fine[id]) act_out[pf++] = id; else act_out[pc++] = id;
+  }
   if (t == 1023) {
-    *Lact_out = scan[1023];
-    if (Lact_host) *(volatile int*)Lact_host = scan[1023];
+    out_dev[0] = n_coarse + sf[1023];
+    out_dev[1] = n_coarse;
+    if (host_mapped) {
+      ((volatile int*)host_mapped)[0] = n_coarse + sf[1023];
+      ((volatile int*)host_mapped)[1] = n_coarse;
+    }
   }
 }
 
@@ -192,42 +238,43 @@ __global__ void k_operand_f32(const int* __restrict__ act, const int* __restrict
 // Split fp16 operand: w is scaled by 2^4 (|w| <= 1 -> <= 16) so most w_lo stay normal fp16;
 // hi = fp16(2^4 w), lo = fp16(2^4 w - hi).  hi + lo = 2^4 w to ~2^-22 relative (absolute error
 // <= 3e-8 / 16 per coordinate from lo subnormals); both GEMM1 passes share one accumulator.
+// Coarse rows (fine[l] == 0) get lo = 0 (their contraction is the one-pass w_h product).
 __global__ void k_operand_f16x2(const int* __restrict__ act, const int* __restrict__ Lact, int cap,
-                                const double* __restrict__ W64, int N, int NP, __half* __restrict__ Whi,
-                                __half* __restrict__ Wlo) {
+                                const double* __restrict__ W64, int N, int NP, const uint8_t* __restrict__ fine,
+                                __half* __restrict__ Whi, __half* __restrict__ Wlo) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int a = (int)(idx / NP), n = (int)(idx % NP);
   if (a >= cap || a >= *Lact) return;
-  double w = n < N ? W64[(int64_t)act[a] * N + n] * 16.0 : 0.0;
+  int l = act[a];
+  double w = n < N ? W64[(int64_t)l * N + n] * 16.0 : 0.0;
   __half hi = __double2half(w);
-  __half lo = __double2half(w - (double)__half2float(hi));
+  __half lo = (fine && !fine[l]) ? __double2half(0.0) : __double2half(w - (double)__half2float(hi));
   Whi[idx] = hi;
-  Wlo[idx] = lo;
+  if (Wlo) Wlo[idx] = lo;
 }
 
-__global__ void k_slot_reduce(const double* __restrict__ Gp, const double* __restrict__ s4p, int S, int64_t cap,
-                              int ldg, int L, int N, double* __restrict__ G_out, int ldo, double* __restrict__ s4_out) {
+__global__ void k_slot_reduce(SlotPartials Gp, const double* __restrict__ s4p, int S, int64_t cap, int ldg, int L,
+                              int N, double* __restrict__ G_out, int ldo, double* __restrict__ s4_out) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int a = (int)(idx / (N + 1)), n = (int)(idx % (N + 1));
   if (a >= L) return;
   double acc = 0.0;
   if (n < N) {
-    for (int s = 0; s < S; ++s) acc += Gp[((int64_t)s * cap + a) * ldg + n];
-    G_out[(int64_t)a * ldo + n] = acc;
+    G_out[(int64_t)a * ldo + n] = slot_sum(Gp, S, cap, ldg, a, n);
   } else if (s4p && s4_out) {
     for (int s = 0; s < S; ++s) acc += s4p[(int64_t)s * cap + a];
     s4_out[a] = acc;
   }
 }
 
-// s4 = w . G_raw (identity sum_m y^3 (w.x) = sum_m y^4), rows by position; one warp per row.
-__global__ void k_s4_from_g(const double* __restrict__ W, const double* __restrict__ G, int ldg, int L, int N,
-                            double* __restrict__ s4) {
+// s4 = w_e . G_raw (identity sum_m y^3 (w_e.x) = sum_m y^4), rows by position; one warp per row.
+__global__ void k_s4_from_g(EvalPoint ev, const double* __restrict__ W, const double* __restrict__ G, int ldg, int L,
+                            int N, double* __restrict__ s4) {
   int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   int lane = threadIdx.x & 31;
   if (a >= L) return;
   double v = 0.0;
-  for (int n = lane; n < N; n += 32) v += W[(int64_t)a * N + n] * G[(int64_t)a * ldg + n];
+  for (int n = lane; n < N; n += 32) v += eval_coord(ev, a, n, W[(int64_t)a * N + n]) * G[(int64_t)a * ldg + n];
   v = warp_sum(v);
   if (lane == 0) s4[a] = v;
 }
@@ -235,25 +282,27 @@ __global__ void k_s4_from_g(const double* __restrict__ W, const double* __restri
 }  // namespace
 
 int launch_cand_init(cudaStream_t st, uint64_t seed, int i, int64_t id_base, int64_t L_local, int N,
-                     const double* Wacc, int k, double* W64, uint8_t* state, uint8_t* keep) {
+                     const double* Wacc, int k, double* W64, uint8_t* state, uint8_t* keep, uint8_t* fine,
+                     uint8_t fine_init, double* dprev) {
   int64_t threads = L_local * 32;
-  k_cand_init<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(seed, i, id_base, L_local, N, Wacc, k, W64, state, keep);
+  k_cand_init<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(seed, i, id_base, L_local, N, Wacc, k, W64, state, keep,
+                                                                fine, fine_init, dprev);
   return 1;
 }
 
-int launch_epilogue(cudaStream_t st, const double* Gp, const double* s4p, int S, int64_t cap, int ldg,
+int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, EvalPoint ev,
                     const int* act, int L_act, const double* Wacc, int k, int N, double M, double tol, int t,
-                    double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep) {
+                    double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep, Promotion pr) {
   if (L_act <= 0) return 0;
   int64_t threads = (int64_t)L_act * 32;
-  k_epilogue<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, act, L_act, Wacc, k, N, M, tol,
-                                                               t, W64, alpha_old, iters, state, keep);
+  k_epilogue<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, ev, act, L_act, Wacc, k, N, M,
+                                                               tol, t, W64, alpha_old, iters, state, keep, pr);
   return 1;
 }
 
-int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, int L_in, int* act_out, int* Lact_out,
-                   int* Lact_host) {
-  k_compact<<<1, 1024, 0, st>>>(act_in, keep, L_in, act_out, Lact_out, Lact_host);
+int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, const uint8_t* fine, int L_in,
+                   int* act_out, int* out_dev, int* host_mapped) {
+  k_compact<<<1, 1024, 0, st>>>(act_in, keep, fine, L_in, act_out, out_dev, host_mapped);
   return 1;
 }
 
@@ -266,14 +315,14 @@ int launch_operand_f32(cudaStream_t st, const int* act, const int* Lact, int cap
 }
 
 int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact, int cap, const double* W64, int N, int NP,
-                         __half* Whi, __half* Wlo) {
+                         const uint8_t* fine, __half* Whi, __half* Wlo) {
   if (cap <= 0) return 0;
   int64_t tot = (int64_t)cap * NP;
-  k_operand_f16x2<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(act, Lact, cap, W64, N, NP, Whi, Wlo);
+  k_operand_f16x2<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(act, Lact, cap, W64, N, NP, fine, Whi, Wlo);
   return 1;
 }
 
-int launch_slot_reduce(cudaStream_t st, const double* Gp, const double* s4p, int S, int64_t cap, int ldg, int L,
+int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, int L,
                        int N, double* G_out, int ldo, double* s4_out) {
   if (L <= 0) return 0;
   int64_t tot = (int64_t)L * (N + 1);
@@ -281,9 +330,10 @@ int launch_slot_reduce(cudaStream_t st, const double* Gp, const double* s4p, int
   return 1;
 }
 
-int launch_s4_from_g(cudaStream_t st, const double* W, const double* G, int ldg, int L, int N, double* s4) {
+int launch_s4_from_g(cudaStream_t st, EvalPoint ev, const double* W, const double* G, int ldg, int L, int N,
+                     double* s4) {
   if (L <= 0) return 0;
-  k_s4_from_g<<<(unsigned)ceil_div((int64_t)L * 32, 256), 256, 0, st>>>(W, G, ldg, L, N, s4);
+  k_s4_from_g<<<(unsigned)ceil_div((int64_t)L * 32, 256), 256, 0, st>>>(ev, W, G, ldg, L, N, s4);
   return 1;
 }
 

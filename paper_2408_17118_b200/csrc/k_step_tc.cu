@@ -9,17 +9,22 @@
 // result of a row is independent of the tile it shares (bitwise-deterministic).
 //
 // Arithmetic (DESIGN.md §5 "precision"): X is rounded once to fp16 (11-bit significand, same
-// as TF32); W is split into hi + lo fp16 planes of 2^4 w (GEMM1 = 2 passes: hi X + lo X, so w is
-// represented to ~2^-22 and the fixed-point map stays smooth at the 1e-10 convergence level);
-// y^3 2^-6 is rounded to fp16 for GEMM2 (1 pass).  Accumulation fp32 in TMEM per slot, fp64
-// across slots (K3).  Issued tensor work = 3 fp16 passes per 2 algorithmic GEMMs.
+// as TF32).  The operand row is w_h = fp16(2^4 w) (one GEMM1 pass) or, for "fine" rows, w_h + w_l
+// with w_l = fp16(2^4 w - w_h) (two passes, w to ~2^-22).  Fine rows are grouped at the end of
+// the active list; tiles >= tile_lo0 run the second pass (coarse rows in such a tile carry
+// w_l = 0, which adds exact zeros).  K3 evaluates the -3w term of eq. (5) at the SAME operand
+// (consistent evaluation of the fixed-point map at the rounded point, whose tangent Jacobian
+// vanishes at a fixed point).  y^3 2^-6 is rounded to fp16 for GEMM2 (1 pass).  Accumulation
+// fp32 in TMEM per slot (stored as exact fp32 x 2^6), fp64 across slots (K3).  Issued tensor
+// work = 2 (coarse tile) or 3 (fine tile) fp16 passes per 2 algorithmic GEMMs.
 //
-// Layout (variant A, NP <= 128):  TMEM  [W_hi NP/2 | W_lo NP/2 | G NP | Y0 128 | Y1 128]
-//                                  SMEM  X stages [NP][128] fp16, 128B-swizzled (2 TMA boxes)
-// Layout (variant B, NP = 256):   TMEM  [W_hi 128 | G 256 | Y0 64 | Y1 64]
-//                                  SMEM  W_lo [128][256] (4 K-major SW128 boxes) + X stages [256][64]
-// Warp roles: 0 = TMA producer + TMEM allocator, 1 = MMA issuer (one thread), 2..5 = epilogue
-// (warp w reaches TMEM lanes 32*(w%4)..+31 = rows of the tile).
+// Layout (NP <= 128, MT = 128):  TMEM  [W_hi NP/2 | (W_lo NP/2) | G NP | Y0 128 | Y1 128]
+//                                 SMEM  X stages [NP][128] fp16, 128B-swizzled (2 TMA boxes)
+// Layout (NP = 256, MT = 64):    TMEM  [W_hi 128 | G 256 | Y0 64 | Y1 64]
+//                                 SMEM  (W_lo [128][256], 4 K-major SW128 boxes) + X stages [256][64]
+// (W_lo parts only in the LO-capable instantiation, launched when the list has fine rows.)
+// Warp roles: 0 = TMA producer + TMEM allocator, 1 = MMA issuer (one elected lane), 2..5 =
+// epilogue (warp w reaches TMEM lanes 32*(w%4)..+31 = rows of the tile).
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -136,28 +141,32 @@ __host__ __device__ constexpr uint32_t idesc_f16(int N, int b_mn_major) {
   return (1u << 4) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-template <int NP, bool WLO_TMEM>
+template <int NP, bool SPLIT>   // SPLIT = LO-capable layout
 struct Cfg {
-  static constexpr int MT = WLO_TMEM ? 128 : 64;                 // samples per chunk (GEMM1 N)
+  static constexpr bool WIDE = NP > 128;                         // NP = 256 layout
+  static constexpr bool WLO_TMEM = SPLIT && !WIDE;               // W_lo as a TMEM A operand
+  static constexpr bool WLO_SMEM = SPLIT && WIDE;                // W_lo as an SMEM A operand
+  static constexpr int MT = WIDE ? 64 : 128;                     // samples per chunk (GEMM1 N)
   static constexpr int XB = NP * 128;                            // bytes of one [NP][64] swizzled box
   static constexpr int X_STAGE = NP * MT * 2;                    // bytes per X stage
-  static constexpr int WLO_BYTES = WLO_TMEM ? 0 : 128 * NP * 2;  // W_lo in SMEM (variant B)
-  static constexpr int STAGES = (WLO_TMEM ? 196608 : 131072) / X_STAGE >= 8 ? 8 : (WLO_TMEM ? 196608 : 131072) / X_STAGE;
+  static constexpr int WLO_BYTES = WLO_SMEM ? 128 * NP * 2 : 0;
+  static constexpr int X_BUDGET = WLO_SMEM ? 131072 : 196608;
+  static constexpr int STAGES = X_BUDGET / X_STAGE >= 8 ? 8 : X_BUDGET / X_STAGE;
   static constexpr int C_WHI = 0;
-  static constexpr int C_WLO = NP / 2;                           // variant A only
-  static constexpr int C_G = WLO_TMEM ? NP : NP / 2;
+  static constexpr int C_WLO = NP / 2;                           // WLO_TMEM only
+  static constexpr int C_G = WLO_TMEM ? NP : (WIDE ? 128 : NP / 2);
   static constexpr int C_Y0 = C_G + NP;
   static constexpr int C_Y1 = C_Y0 + MT;
   static_assert(C_Y1 + MT <= 512, "TMEM budget");
   static constexpr int SMEM = 1024 + WLO_BYTES + STAGES * X_STAGE + 1024;
 };
 
-template <int NP, bool WLO_TMEM>
+template <int NP, bool SPLIT>
 __global__ void __launch_bounds__(192, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
           const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_act, int64_t M, int64_t slot_len,
-          double* __restrict__ Gp, int64_t cap, int n_tiles) {
-  using C = Cfg<NP, WLO_TMEM>;
+          float* __restrict__ Gp, int64_t cap, int n_tiles, int tile_lo0) {
+  using C = Cfg<NP, SPLIT>;
   constexpr int MT = C::MT;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -179,6 +188,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const int64_t m_begin = (int64_t)s * slot_len;
   const int64_t m_end = min(M, m_begin + slot_len);
   const int nchunk = (int)ceil_div(m_end - m_begin, MT);
+  const bool lo_pass = SPLIT && tile >= tile_lo0;   // CTA-uniform
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
@@ -208,7 +218,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   if (warp == 0) {
     // ===== TMA producer =====
     if (lane == 0) {
-      if (!WLO_TMEM) {
+      if (C::WLO_SMEM && lo_pass) {
         mbar_expect_tx(wlo_full, C::WLO_BYTES);
         for (int kb = 0; kb < NP / 64; ++kb) tma_load_2d(s_wlo + kb * 16384, &tmWlo, wlo_full, kb * 64, row0);
       }
@@ -232,7 +242,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     const uint64_t dk0 = sdesc(smem_u32(s_x), 16, 1024);      // X as K-major B (GEMM2)
     const uint64_t dw0 = sdesc(smem_u32(s_wlo), 16, 1024);    // W_lo as K-major A (variant B)
     mbar_wait(w_ready, 0);
-    if (!WLO_TMEM) mbar_wait(wlo_full, 0);
+    if (C::WLO_SMEM && lo_pass) mbar_wait(wlo_full, 0);
     tc_fence_after();
     auto gemm1 = [&](int j) {
       const int st = j % C::STAGES, b = j & 1;
@@ -244,12 +254,15 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
         for (int kb = 0; kb < NP / 16; ++kb)   // pass 1: W_hi (TMEM) x X
           mma_ts(t_y, tmem + C::C_WHI + kb * 8, bx + (uint64_t)(kb * 128), id1, kb > 0 ? 1u : 0u);
+        if (lo_pass) {
 #pragma unroll
-        for (int kb = 0; kb < NP / 16; ++kb) {   // pass 2: W_lo x X
-          if (WLO_TMEM)
-            mma_ts(t_y, tmem + C::C_WLO + kb * 8, bx + (uint64_t)(kb * 128), id1, 1u);
-          else
-            mma_ss(t_y, dw0 + (uint64_t)(((kb >> 2) * 16384 + (kb & 3) * 32) >> 4), bx + (uint64_t)(kb * 128), id1, 1u);
+          for (int kb = 0; kb < NP / 16; ++kb) {   // pass 2: W_lo x X
+            if (C::WLO_TMEM)
+              mma_ts(t_y, tmem + C::C_WLO + kb * 8, bx + (uint64_t)(kb * 128), id1, 1u);
+            else
+              mma_ss(t_y, dw0 + (uint64_t)(((kb >> 2) * 16384 + (kb & 3) * 32) >> 4), bx + (uint64_t)(kb * 128), id1,
+                     1u);
+          }
         }
         tc_commit(&yfull[b]);
       }
@@ -294,7 +307,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = ok ? __ldg(wh + c + k) : 0u;
         tmem_st8(tmem + lane_off + C::C_WHI + c, v);
-        if (WLO_TMEM) {
+        if (C::WLO_TMEM && lo_pass) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) v[k] = ok ? __ldg(wl + c + k) : 0u;
           tmem_st8(tmem + lane_off + C::C_WLO + c, v);
@@ -335,10 +348,10 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       tc_fence_before();
       mbar_arrive(&y3ready[b]);
     }
-    // G (fp32, scaled 2^-6) -> fp64 slot partial
+    // G (fp32, scaled 2^-6) -> fp32 slot partial (x 2^6: exact)
     mbar_wait(gdone, 0);
     tc_fence_after();
-    double* out = Gp + ((int64_t)s * cap + row) * NP;
+    float* out = Gp + ((int64_t)s * cap + row) * NP;
     bool ok = row < L_act && nchunk > 0;
 #pragma unroll 1
     for (int c = 0; c < NP; c += 32) {
@@ -348,11 +361,11 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       if (ok) {
 #pragma unroll
         for (int k = 0; k < 32; ++k)
-          if (NP % 32 == 0 || c + k < NP) out[c + k] = (double)__uint_as_float(v[k]) * 64.0;
+          if (NP % 32 == 0 || c + k < NP) out[c + k] = __uint_as_float(v[k]) * 64.0f;
       }
     }
     if (row < L_act && nchunk == 0)
-      for (int c = 0; c < NP; ++c) out[c] = 0.0;
+      for (int c = 0; c < NP; ++c) out[c] = 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -393,19 +406,38 @@ CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld,
   return m;
 }
 
-template <int NP, bool A>
+template <int NP, bool SPLIT>
 void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                    int L_act, int64_t slot_len, int S, double* Gp, int64_t cap) {
-  using C = Cfg<NP, A>;
+                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0) {
+  using C = Cfg<NP, SPLIT>;
   static bool attr = false;
   if (!attr) {
-    OICA_CUDA(cudaFuncSetAttribute(k_step_tc<NP, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    OICA_CUDA(cudaFuncSetAttribute(k_step_tc<NP, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
   CUtensorMap tx = make_map(Xh, NP, ldx, ldx, NP);
-  CUtensorMap tw = make_map(Wlo, cap, NP, NP, 128);
+  CUtensorMap tw = tx;
+  if (C::WLO_SMEM) tw = make_map(Wlo, cap, NP, NP, 128);
   int n_tiles = (int)ceil_div(L_act, 128);
-  k_step_tc<NP, A><<<(unsigned)(n_tiles * S), 192, C::SMEM, st>>>(tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_tiles);
+  k_step_tc<NP, SPLIT><<<(unsigned)(n_tiles * S), 192, C::SMEM, st>>>(tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap,
+                                                                       n_tiles, tile_lo0);
+}
+
+template <bool SPLIT>
+void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi, const __half* Wlo,
+               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0) {
+  switch (NP) {
+    case 16: launch_variant<16, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 32: launch_variant<32, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 48: launch_variant<48, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 64: launch_variant<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 80: launch_variant<80, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 96: launch_variant<96, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 112: launch_variant<112, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 128: launch_variant<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 256: launch_variant<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
+  }
 }
 
 __global__ void k_x_prepare_f16(const float* __restrict__ X, int64_t ld, int N, int64_t M, int NP, int64_t ldx,
@@ -423,22 +455,12 @@ bool tc_supported(int N) { return N >= 1 && N <= 256; }
 int tc_np(int N) { return N <= 128 ? (int)round_up(N < 16 ? 16 : N, 16) : 256; }
 
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
-                   const __half* Wlo, int L_act, int64_t slot_len, int S, int flush, double* Gp, double* s4p,
-                   int64_t cap, int num_sms) {
-  (void)flush; (void)s4p; (void)num_sms;
+                   const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap) {
   if (L_act <= 0) return 0;
-  switch (NP) {
-    case 16: launch_variant<16, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
-    case 32: launch_variant<32, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
-    case 48: launch_variant<48, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
-    case 64: launch_variant<64, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
-    case 80: launch_variant<80, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
-    case 96: launch_variant<96, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
-    case 112: launch_variant<112, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
-    case 128: launch_variant<128, true>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
-    case 256: launch_variant<256, false>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap); break;
-    default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
-  }
+  if (n_coarse < L_act)   // fine rows present: LO-capable layout, second pass from tile n_coarse/128
+    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse / 128);
+  else
+    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0);
   return 1;
 }
 

@@ -10,20 +10,25 @@
 namespace oica {
 
 // ---- K1: candidate draw + projection + normalisation
+// Also resets the per-candidate precision state: fine[j] = fine_init, dprev[j] = +inf.
 int launch_cand_init(cudaStream_t st, uint64_t seed, int i, int64_t id_base, int64_t L_local, int N,
-                     const double* Wacc, int k, double* W64, uint8_t* state, uint8_t* keep);
+                     const double* Wacc, int k, double* W64, uint8_t* state, uint8_t* keep, uint8_t* fine,
+                     uint8_t fine_init, double* dprev);
 
 // ---- K4: order-preserving compaction of the active set
-// act_in == nullptr means the identity list.  Writes act_out, *Lact_out_dev and *Lact_host.
-int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, int L_in, int* act_out,
-                   int* Lact_out_dev, int* Lact_host);
+// act_in == nullptr means the identity list.  Kept rows are stably partitioned: coarse rows
+// first, then rows with fine[id] != 0 (fine may be null).  Writes act_out, out_dev[0] = L_act,
+// out_dev[1] = number of coarse rows, and the same two ints to host_mapped (may be null).
+int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, const uint8_t* fine, int L_in,
+                   int* act_out, int* out_dev, int* host_mapped);
 
 // Operand rows for the step kernel, gathered in active order from the fp64 master.
 int launch_operand_f32(cudaStream_t st, const int* act, const int* Lact_dev, int cap, const double* W64,
                        int N, int NP, float* W32);
-// Split-fp16 operand (TC path): hi = fp16(w*2^s), lo = fp16((w*2^s - hi)*2^11), K-major rows.
+// Split-fp16 operand (TC path): hi = fp16(2^4 w), lo = fp16(2^4 w - hi) for fine rows, 0 for
+// coarse rows (fine == null: all rows fine), K-major rows in active order.
 int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact_dev, int cap, const double* W64,
-                         int N, int NP, __half* Whi, __half* Wlo);
+                         int N, int NP, const uint8_t* fine, __half* Whi, __half* Wlo);
 
 // ---- K2b: fused GEMM-cube-GEMM on CUDA cores (PAPER.md:243-245 before the -3B term)
 // Gp[s][a][n] (stride ldg = NP), s4p[s][a] over slots s of slot_len samples.
@@ -31,16 +36,42 @@ int launch_step_simt(cudaStream_t st, const float* X, int64_t ld, int64_t M, int
                      const float* W32, int L_act, int64_t slot_len, int S, int flush,
                      double* Gp, double* s4p, int64_t cap);
 
+// Slot partials of the step kernel: fp64 (SIMT) or fp32 (tensor cores: the exact TMEM value).
+struct SlotPartials {
+  const void* p;
+  bool f32;
+};
+// The point the contraction was evaluated at, rows in ACTIVE order (stride NP): the -3w term
+// and the alpha~ identity use it so eq. (5) is evaluated consistently.
+// f16: (hi + lo) / 2^4 (lo may be null); f32: W32; all null: the fp64 master row.
+struct EvalPoint {
+  const __half* hi;
+  const __half* lo;
+  const float* f32;
+  int ld;
+};
+
 // ---- K3: fp64 epilogue: slot sum, /M - 3w, projection, normalise, convergence
-int launch_epilogue(cudaStream_t st, const double* Gp, const double* s4p, int S, int64_t cap, int ldg,
-                    const int* act, int L_act, const double* Wacc, int k, int N, double M, double tol,
-                    int t, double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep);
+// Precision promotion (TC): an unconverged row becomes fine when its step
+// distance d <= d_promote stagnates (d > 1e-3 d_prev) or t >= t_force.  fine may be null.
+struct Promotion {
+  uint8_t* fine;
+  double* dprev;
+  double d_promote;
+  int t_force;
+};
+int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
+                    EvalPoint ev, const int* act, int L_act, const double* Wacc, int k, int N, double M,
+                    double tol, int t, double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep,
+                    Promotion pr);
 
 // Fixed-order slot sum into G_out (L x ldo) and s4_out (L).
-int launch_slot_reduce(cudaStream_t st, const double* Gp, const double* s4p, int S, int64_t cap, int ldg,
+int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
                        int L, int N, double* G_out, int ldo, double* s4_out);
 
-int launch_s4_from_g(cudaStream_t st, const double* W, const double* G, int ldg, int L, int N, double* s4);
+// s4 = w_eval . G (identity sum_m y^3 (w.x) = sum_m y^4), rows by position.
+int launch_s4_from_g(cudaStream_t st, EvalPoint ev, const double* W, const double* G, int ldg, int L, int N,
+                     double* s4);
 
 // ---- K5: device-side argmax, cluster assignment, exact alpha, merge + accept
 struct SelectWork;  // defined in k_select.cu
@@ -75,9 +106,9 @@ int launch_merge_accept(cudaStream_t st, const RankSummary* all, const double* w
 struct TcPlan;
 bool tc_supported(int N);
 int tc_np(int N);
+// Rows [0, n_coarse) are coarse (GEMM1 on W_hi), the rest fine (W_hi + W_lo).  Gp[s][a][n] fp32.
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
-                   const __half* Wlo, int L_act, int64_t slot_len, int S, int flush, double* Gp,
-                   double* s4p, int64_t cap, int num_sms);
+                   const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap);
 int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP,
                          int64_t ldx, __half* Xh);
 

@@ -46,6 +46,8 @@ constexpr int kMaxSlots = 128;
 constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
 constexpr int64_t kSlotAlign = 128;
 constexpr int64_t kTcMinSamples = 131072;   // OICA_PREC_AUTO switches to tensor cores at this M
+constexpr double kPromoteD = 1e-6;          // TC precision promotion: stagnating d below this ...
+constexpr int kPromoteT = 40;               // ... or t >= this
 
 }  // namespace
 
@@ -73,11 +75,13 @@ struct oica_ctx {
   uint64_t seed = 0;
   int64_t L = 0, Ll = 0, id_base = 0;
   DevBuf<double> W64, alpha_old, Gp, s4p, Gsum, s4sum;
+  DevBuf<float> Gp32;   // TC slot partials
   DevBuf<float> W32;
   DevBuf<__half> Whi, Wlo;
   DevBuf<int> act0, act1, iters, Lact_dev;
-  DevBuf<uint8_t> state, keep;
-  int* Lact_host = nullptr;
+  DevBuf<uint8_t> state, keep, fine;
+  DevBuf<double> dprev;
+  int* Lact_host = nullptr;   // mapped: [L_act, n_coarse]
   DevBuf<double> Wacc;
   // selection
   DevBuf<int> cluster, pc, qc, csize, counts;
@@ -94,6 +98,16 @@ struct oica_ctx {
   size_t ev_used = 0;
 
   int world() const { return cfg.world; }
+  bool tc() const { return precision == OICA_PREC_TC || precision == OICA_PREC_TC_SPLIT; }
+  bool split() const { return precision == OICA_PREC_TC_SPLIT; }
+  SlotPartials partials() const { return tc() ? SlotPartials{Gp32.p, true} : SlotPartials{Gp.p, false}; }
+  EvalPoint eval_point() const {
+    return tc() ? EvalPoint{Whi.p, Wlo.p, nullptr, (int)NP} : EvalPoint{nullptr, nullptr, W32.p, (int)NP};
+  }
+  Promotion promotion() const {
+    return tc() ? Promotion{fine.p, dprev.p, kPromoteD, kPromoteT} : Promotion{nullptr, nullptr, 0.0, 0};
+  }
+  const uint8_t* fine_flags() const { return tc() ? fine.p : nullptr; }
   bool mshard() const { return cfg.world > 1 && cfg.shard_mode == OICA_SHARD_M; }
 
   void count(int n) { stats.kernel_launches += n; }
@@ -201,13 +215,16 @@ void ensure_candidate_buffers(oica_ctx* c) {
   c->keep.ensure(Ll);
   c->act0.ensure(Ll);
   c->act1.ensure(Ll);
-  c->Lact_dev.ensure(1);
-  c->Gp.ensure((size_t)c->S * Ll * NP);
-  c->s4p.ensure((size_t)c->S * Ll);
-  if (c->precision == OICA_PREC_TC) {
+  c->Lact_dev.ensure(2);
+  c->fine.ensure(Ll);
+  c->dprev.ensure(Ll);
+  if (c->tc()) {
+    c->Gp32.ensure((size_t)c->S * Ll * NP);
     c->Whi.ensure(Ll * NP);
     c->Wlo.ensure(Ll * NP);
   } else {
+    c->Gp.ensure((size_t)c->S * Ll * NP);
+    c->s4p.ensure((size_t)c->S * Ll);
     c->W32.ensure(Ll * NP);
   }
   if (c->mshard()) {
@@ -234,31 +251,40 @@ void ensure_candidate_buffers(oica_ctx* c) {
 
 // Build the step-kernel operand rows for the active list `act` (count in Lact_dev, <= cap).
 void build_operand(oica_ctx* c, const int* act, int cap) {
-  if (c->precision == OICA_PREC_TC)
-    c->count(launch_operand_f16x2(c->st, act, c->Lact_dev.p, cap, c->W64.p, (int)c->N, (int)c->NP, c->Whi.p, c->Wlo.p));
+  if (c->tc())
+    c->count(launch_operand_f16x2(c->st, act, c->Lact_dev.p, cap, c->W64.p, (int)c->N, (int)c->NP, c->fine.p,
+                                  c->Whi.p, c->Wlo.p));
   else
     c->count(launch_operand_f32(c->st, act, c->Lact_dev.p, cap, c->W64.p, (int)c->N, (int)c->NP, c->W32.p));
 }
 
-// One fused contraction over the active rows (positions 0..L_act-1) into the slots.
-void run_step(oica_ctx* c, int L_act, bool timed) {
+// One fused contraction over the active rows (positions 0..L_act-1; rows >= n_coarse are fine)
+// into the slots.
+void run_step(oica_ctx* c, int L_act, int n_coarse, bool timed) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
     e0 = c->event();
     OICA_CUDA(cudaEventRecord(e0, c->st));
   }
   int n;
-  if (c->precision == OICA_PREC_TC)
-    n = launch_step_tc(c->st, c->Xh.p, c->ldx, c->M, (int)c->NP, c->Whi.p, c->Wlo.p, L_act, c->slot_len, c->S, kFlush,
-                       c->Gp.p, c->s4p.p, c->Ll, c->num_sms);
-  else
+  double issued;
+  if (c->tc()) {
+    n = launch_step_tc(c->st, c->Xh.p, c->ldx, c->M, (int)c->NP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
+                       c->S, c->Gp32.p, c->Ll);
+    int64_t tiles = ceil_div(L_act, 128), lo_tiles = n_coarse < L_act ? tiles - n_coarse / 128 : 0;
+    issued = 128.0 * (double)c->NP * (double)c->M * 2.0 * (2.0 * (double)tiles + (double)lo_tiles);
+    c->stats.fine_rows += L_act - n_coarse;
+  } else {
     n = launch_step_simt(c->st, c->X, c->ld, c->M, (int)c->N, (int)c->NP, c->W32.p, L_act, c->slot_len, c->S, kFlush,
                          c->Gp.p, c->s4p.p, c->Ll);
+    issued = (double)round_up(L_act, 64) * (double)c->NP * (double)c->M * 4.0;
+  }
   OICA_CUDA(cudaGetLastError());
   c->count(n);
   c->stats.step_launches += n;
   c->stats.step_flops += (double)L_act * (4.0 * (double)c->N * (double)c->Mg + 3.0 * (double)c->Mg) *
                          ((double)c->M / (double)c->Mg);
+  c->stats.step_issued_flops += issued;
   if (timed) {
     e1 = c->event();
     OICA_CUDA(cudaEventRecord(e1, c->st));
@@ -288,10 +314,13 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
   for (int k = k_prefix; k < N_out; ++k) {
     const int i = k + 1;  // 1-based component index
     // a1: fresh candidates for this component (A8)
-    c->count(launch_cand_init(st, c->seed, i, c->id_base, c->Ll, N, c->Wacc.p, k, c->W64.p, c->state.p, c->keep.p));
-    c->count(launch_compact(st, nullptr, c->keep.p, (int)c->Ll, c->act0.p, c->Lact_dev.p, c->Lact_host));
+    c->count(launch_cand_init(st, c->seed, i, c->id_base, c->Ll, N, c->Wacc.p, k, c->W64.p, c->state.p, c->keep.p,
+                              c->fine.p, c->split() ? 1 : 0, c->dprev.p));
+    c->count(launch_compact(st, nullptr, c->keep.p, c->fine_flags(), (int)c->Ll, c->act0.p, c->Lact_dev.p,
+                            c->Lact_host));
     OICA_CUDA(cudaStreamSynchronize(st));
-    int L_act = *(volatile int*)c->Lact_host;
+    int L_act = ((volatile int*)c->Lact_host)[0];
+    int n_coarse = ((volatile int*)c->Lact_host)[1];
     int* act = c->act0.p;
     int* act_next = c->act1.p;
     build_operand(c, act, L_act);
@@ -303,31 +332,32 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
       sum_active += L_act;
       c->stats.iterations += 1;
       c->stats.sum_active += L_act;
-      run_step(c, L_act, true);
-      const bool tc = c->precision == OICA_PREC_TC;
-      const double* G = c->Gp.p;
-      const double* s4 = tc ? nullptr : c->s4p.p;   // TC: alpha~ from the identity w . G (K3)
+      run_step(c, L_act, n_coarse, true);
+      const bool tc = c->tc();
+      SlotPartials G = c->partials();
+      const double* s4 = tc ? nullptr : c->s4p.p;   // TC: alpha~ from the identity w_e . G (K3)
       int S = c->S;
       int64_t cap = c->Ll;
       if (c->mshard()) {  // one fp64 allreduce of (G, s4) per iteration
-        c->count(launch_slot_reduce(st, c->Gp.p, tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, L_act, N, c->Gsum.p,
-                                    (int)c->NP, c->s4sum.p));
+        c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, (int)c->NP, L_act, N, c->Gsum.p, (int)c->NP, c->s4sum.p));
         auto& nc = Nccl::get();
         OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_act * c->NP, ncclFloat64, ncclSum, c->comm, st));
         if (!tc) OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_act, ncclFloat64, ncclSum, c->comm, st));
-        G = c->Gsum.p;
+        G = SlotPartials{c->Gsum.p, false};
         s4 = tc ? nullptr : c->s4sum.p;
         S = 1;
         cap = c->Ll;
       }
-      c->count(launch_epilogue(st, G, s4, S, cap, (int)c->NP, act, L_act, c->Wacc.p, k, N, (double)c->Mg, tol, t,
-                               c->W64.p, c->alpha_old.p, c->iters.p, c->state.p, c->keep.p));
-      c->count(launch_compact(st, act, c->keep.p, L_act, act_next, c->Lact_dev.p, c->Lact_host));
+      c->count(launch_epilogue(st, G, s4, S, cap, (int)c->NP, c->eval_point(), act, L_act, c->Wacc.p, k, N,
+                               (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p, c->keep.p,
+                               c->promotion()));
+      c->count(launch_compact(st, act, c->keep.p, c->fine_flags(), L_act, act_next, c->Lact_dev.p, c->Lact_host));
       std::swap(act, act_next);
       if (t < K) build_operand(c, act, L_act);
       check_launch();
       OICA_CUDA(cudaStreamSynchronize(st));
-      L_act = *(volatile int*)c->Lact_host;
+      L_act = ((volatile int*)c->Lact_host)[0];
+      n_coarse = ((volatile int*)c->Lact_host)[1];
       if (t >= K) break;  // ... while t < K and B non-empty (A19)
     }
     // a7: selection and accept
@@ -397,9 +427,10 @@ void set_data_impl(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int
   int req = c->cfg.precision;
   // AUTO: tensor cores once M is large enough that the fp16 rounding noise of the contraction
   // (~2^-12 / sqrt(M) relative in G) sits well below the 1e-10 convergence test.
-  bool tc = (req == OICA_PREC_TC || (req == OICA_PREC_AUTO && M_global >= kTcMinSamples)) && tc_supported((int)N);
-  OICA_REQUIRE(!(req == OICA_PREC_TC && !tc), OICA_ERR_INVALID_ARGUMENT, "tensor-core step unsupported for this N");
-  c->precision = tc ? OICA_PREC_TC : OICA_PREC_FP32;
+  bool want_tc = req == OICA_PREC_TC || req == OICA_PREC_TC_SPLIT;
+  bool tc = (want_tc || (req == OICA_PREC_AUTO && M_global >= kTcMinSamples)) && tc_supported((int)N);
+  OICA_REQUIRE(!(want_tc && !tc), OICA_ERR_INVALID_ARGUMENT, "tensor-core step unsupported for this N");
+  c->precision = tc ? (req == OICA_PREC_TC_SPLIT ? OICA_PREC_TC_SPLIT : OICA_PREC_TC) : OICA_PREC_FP32;
   c->NP = tc ? tc_np((int)N) : (N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256);
   plan_slots(c);
   c->stats.precision = c->precision;
@@ -469,7 +500,7 @@ oica_status oica_create(const oica_config* cfg, oica_ctx** out) {
       OICA_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
       c->own_stream = true;
     }
-    OICA_CUDA(cudaHostAlloc((void**)&c->Lact_host, sizeof(int), cudaHostAllocMapped));
+    OICA_CUDA(cudaHostAlloc((void**)&c->Lact_host, 2 * sizeof(int), cudaHostAllocMapped));
     if (cfg->world > 1) {
       ncclUniqueId id;
       std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
@@ -595,15 +626,15 @@ oica_status oica_fixed_point_step(oica_ctx* c, const double* W_dev, int64_t L, d
     OICA_REQUIRE(W_dev && G_dev && s4_dev && L >= 1 && L <= c->Ll, OICA_ERR_INVALID_ARGUMENT, "bad arguments");
     // stage caller rows through the fp64 master (identity active list)
     OICA_CUDA(cudaMemcpyAsync(c->W64.p, W_dev, sizeof(double) * L * c->N, cudaMemcpyDeviceToDevice, c->st));
-    std::vector<uint8_t> ones((size_t)L, 1);
-    OICA_CUDA(cudaMemcpyAsync(c->keep.p, ones.data(), L, cudaMemcpyHostToDevice, c->st));
-    c->count(launch_compact(c->st, nullptr, c->keep.p, (int)L, c->act0.p, c->Lact_dev.p, nullptr));
+    OICA_CUDA(cudaMemsetAsync(c->keep.p, 1, L, c->st));
+    OICA_CUDA(cudaMemsetAsync(c->fine.p, c->split() ? 1 : 0, L, c->st));   // one precision for all rows
+    c->count(launch_compact(c->st, nullptr, c->keep.p, nullptr, (int)L, c->act0.p, c->Lact_dev.p, nullptr));
     build_operand(c, c->act0.p, (int)L);
-    run_step(c, (int)L, true);
-    bool tc = c->precision == OICA_PREC_TC;
-    c->count(launch_slot_reduce(c->st, c->Gp.p, tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L, (int)c->N,
-                                G_dev, (int)c->N, s4_dev));
-    if (tc) c->count(launch_s4_from_g(c->st, c->W64.p, G_dev, (int)c->N, (int)L, (int)c->N, s4_dev));
+    run_step(c, (int)L, c->split() ? 0 : (int)L, true);
+    bool tc = c->tc();
+    c->count(launch_slot_reduce(c->st, c->partials(), tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L,
+                                (int)c->N, G_dev, (int)c->N, s4_dev));
+    if (tc) c->count(launch_s4_from_g(c->st, c->eval_point(), c->W64.p, G_dev, (int)c->N, (int)L, (int)c->N, s4_dev));
     check_launch();
     c->harvest_events();
   });
@@ -618,7 +649,7 @@ oica_status oica_draw_candidates(oica_ctx* c, int32_t i, const double* W_acc, in
     if (k > 0)
       OICA_CUDA(cudaMemcpyAsync(c->Wacc.p, W_acc, sizeof(double) * k * c->N, cudaMemcpyHostToDevice, c->st));
     c->count(launch_cand_init(c->st, c->seed, i, c->id_base, c->Ll, (int)c->N, c->Wacc.p, k, W_dev, c->state.p,
-                              c->keep.p));
+                              c->keep.p, nullptr, 0, nullptr));
     check_launch();
     OICA_CUDA(cudaStreamSynchronize(c->st));
     c->last_valid = false;

@@ -24,7 +24,7 @@ OK = 0
 STATUS = ["OK", "INVALID_ARGUMENT", "DIMENSION_MISMATCH", "RANK_DEFICIENT", "ALL_CANDIDATES_DEGENERATE",
           "DOMAIN", "STATE", "UNSUPPORTED_DEVICE", "OUT_OF_MEMORY", "CUDA", "NCCL"]
 
-PREC_AUTO, PREC_FP32, PREC_TC = 0, 1, 2
+PREC_AUTO, PREC_FP32, PREC_TC, PREC_TC_SPLIT = 0, 1, 2, 3
 SHARD_L, SHARD_M = 0, 1
 INCLUDE_UNCONVERGED, STOP_ON_GAUSSIANITY, RAW_ARGMAX = 0x1, 0x2, 0x4
 MAX_CLUSTERS = 8
@@ -57,7 +57,8 @@ class Result(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("step_launches", C.c_int64), ("step_ms", C.c_double),
                 ("step_flops", C.c_double), ("iterations", C.c_int64), ("sum_active", C.c_int64),
-                ("precision", C.c_int32), ("slots", C.c_int32)]
+                ("precision", C.c_int32), ("slots", C.c_int32), ("step_issued_flops", C.c_double),
+                ("fine_rows", C.c_int64)]
 
 
 class ClusterRecord(C.Structure):

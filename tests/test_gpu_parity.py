@@ -17,7 +17,8 @@ from paper_2408_17118_b200 import oica
 
 pytestmark = pytest.mark.gpu
 
-PRECISIONS = [oica.PREC_FP32, oica.PREC_AUTO]
+PRECISIONS = [oica.PREC_FP32, oica.PREC_AUTO, oica.PREC_TC, oica.PREC_TC_SPLIT]
+TC_MODES = (oica.PREC_TC, oica.PREC_TC_SPLIT)
 
 
 @functools.lru_cache(maxsize=None)
@@ -123,8 +124,8 @@ LARGE_M = ["p_tc_n32", "p_tc_n128", "p_tc_n256"]      # M >= 131072: AUTO -> ten
 
 
 @pytest.mark.parametrize("name,precision",
-                         [(n, p) for n in SMALL for p in (oica.PREC_FP32, oica.PREC_TC)] +
-                         [(n, oica.PREC_AUTO) for n in LARGE_M])
+                         [(n, p) for n in SMALL for p in (oica.PREC_FP32, *TC_MODES)] +
+                         [(n, p) for n in LARGE_M for p in (oica.PREC_AUTO, oica.PREC_TC_SPLIT)])
 def test_extract_parity(name, precision):
     cfg, ctx = ctx_for(name, precision)
     _, _, X64 = prepared(name)
@@ -133,13 +134,13 @@ def test_extract_parity(name, precision):
     st = ctx.stats()
     used = st["precision"]
     if name in LARGE_M:
-        assert used == oica.PREC_TC
+        assert used in TC_MODES and (precision != oica.PREC_TC_SPLIT or used == oica.PREC_TC_SPLIT)
     assert res.n_extracted == cfg.N_out
     rep = _compare(res, res_or, W_or, X64)
     assert np.abs(res.W @ res.W.T - np.eye(cfg.N_out)).max() < 1e-10
     # the convergence census is exact up to candidates sitting at d ~ tol; at small M the tensor-core
     # path's fp16 rounding noise (~2^-12/sqrt(M) in G) leaves more of them unconverged
-    loose = used == oica.PREC_TC and cfg.M < 131072
+    loose = used in TC_MODES and cfg.M < 131072
     slack = cfg.L // 2 if loose else max(2, cfg.L // 50)
     for k, r in enumerate(res_or):
         assert res.n_degenerate[k] == r.n_degenerate
