@@ -23,11 +23,21 @@
 // Layout (NP = 256, MT = 64):    TMEM  [W_hi 128 | G 256 | Y0 64 | Y1 64]
 //                                 SMEM  (W_lo [128][256], 4 K-major SW128 boxes) + X stages [256][64]
 // (W_lo parts only in the LO-capable instantiation, launched when the list has fine rows.)
+// Y3 is written in place per 32-column group g: y^3 of columns [32g, 32g+32) as fp16 pairs in
+// columns [32g, 32g+16), so the GEMM2 A-operand K-slice kk sits at column 32(kk/2) + 8(kk%2).
 // Warp roles: 0 = TMA producer + TMEM allocator, 1 = MMA issuer (one elected lane), 2..5 =
 // epilogue (warp w reaches TMEM lanes 32*(w%4)..+31 = rows of the tile).
+//
+// Cluster multicast (CL = 2, default for NP = 256): the two CTAs of a cluster are two row tiles
+// of the same slot, so they stream the same X chunks; each loads half the rows of every chunk
+// and multicasts it to both (one L2 read feeds two SMs), and a stage is refilled only after
+// both CTAs' MMAs released it (the `empty` barrier counts CL commits, multicast by every CTA).
+// Measured (scripts/tc_variants.py, cfg-4 shape): the X stream alone takes 175 ms per full-L
+// launch without multicast (L2 -> SM at ~6 TB/s paces the kernel) and 95 ms with CL = 2.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -69,6 +79,26 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// multicast variant: the box lands at the same smem offset in every CTA of ctaMask, and each
+// destination CTA's mbarrier (same offset) receives the complete_tx of the bytes written there
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -85,6 +115,13 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// arrive on the mbarrier at the same smem offset in every CTA of ctaMask once prior MMAs complete
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
                : "memory");
 }
 // D[tmem] (+)= A[smem desc] * B[smem desc]
@@ -161,13 +198,18 @@ struct Cfg {
   static constexpr int SMEM = 1024 + WLO_BYTES + STAGES * X_STAGE + 1024;
 };
 
-template <int NP, bool SPLIT>
-__global__ void __launch_bounds__(192, 1)
+// CL = cluster size sharing each X chunk (multicast); NW = epilogue warps (4 or 8)
+template <int NP, bool SPLIT, int EPI, int CL, int NW>
+__global__ void __launch_bounds__(64 + 32 * NW, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
           const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_act, int64_t M, int64_t slot_len,
-          float* __restrict__ Gp, int64_t cap, int n_tiles, int tile_lo0) {
+          float* __restrict__ Gp, int64_t cap, int n_tiles, int tile_lo0, int order, int S_) {
   using C = Cfg<NP, SPLIT>;
   constexpr int MT = C::MT;
+  // MODE 0 = the step; timing experiments (scripts/tc_variants.py): 3 = no
+  // epilogue (MMA + data), 4 = GEMM1 only, 5 = GEMM2 only, 6 = no MMA (X streaming only)
+  constexpr int MODE = EPI;
+  constexpr int EPI_ARRIVALS = 32 * NW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* s_wlo = smem;
@@ -183,23 +225,25 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   uint32_t* tmem_slot = (uint32_t*)(gdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x % n_tiles, s = blockIdx.x / n_tiles;
+  const int tile = order ? blockIdx.x / S_ : blockIdx.x % n_tiles, s = order ? blockIdx.x % S_ : blockIdx.x / n_tiles;
   const int row0 = tile * 128;
   const int64_t m_begin = (int64_t)s * slot_len;
   const int64_t m_end = min(M, m_begin + slot_len);
   const int nchunk = (int)ceil_div(m_end - m_begin, MT);
   const bool lo_pass = SPLIT && tile >= tile_lo0;   // CTA-uniform
 
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
+  static_assert(CL == 1 || (NP / CL) % 8 == 0, "multicast slices must be whole 8-row swizzle atoms");
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], CL);   // released by the MMA commit of every CTA that shares the stage
     }
     mbar_init(wlo_full, 1);
-    mbar_init(w_ready, 128);
+    mbar_init(w_ready, EPI_ARRIVALS);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&yfull[b], 1);
-      mbar_init(&y3ready[b], 128);
+      mbar_init(&y3ready[b], EPI_ARRIVALS);
     }
     mbar_init(gdone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -211,7 +255,10 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync_all();   // peers multicast into this CTA's barriers: all must be initialised
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -222,14 +269,26 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         mbar_expect_tx(wlo_full, C::WLO_BYTES);
         for (int kb = 0; kb < NP / 64; ++kb) tma_load_2d(s_wlo + kb * 16384, &tmWlo, wlo_full, kb * 64, row0);
       }
+      // CL > 1: this CTA loads rows [crank*SR, (crank+1)*SR) of every chunk and multicasts them
+      // to the whole cluster (all CTAs of a cluster share the slot, hence the chunks)
+      constexpr int SR = NP / CL;
+      const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
       for (int j = 0; j < nchunk; ++j) {
         int st = j % C::STAGES;
         if (j >= C::STAGES) mbar_wait(&empty[st], ((j / C::STAGES) - 1) & 1);
         mbar_expect_tx(&full[st], C::X_STAGE);
         int m0 = (int)(m_begin + (int64_t)j * MT);
         uint8_t* dst = s_x + st * C::X_STAGE;
-        for (int h = 0; h < MT / 64; ++h) tma_load_2d(dst + h * C::XB, &tmX, &full[st], m0 + 64 * h, 0);
+        for (int h = 0; h < MT / 64; ++h) {
+          if (CL == 1)
+            tma_load_2d(dst + h * C::XB, &tmX, &full[st], m0 + 64 * h, 0);
+          else
+            tma_load_2d_mc(dst + h * C::XB + crank * SR * 128, &tmX, &full[st], m0 + 64 * h, crank * SR, kMask);
+        }
       }
+      if (CL > 1)   // peers' releases of the last stages must land before this CTA may exit
+        for (int j = nchunk > C::STAGES ? nchunk - C::STAGES : 0; j < nchunk; ++j)
+          mbar_wait(&empty[j % C::STAGES], (j / C::STAGES) & 1);
     }
   } else if (warp == 1) {
     // ===== MMA issuer: the whole warp follows the schedule, one elected lane issues =====
@@ -248,6 +307,11 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const int st = j % C::STAGES, b = j & 1;
       mbar_wait(&full[st], (j / C::STAGES) & 1);
       tc_fence_after();
+      if (MODE == 5 || MODE == 6) {   // experiment: GEMM2 only / no MMA
+        if (elect_one()) tc_commit(&yfull[b]);
+        __syncwarp();
+        return;
+      }
       if (elect_one()) {
         const uint64_t bx = dx0 + (uint64_t)((st * C::X_STAGE) >> 4);
         const uint32_t t_y = tmem + (b ? C::C_Y1 : C::C_Y0);
@@ -272,14 +336,24 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const int st = j % C::STAGES, b = j & 1;
       mbar_wait(&y3ready[b], (j >> 1) & 1);
       tc_fence_after();
+      if (MODE == 4 || MODE == 6) {   // experiment: GEMM1 only / no MMA
+        if (elect_one()) {
+          if (CL > 1) tc_commit_mc(&empty[st], kMask); else tc_commit(&empty[st]);
+        }
+        __syncwarp();
+        return;
+      }
       if (elect_one()) {
         const uint64_t bk = dk0 + (uint64_t)((st * C::X_STAGE) >> 4);
         const uint32_t t_y3 = tmem + (b ? C::C_Y1 : C::C_Y0);
 #pragma unroll
         for (int kk = 0; kk < MT / 16; ++kk)
-          mma_ts(t_g, t_y3 + kk * 8, bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2,
+          mma_ts(t_g, t_y3 + (kk >> 1) * 32 + (kk & 1) * 8, bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2,
                  (j > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(&empty[st]);
+        if (CL > 1)
+          tc_commit_mc(&empty[st], kMask);
+        else
+          tc_commit(&empty[st]);
       }
       __syncwarp();
     };
@@ -291,8 +365,10 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (elect_one()) tc_commit(gdone);
     __syncwarp();
   } else {
-    // ===== epilogue warps (128 threads, thread <-> TMEM lane <-> tile row) =====
-    const int q = warp & 3;
+    // ===== epilogue warps (NW warps; warp w reaches TMEM lanes 32*(w%4)..+31 = tile rows; the
+    // NW/4 warps of one lane quadrant split the columns in 32-column groups) =====
+    constexpr int NH = NW / 4;
+    const int q = warp & 3, h = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     const int row = row0 + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
@@ -302,7 +378,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const uint32_t* wl = (const uint32_t*)(Wlo + (int64_t)row * NP);
       bool ok = row < L_act;
 #pragma unroll 1
-      for (int c = 0; c < NP / 2; c += 8) {   // NP/2 is a multiple of 8 columns
+      for (int c = 8 * h; c < NP / 2; c += 8 * NH) {   // NP/2 is a multiple of 8 columns
         uint32_t v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = ok ? __ldg(wh + c + k) : 0u;
@@ -317,32 +393,36 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       tc_fence_before();
       mbar_arrive(w_ready);
     }
+    // Y group g = columns [32g, 32g+32) -> y^3 2^-6 as fp16 pairs in columns [32g, 32g+16)
+    // (in place, inside the group this warp owns: the A operand K-slice kk of GEMM2 sits at
+    // column 32*(kk/2) + 8*(kk%2))
+    constexpr int NG = MT / 32 / NH;   // groups per warp
     for (int j = 0; j < nchunk; ++j) {
       const int b = j & 1;
       const uint32_t t_y = tmem + lane_off + (b ? C::C_Y1 : C::C_Y0);
       mbar_wait(&yfull[b], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t packed[MT / 2];
+      if (MODE >= 3) {   // experiment: no TMEM traffic (MMA pipeline upper bound)
+        tc_fence_before();
+        mbar_arrive(&y3ready[b]);
+        continue;
+      }
+      uint32_t v[NG][32];
 #pragma unroll
-      for (int c = 0; c < MT; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(t_y + c, v);
-        tmem_wait_ld();
+      for (int u = 0; u < NG; ++u) tmem_ld32(t_y + 32 * (h + NH * u), v[u]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int u = 0; u < NG; ++u) {
+        uint32_t pk[16];
 #pragma unroll
         for (int k = 0; k < 32; k += 2) {
           // accumulator = 2^4 y  ->  2^-6 y^3 = acc^3 2^-18
-          float a0 = __uint_as_float(v[k]), a1 = __uint_as_float(v[k + 1]);
+          float a0 = __uint_as_float(v[u][k]), a1 = __uint_as_float(v[u][k + 1]);
           float c0 = a0 * a0 * a0 * 0x1.0p-18f, c1 = a1 * a1 * a1 * 0x1.0p-18f;
-          __half2 h = __floats2half2_rn(c0, c1);
-          packed[(c + k) / 2] = *reinterpret_cast<uint32_t*>(&h);
+          __half2 hh = __floats2half2_rn(c0, c1);
+          pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
         }
-      }
-#pragma unroll
-      for (int c = 0; c < MT / 2; c += 16) {
-        uint32_t v[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = packed[c + k];
-        tmem_st16(t_y + c, v);   // Y^3 (fp16 pairs) in place: A operand of GEMM2
+        tmem_st16(t_y + 32 * (h + NH * u), pk);   // Y^3 (fp16 pairs): A operand of GEMM2
       }
       tmem_wait_st();
       tc_fence_before();
@@ -354,7 +434,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     float* out = Gp + ((int64_t)s * cap + row) * NP;
     bool ok = row < L_act && nchunk > 0;
 #pragma unroll 1
-    for (int c = 0; c < NP; c += 32) {
+    for (int c = 32 * h; c < NP; c += 32 * NH) {
       uint32_t v[32];
       tmem_ld32(tmem + lane_off + C::C_G + c, v);
       tmem_wait_ld();
@@ -364,11 +444,14 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           if (NP % 32 == 0 || c + k < NP) out[c + k] = __uint_as_float(v[k]) * 64.0f;
       }
     }
-    if (row < L_act && nchunk == 0)
+    if (row < L_act && nchunk == 0 && h == 0)
       for (int c = 0; c < NP; ++c) out[c] = 0.f;
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync_all();
+  else
+    __syncthreads();
   tc_fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
@@ -406,36 +489,78 @@ CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld,
   return m;
 }
 
-template <int NP, bool SPLIT>
-void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0) {
+template <int NP, bool SPLIT, int EPI, int CL, int NW>
+void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
+               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0) {
   using C = Cfg<NP, SPLIT>;
+  auto kern = k_step_tc<NP, SPLIT, EPI, CL, NW>;
   static bool attr = false;
   if (!attr) {
-    OICA_CUDA(cudaFuncSetAttribute(k_step_tc<NP, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    OICA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    if (CL > 1) OICA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
-  CUtensorMap tx = make_map(Xh, NP, ldx, ldx, NP);
+  CUtensorMap tx = make_map(Xh, NP, ldx, ldx, NP / CL);
   CUtensorMap tw = tx;
   if (C::WLO_SMEM) tw = make_map(Wlo, cap, NP, NP, 128);
-  int n_tiles = (int)ceil_div(L_act, 128);
-  k_step_tc<NP, SPLIT><<<(unsigned)(n_tiles * S), 192, C::SMEM, st>>>(tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap,
-                                                                       n_tiles, tile_lo0);
+  int n_tiles = (int)round_up(ceil_div(L_act, 128), CL);   // a cluster = CL tiles of one slot
+  static int order = [] { const char* e = getenv("OICA_TC_ORDER"); return e ? atoi(e) : 0; }();
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(n_tiles * S));
+  lc.blockDim = dim3(64 + 32 * NW);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_tiles, tile_lo0,
+                               CL > 1 ? 0 : order, S));
+}
+
+template <int NP, bool SPLIT, int EPI>
+void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
+                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0) {
+  // Cluster multicast of the X chunks: on by default for the NP = 256 layout,
+  // where X streaming through L2 (~6 TB/s) otherwise paces the kernel; OICA_TC_CL=1|2 overrides.
+  static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
+  const int cl = cl_env ? cl_env : (NP > 128 ? 2 : 1);
+  constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
+  if (cl == 2)
+    launch_cl<NP, SPLIT, EPI, CL2, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0);
+  else
+    launch_cl<NP, SPLIT, EPI, 1, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0);
+}
+
+template <int NP, bool SPLIT>
+void launch_epi(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
+                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0) {
+  static int epi = [] { const char* e = getenv("OICA_TC_EPI"); return e ? atoi(e) : 0; }();
+  switch (epi) {
+    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+  }
 }
 
 template <bool SPLIT>
 void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi, const __half* Wlo,
                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0) {
   switch (NP) {
-    case 16: launch_variant<16, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 32: launch_variant<32, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 48: launch_variant<48, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 64: launch_variant<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 80: launch_variant<80, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 96: launch_variant<96, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 112: launch_variant<112, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 128: launch_variant<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 256: launch_variant<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 64: launch_variant<64, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
   }
 }
