@@ -117,9 +117,10 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
                            EvalPoint ev, const int* __restrict__ act, int L_act, const double* __restrict__ Wacc,
                            int k, int N, double M, double tol, int t, double* __restrict__ W64,
                            double* __restrict__ alpha_old, int* __restrict__ iters, uint8_t* __restrict__ state,
-                           uint8_t* __restrict__ keep, Promotion pr) {
+                           uint8_t* __restrict__ keep, Promotion pr, const int* __restrict__ cnt) {
   int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   int lane = threadIdx.x & 31;
+  if (cnt) L_act = min(L_act, cnt[0]);   // device count when the grid is an upper bound
   if (a >= L_act) return;
   int l = act[a];
   double g[kMaxV], wo[kMaxV];
@@ -189,9 +190,11 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
 // rows followed by fine rows.
 __global__ void __launch_bounds__(1024) k_compact(const int* __restrict__ act_in, const uint8_t* __restrict__ keep,
                                                   const uint8_t* __restrict__ fine, int L_in, int* __restrict__ act_out,
-                                                  int* __restrict__ out_dev, int* host_mapped) {
+                                                  int* out_dev, int* host_mapped, const int* cnt_in, int* hist) {
   __shared__ int sc[1024], sf[1024];
   int t = threadIdx.x;
+  if (cnt_in) L_in = min(L_in, cnt_in[0]);   // may alias out_dev: read before the barrier below
+  __syncthreads();
   int per = (L_in + 1023) / 1024;
   int b = t * per, e = min(L_in, b + per);
   int cc = 0, cf = 0;
@@ -223,6 +226,10 @@ __global__ void __launch_bounds__(1024) k_compact(const int* __restrict__ act_in
     if (host_mapped) {
       ((volatile int*)host_mapped)[0] = n_coarse + sf[1023];
       ((volatile int*)host_mapped)[1] = n_coarse;
+    }
+    if (hist) {
+      hist[0] = n_coarse + sf[1023];
+      hist[1] = n_coarse;
     }
   }
 }
@@ -292,17 +299,18 @@ int launch_cand_init(cudaStream_t st, uint64_t seed, int i, int64_t id_base, int
 
 int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, EvalPoint ev,
                     const int* act, int L_act, const double* Wacc, int k, int N, double M, double tol, int t,
-                    double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep, Promotion pr) {
+                    double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep, Promotion pr,
+                    const int* cnt) {
   if (L_act <= 0) return 0;
   int64_t threads = (int64_t)L_act * 32;
   k_epilogue<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, ev, act, L_act, Wacc, k, N, M,
-                                                               tol, t, W64, alpha_old, iters, state, keep, pr);
+                                                               tol, t, W64, alpha_old, iters, state, keep, pr, cnt);
   return 1;
 }
 
 int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, const uint8_t* fine, int L_in,
-                   int* act_out, int* out_dev, int* host_mapped) {
-  k_compact<<<1, 1024, 0, st>>>(act_in, keep, fine, L_in, act_out, out_dev, host_mapped);
+                   int* act_out, int* out_dev, int* host_mapped, const int* cnt_in, int* hist) {
+  k_compact<<<1, 1024, 0, st>>>(act_in, keep, fine, L_in, act_out, out_dev, host_mapped, cnt_in, hist);
   return 1;
 }
 

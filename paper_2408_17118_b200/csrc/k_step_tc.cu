@@ -10,13 +10,14 @@
 //
 // Arithmetic (DESIGN.md §5 "precision"): X is rounded once to fp16 (11-bit significand, same
 // as TF32).  The operand row is w_h = fp16(2^4 w) (one GEMM1 pass) or, for "fine" rows, w_h + w_l
-// with w_l = fp16(2^4 w - w_h) (two passes, w to ~2^-22).  Fine rows are grouped at the end of
+// with w_l = fp16(2^4 w - w_h) (two passes, w to ~2^-22); fine tiles also run GEMM2 twice, on
+// y^3 2^-6 rounded to fp16 and on its fp16 residual (y^3 to ~2^-22).  Fine rows are grouped at the end of
 // the active list; tiles >= tile_lo0 run the second pass (coarse rows in such a tile carry
 // w_l = 0, which adds exact zeros).  K3 evaluates the -3w term of eq. (5) at the SAME operand
 // (consistent evaluation of the fixed-point map at the rounded point, whose tangent Jacobian
 // vanishes at a fixed point).  y^3 2^-6 is rounded to fp16 for GEMM2 (1 pass).  Accumulation
 // fp32 in TMEM per slot (stored as exact fp32 x 2^6), fp64 across slots (K3).  Issued tensor
-// work = 2 (coarse tile) or 3 (fine tile) fp16 passes per 2 algorithmic GEMMs.
+// work = 2 (coarse tile) or 4 (fine tile) fp16 passes per 2 algorithmic GEMMs.
 //
 // Layout (NP <= 128, MT = 128):  TMEM  [W_hi NP/2 | (W_lo NP/2) | G NP | Y0 128 | Y1 128]
 //                                 SMEM  X stages [NP][128] fp16, 128B-swizzled (2 TMA boxes)
@@ -202,8 +203,8 @@ struct Cfg {
 template <int NP, bool SPLIT, int EPI, int CL, int NW>
 __global__ void __launch_bounds__(64 + 32 * NW, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
-          const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_act, int64_t M, int64_t slot_len,
-          float* __restrict__ Gp, int64_t cap, int n_tiles, int tile_lo0, int order, int S_) {
+          const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_ub, int64_t M, int64_t slot_len,
+          float* __restrict__ Gp, int64_t cap, int n_tiles, int tile_lo0_h, int order, int S_, const int* __restrict__ cnt) {
   using C = Cfg<NP, SPLIT>;
   constexpr int MT = C::MT;
   // MODE 0 = the step; timing experiments (scripts/tc_variants.py): 3 = no
@@ -226,6 +227,11 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = order ? blockIdx.x / S_ : blockIdx.x % n_tiles, s = order ? blockIdx.x % S_ : blockIdx.x / n_tiles;
+  // active-row count and coarse/fine split: from the device counters when the grid was sized
+  // from an upper bound (iterations enqueued without a host round trip)
+  const int L_act = cnt ? min(L_ub, cnt[0]) : L_ub;
+  const int tile_lo0 = cnt ? cnt[1] / 128 : tile_lo0_h;
+  if ((tile - tile % CL) * 128 >= L_act) return;   // cluster-uniform: no barrier was touched
   const int row0 = tile * 128;
   const int64_t m_begin = (int64_t)s * slot_len;
   const int64_t m_end = min(M, m_begin + slot_len);
@@ -350,6 +356,12 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         for (int kk = 0; kk < MT / 16; ++kk)
           mma_ts(t_g, t_y3 + (kk >> 1) * 32 + (kk & 1) * 8, bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2,
                  (j > 0 || kk > 0) ? 1u : 0u);
+        if (lo_pass) {   // fine tile: second GEMM2 pass on the y^3 residual (columns 32g+16..)
+#pragma unroll
+          for (int kk = 0; kk < MT / 16; ++kk)
+            mma_ts(t_g, t_y3 + (kk >> 1) * 32 + 16 + (kk & 1) * 8,
+                   bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2, 1u);
+        }
         if (CL > 1)
           tc_commit_mc(&empty[st], kMask);
         else
@@ -413,7 +425,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       tmem_wait_ld();
 #pragma unroll
       for (int u = 0; u < NG; ++u) {
-        uint32_t pk[16];
+        uint32_t pk[16], pl[16];
 #pragma unroll
         for (int k = 0; k < 32; k += 2) {
           // accumulator = 2^4 y  ->  2^-6 y^3 = acc^3 2^-18
@@ -421,8 +433,14 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           float c0 = a0 * a0 * a0 * 0x1.0p-18f, c1 = a1 * a1 * a1 * 0x1.0p-18f;
           __half2 hh = __floats2half2_rn(c0, c1);
           pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
+          if (SPLIT) {   // residual y^3 2^-6 - hi (fine tiles: GEMM2 second pass)
+            float2 hf = __half22float2(hh);
+            __half2 hl = __floats2half2_rn(c0 - hf.x, c1 - hf.y);
+            pl[k / 2] = *reinterpret_cast<uint32_t*>(&hl);
+          }
         }
         tmem_st16(t_y + 32 * (h + NH * u), pk);   // Y^3 (fp16 pairs): A operand of GEMM2
+        if (lo_pass) tmem_st16(t_y + 32 * (h + NH * u) + 16, pl);
       }
       tmem_wait_st();
       tc_fence_before();
@@ -491,7 +509,7 @@ CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld,
 
 template <int NP, bool SPLIT, int EPI, int CL, int NW>
 void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0) {
+               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt) {
   using C = Cfg<NP, SPLIT>;
   auto kern = k_step_tc<NP, SPLIT, EPI, CL, NW>;
   static bool attr = false;
@@ -518,49 +536,49 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   lc.attrs = at;
   lc.numAttrs = 1;
   OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_tiles, tile_lo0,
-                               CL > 1 ? 0 : order, S));
+                               CL > 1 ? 0 : order, S, cnt));
 }
 
 template <int NP, bool SPLIT, int EPI>
 void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0) {
+                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt) {
   // Cluster multicast of the X chunks: on by default for the NP = 256 layout,
   // where X streaming through L2 (~6 TB/s) otherwise paces the kernel; OICA_TC_CL=1|2 overrides.
   static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
   const int cl = cl_env ? cl_env : (NP > 128 ? 2 : 1);
   constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
   if (cl == 2)
-    launch_cl<NP, SPLIT, EPI, CL2, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0);
+    launch_cl<NP, SPLIT, EPI, CL2, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
   else
-    launch_cl<NP, SPLIT, EPI, 1, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0);
+    launch_cl<NP, SPLIT, EPI, 1, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
 }
 
 template <int NP, bool SPLIT>
 void launch_epi(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0) {
+                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt) {
   static int epi = [] { const char* e = getenv("OICA_TC_EPI"); return e ? atoi(e) : 0; }();
   switch (epi) {
-    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
   }
 }
 
 template <bool SPLIT>
 void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi, const __half* Wlo,
-               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0) {
+               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt) {
   switch (NP) {
-    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 64: launch_variant<64, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
-    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0); break;
+    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 64: launch_variant<64, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
   }
 }
@@ -580,12 +598,13 @@ bool tc_supported(int N) { return N >= 1 && N <= 256; }
 int tc_np(int N) { return N <= 128 ? (int)round_up(N < 16 ? 16 : N, 16) : 256; }
 
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
-                   const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap) {
+                   const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
+                   const int* cnt, bool lo_capable) {
   if (L_act <= 0) return 0;
-  if (n_coarse < L_act)   // fine rows present: LO-capable layout, second pass from tile n_coarse/128
-    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse / 128);
+  if (lo_capable || n_coarse < L_act)   // fine rows (possibly): LO-capable layout, 2nd pass from tile n_coarse/128
+    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse / 128, cnt);
   else
-    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0);
+    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0, cnt);
   return 1;
 }
 

@@ -19,8 +19,10 @@ int launch_cand_init(cudaStream_t st, uint64_t seed, int i, int64_t id_base, int
 // act_in == nullptr means the identity list.  Kept rows are stably partitioned: coarse rows
 // first, then rows with fine[id] != 0 (fine may be null).  Writes act_out, out_dev[0] = L_act,
 // out_dev[1] = number of coarse rows, and the same two ints to host_mapped (may be null).
+// cnt_in (device, may be null): the true L_in (L_in is then an upper bound); hist (may be null):
+// the new [L_act, n_coarse] pair is also appended there.
 int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, const uint8_t* fine, int L_in,
-                   int* act_out, int* out_dev, int* host_mapped);
+                   int* act_out, int* out_dev, int* host_mapped, const int* cnt_in = nullptr, int* hist = nullptr);
 
 // Operand rows for the step kernel, gathered in active order from the fp64 master.
 int launch_operand_f32(cudaStream_t st, const int* act, const int* Lact_dev, int cap, const double* W64,
@@ -34,7 +36,7 @@ int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact_dev, i
 // Gp[s][a][n] (stride ldg = NP), s4p[s][a] over slots s of slot_len samples.
 int launch_step_simt(cudaStream_t st, const float* X, int64_t ld, int64_t M, int N, int NP,
                      const float* W32, int L_act, int64_t slot_len, int S, int flush,
-                     double* Gp, double* s4p, int64_t cap);
+                     double* Gp, double* s4p, int64_t cap, const int* cnt);
 
 // Slot partials of the step kernel: fp64 (SIMT) or fp32 (tensor cores: the exact TMEM value).
 struct SlotPartials {
@@ -63,7 +65,7 @@ struct Promotion {
 int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
                     EvalPoint ev, const int* act, int L_act, const double* Wacc, int k, int N, double M,
                     double tol, int t, double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep,
-                    Promotion pr);
+                    Promotion pr, const int* cnt);
 
 // Fixed-order slot sum into G_out (L x ldo) and s4_out (L).
 int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
@@ -107,8 +109,12 @@ struct TcPlan;
 bool tc_supported(int N);
 int tc_np(int N);
 // Rows [0, n_coarse) are coarse (GEMM1 on W_hi), the rest fine (W_hi + W_lo).  Gp[s][a][n] fp32.
+// L_act / n_coarse size the grid; when cnt (device [L_act, n_coarse]) is given they are upper
+// bounds and the kernel takes the true values from cnt (tiles beyond exit at once).
+// lo_capable: launch the LO-capable layout even if n_coarse == L_act (fine rows may appear).
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
-                   const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap);
+                   const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
+                   const int* cnt, bool lo_capable);
 int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP,
                          int64_t ldx, __half* Xh);
 

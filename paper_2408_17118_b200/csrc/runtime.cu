@@ -48,6 +48,8 @@ constexpr int64_t kSlotAlign = 128;
 constexpr int64_t kTcMinSamples = 131072;   // OICA_PREC_AUTO switches to tensor cores at this M
 constexpr double kPromoteD = 1e-6;          // TC precision promotion: stagnating d below this ...
 constexpr int kPromoteT = 40;               // ... or t >= this
+constexpr int kBatchRows = 2048;            // below this many active rows, iterations are enqueued ...
+constexpr int kBatch = 8;                   // ... this many at a time without a host round trip
 
 }  // namespace
 
@@ -78,7 +80,7 @@ struct oica_ctx {
   DevBuf<float> Gp32;   // TC slot partials
   DevBuf<float> W32;
   DevBuf<__half> Whi, Wlo;
-  DevBuf<int> act0, act1, iters, Lact_dev;
+  DevBuf<int> act0, act1, iters, Lact_dev, hist;
   DevBuf<uint8_t> state, keep, fine;
   DevBuf<double> dprev;
   int* Lact_host = nullptr;   // mapped: [L_act, n_coarse]
@@ -259,36 +261,45 @@ void build_operand(oica_ctx* c, const int* act, int cap) {
 }
 
 // One fused contraction over the active rows (positions 0..L_act-1; rows >= n_coarse are fine)
-// into the slots.
-void run_step(oica_ctx* c, int L_act, int n_coarse, bool timed) {
+// into the slots.  With cnt (device [L_act, n_coarse]) the host values are upper bounds that
+// only size the grid (iterations enqueued without a host round trip).
+void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, bool lo_capable, bool timed) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
     e0 = c->event();
     OICA_CUDA(cudaEventRecord(e0, c->st));
   }
   int n;
-  double issued;
-  if (c->tc()) {
+  if (c->tc())
     n = launch_step_tc(c->st, c->Xh.p, c->ldx, c->M, (int)c->NP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
-                       c->S, c->Gp32.p, c->Ll);
-    int64_t tiles = ceil_div(L_act, 128), lo_tiles = n_coarse < L_act ? tiles - n_coarse / 128 : 0;
-    issued = 128.0 * (double)c->NP * (double)c->M * 2.0 * (2.0 * (double)tiles + (double)lo_tiles);
-    c->stats.fine_rows += L_act - n_coarse;
-  } else {
+                       c->S, c->Gp32.p, c->Ll, cnt, lo_capable);
+  else
     n = launch_step_simt(c->st, c->X, c->ld, c->M, (int)c->N, (int)c->NP, c->W32.p, L_act, c->slot_len, c->S, kFlush,
-                         c->Gp.p, c->s4p.p, c->Ll);
-    issued = (double)round_up(L_act, 64) * (double)c->NP * (double)c->M * 4.0;
-  }
+                         c->Gp.p, c->s4p.p, c->Ll, cnt);
   OICA_CUDA(cudaGetLastError());
   c->count(n);
   c->stats.step_launches += n;
-  c->stats.step_flops += (double)L_act * (4.0 * (double)c->N * (double)c->Mg + 3.0 * (double)c->Mg) *
-                         ((double)c->M / (double)c->Mg);
-  c->stats.step_issued_flops += issued;
   if (timed) {
     e1 = c->event();
     OICA_CUDA(cudaEventRecord(e1, c->st));
   }
+}
+
+// Work counters of one executed iteration with L_act rows, n_coarse of them coarse.
+void account_iteration(oica_ctx* c, int L_act, int n_coarse) {
+  double issued;
+  if (c->tc()) {
+    int64_t tiles = ceil_div(L_act, 128), lo_tiles = n_coarse < L_act ? tiles - n_coarse / 128 : 0;
+    issued = 128.0 * (double)c->NP * (double)c->M * 2.0 * (2.0 * (double)tiles + 2.0 * (double)lo_tiles);
+    c->stats.fine_rows += L_act - n_coarse;
+  } else {
+    issued = (double)round_up(L_act, 64) * (double)c->NP * (double)c->M * 4.0;
+  }
+  c->stats.iterations += 1;
+  c->stats.sum_active += L_act;
+  c->stats.step_flops += (double)L_act * (4.0 * (double)c->N * (double)c->Mg + 3.0 * (double)c->Mg) *
+                         ((double)c->M / (double)c->Mg);
+  c->stats.step_issued_flops += issued;
 }
 
 void check_launch() { OICA_CUDA(cudaGetLastError()); }
@@ -311,6 +322,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
   out->stopped = 0;
   std::vector<double> w_host(N);
   ComponentRecord rec_h{};
+  c->hist.ensure(2 * ((size_t)K + 1));
   for (int k = k_prefix; k < N_out; ++k) {
     const int i = k + 1;  // 1-based component index
     // a1: fresh candidates for this component (A8)
@@ -324,42 +336,63 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     int* act = c->act0.p;
     int* act_next = c->act1.p;
     build_operand(c, act, L_act);
+    // a2-a6: the do-while of PAPER.md:241-256.  Iterations are enqueued in batches without a
+    // host round trip once few rows remain (every kernel takes the true active count from the
+    // device counters; the host value is an upper bound that sizes the grids); the per-iteration
+    // counts are read back from `hist` afterwards.
+    const int L0 = L_act, nc0 = n_coarse;
     int t = 0;
-    int64_t sum_active = 0;
-    // a2-a6: the do-while of PAPER.md:241-256
-    while (L_act > 0) {
-      ++t;
-      sum_active += L_act;
-      c->stats.iterations += 1;
-      c->stats.sum_active += L_act;
-      run_step(c, L_act, n_coarse, true);
-      const bool tc = c->tc();
-      SlotPartials G = c->partials();
-      const double* s4 = tc ? nullptr : c->s4p.p;   // TC: alpha~ from the identity w_e . G (K3)
-      int S = c->S;
-      int64_t cap = c->Ll;
-      if (c->mshard()) {  // one fp64 allreduce of (G, s4) per iteration
-        c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, (int)c->NP, L_act, N, c->Gsum.p, (int)c->NP, c->s4sum.p));
-        auto& nc = Nccl::get();
-        OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_act * c->NP, ncclFloat64, ncclSum, c->comm, st));
-        if (!tc) OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_act, ncclFloat64, ncclSum, c->comm, st));
-        G = SlotPartials{c->Gsum.p, false};
-        s4 = tc ? nullptr : c->s4sum.p;
-        S = 1;
-        cap = c->Ll;
+    int L_ub = L_act, nc_ub = n_coarse;
+    while (L_ub > 0 && t < K) {
+      const int B = std::min(K - t, (L_ub <= kBatchRows && !c->mshard()) ? kBatch : 1);
+      for (int b = 0; b < B; ++b) {
+        ++t;
+        const int* cnt = c->Lact_dev.p;
+        run_step(c, L_ub, nc_ub, cnt, B > 1 && c->tc() && !c->split(), true);
+        const bool tc = c->tc();
+        SlotPartials G = c->partials();
+        const double* s4 = tc ? nullptr : c->s4p.p;   // TC: alpha~ from the identity w_e . G (K3)
+        int S = c->S;
+        int64_t cap = c->Ll;
+        if (c->mshard()) {  // one fp64 allreduce of (G, s4) per iteration; B == 1 here
+          c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, (int)c->NP, L_ub, N, c->Gsum.p, (int)c->NP, c->s4sum.p));
+          auto& nc = Nccl::get();
+          OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_ub * c->NP, ncclFloat64, ncclSum, c->comm, st));
+          if (!tc) OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st));
+          G = SlotPartials{c->Gsum.p, false};
+          s4 = tc ? nullptr : c->s4sum.p;
+          S = 1;
+          cap = c->Ll;
+        }
+        c->count(launch_epilogue(st, G, s4, S, cap, (int)c->NP, c->eval_point(), act, L_ub, c->Wacc.p, k, N,
+                                 (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p, c->keep.p,
+                                 c->promotion(), cnt));
+        c->count(launch_compact(st, act, c->keep.p, c->fine_flags(), L_ub, act_next, c->Lact_dev.p, c->Lact_host,
+                                cnt, c->hist.p + 2 * t));
+        std::swap(act, act_next);
+        if (t < K) build_operand(c, act, L_ub);
+        check_launch();
       }
-      c->count(launch_epilogue(st, G, s4, S, cap, (int)c->NP, c->eval_point(), act, L_act, c->Wacc.p, k, N,
-                               (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p, c->keep.p,
-                               c->promotion()));
-      c->count(launch_compact(st, act, c->keep.p, c->fine_flags(), L_act, act_next, c->Lact_dev.p, c->Lact_host));
-      std::swap(act, act_next);
-      if (t < K) build_operand(c, act, L_act);
-      check_launch();
       OICA_CUDA(cudaStreamSynchronize(st));
-      L_act = ((volatile int*)c->Lact_host)[0];
-      n_coarse = ((volatile int*)c->Lact_host)[1];
-      if (t >= K) break;  // ... while t < K and B non-empty (A19)
+      L_ub = ((volatile int*)c->Lact_host)[0];
+      nc_ub = ((volatile int*)c->Lact_host)[1];
     }
+    // per-iteration counts: entering iteration t' the active set had hist[t'-1] rows (t' >= 2)
+    std::vector<int> hist(2 * (size_t)(t + 1), 0);
+    if (t > 0) {
+      OICA_CUDA(cudaMemcpyAsync(hist.data(), c->hist.p, sizeof(int) * 2 * (size_t)(t + 1), cudaMemcpyDeviceToHost, st));
+      OICA_CUDA(cudaStreamSynchronize(st));
+    }
+    int64_t sum_active = 0;
+    int t_exec = 0;
+    for (int tt = 1; tt <= t; ++tt) {
+      int Lin = tt == 1 ? L0 : hist[2 * (tt - 1)], ncin = tt == 1 ? nc0 : hist[2 * (tt - 1) + 1];
+      if (Lin <= 0) break;
+      account_iteration(c, Lin, ncin);
+      sum_active += Lin;
+      t_exec = tt;
+    }
+    t = t_exec;
     // a7: selection and accept
     c->count(launch_select_local(st, c->W64.p, c->alpha_old.p, c->state.p, c->iters.p, (int)c->Ll, c->id_base, N,
                                  flags, c->X, c->ld, c->M, c->cluster.p, c->pc.p, c->qc.p, c->csize.p, c->ups_max.p,
@@ -630,7 +663,8 @@ oica_status oica_fixed_point_step(oica_ctx* c, const double* W_dev, int64_t L, d
     OICA_CUDA(cudaMemsetAsync(c->fine.p, c->split() ? 1 : 0, L, c->st));   // one precision for all rows
     c->count(launch_compact(c->st, nullptr, c->keep.p, nullptr, (int)L, c->act0.p, c->Lact_dev.p, nullptr));
     build_operand(c, c->act0.p, (int)L);
-    run_step(c, (int)L, c->split() ? 0 : (int)L, true);
+    run_step(c, (int)L, c->split() ? 0 : (int)L, nullptr, false, true);
+    account_iteration(c, (int)L, c->split() ? 0 : (int)L);
     bool tc = c->tc();
     c->count(launch_slot_reduce(c->st, c->partials(), tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L,
                                 (int)c->N, G_dev, (int)c->N, s4_dev));
