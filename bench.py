@@ -217,6 +217,7 @@ def run_oica(args, cfg):
 
     if args.all_components:   # time the whole extraction: components 1..N_out after a warm-up pass
         args.steps = cfg.N_out
+    xflags = oica.REDUCE_X if args.reduce else 0
     N_out = args.warmup + args.steps
     assert args.all_components or N_out <= cfg.N_out, "warmup + steps exceeds the config's N_out"
     Wacc = np.zeros((cfg.N_out, cfg.N))
@@ -225,11 +226,12 @@ def run_oica(args, cfg):
     def step(k):
         if args.all_components and k >= args.warmup:
             k -= args.warmup   # timed pass restarts at component 1
-        r = ctx.extract(k + 1, cfg.K, cfg.tol, W_prefix=Wacc[:k] if k else None)
+        r = ctx.extract(k + 1, cfg.K, cfg.tol, flags=xflags, W_prefix=Wacc[:k] if k else None)
         Wacc[k] = r.W[k]
         recs.append(dict(i=k + 1, index=int(r.index[k]), alpha=float(r.alpha[k]), upsilon=float(r.upsilon[k]),
                          sum_active=int(r.sum_active[k]), n_iter=int(r.n_iter[k]), cluster=int(r.cluster_size[k]),
-                         n_conv=int(r.n_converged[k]), n_unconv=int(r.n_unconverged[k]), near_tie=int(r.near_tie[k])))
+                         n_conv=int(r.n_converged[k]), n_unconv=int(r.n_unconverged[k]), near_tie=int(r.near_tie[k]),
+                         dim=int(r.dim[k])))
         return r
 
     for k in range(args.warmup):
@@ -252,7 +254,9 @@ def run_oica(args, cfg):
     st = ctx.stats()
     timed = recs[args.warmup:]
     M = cfg.M
-    flops = sum(r["sum_active"] for r in timed) * (4.0 * cfg.N * M + 3.0 * M)
+    # algorithmic work of the timed steps: the iteration of component i runs in dim_i = N (or
+    # N - i + 1 with --reduce)
+    flops = sum(r["sum_active"] * (4.0 * r["dim"] * M + 3.0 * M) for r in timed)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -274,7 +278,7 @@ def run_oica(args, cfg):
             if args.all_components:
                 k -= args.warmup
             ctx.set_data_host_ptr(Xh.data_ptr(), cfg.N, M_local, M_local, M_global=cfg.M)
-            r = ctx.extract(k + 1, cfg.K, cfg.tol, W_prefix=Wacc[:k] if k else None)
+            r = ctx.extract(k + 1, cfg.K, cfg.tol, flags=xflags, W_prefix=Wacc[:k] if k else None)
             d2h += 8 * cfg.N + 112 + 4 * int(r.n_iter[k])
         f1.record(stream)
         torch.cuda.synchronize(dev)
@@ -331,7 +335,8 @@ def run_oica(args, cfg):
                       "N_out": cfg.N_out, "components_timed": [r["i"] for r in timed],
                       "parallelism": f"{'m' if shard == oica.SHARD_M else 'l'}shard{world}",
                       "l2": f"inputs larger than L2 (X = {4 * cfg.N * cfg.M / 1e9:.2f} GB fp32), no flush",
-                      "precision": precision, "slots": st["slots"]},
+                      "precision": precision, "slots": st["slots"],
+                      "reduced_x": bool(args.reduce)},
            "seconds_per_component": sec_per_comp, "seconds_all_components": sec_all,
            "gpu_launches": st["kernel_launches"], "roofline": roof, "e2e": e2e, "cpu_baseline": cb,
            "clocks": clocks, "components": timed, "setup_s": setup_s}
@@ -351,6 +356,8 @@ def main():
     ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tc", "tc_split"])
     ap.add_argument("--shard", default="l", choices=["l", "m"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--reduce", action="store_true",
+                    help="iterate on the reduced data X~ = G X (PAPER.md §3.3, OICA_REDUCE_X)")
     ap.add_argument("--all-components", action="store_true",
                     help="time all N_out components (seconds to extract all N); --steps is ignored")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -99,12 +99,20 @@ typedef struct {
   uint8_t* near_tie;      /* best and second-best clusters within 1e-6 relative (A6)         */
   int32_t n_extracted;    /* rows written (< N_out only with OICA_STOP_ON_GAUSSIANITY)       */
   int32_t stopped;        /* 1 if the Gaussianity test ended extraction   */
+  int32_t* dim;           /* dimension the component's iteration ran in: N, or N-i+1 with   */
+                          /* OICA_REDUCE_X (algorithmic work = sum_active (4 dim M + 3 M))   */
 } oica_result;
 
 /* Flags for oica_extract_components. */
 #define OICA_INCLUDE_UNCONVERGED 0x1u  /* rows still active at K join the argmax (A4, Alg. 1)   */
 #define OICA_STOP_ON_GAUSSIANITY 0x2u  /* break on the Gaussianity test     */
 #define OICA_RAW_ARGMAX          0x4u  /* accept p = argmax itself, no cluster rule (A6)        */
+/* §3.3 reduction (Alg. 2 lines 4-12 and 28): component
+ * i iterates on X~ = G X (d = N-i+1 rows, G an orthonormal basis of the complement of the
+ * accepted rows) instead of projecting every update; candidates start at b0 = G r/||G r|| (A9),
+ * the accepted row is w = G^T b.  Same trajectories as the default projection form in exact
+ * arithmetic; 4 d M instead of 4 N M flop per row-iteration. */
+#define OICA_REDUCE_X            0x8u
 
 /* Counters of the last extract / step call (for benchmarks; all host values). */
 typedef struct {
@@ -216,6 +224,14 @@ typedef struct {
  * largest upsilon (ties -> lowest q); near_tie if the runner-up is within 1e-6 relative.
  * Host pointers; pure function.  Writes the winner index into `records` (*winner) and the
  * merged size / near-tie flag. */
+/* Host-only helpers of OICA_REDUCE_X (pure functions, no device).  oica_complement_basis: W is
+ * k x N with orthonormal rows (k < N); writes G, (N-k) x N, rows orthonormal and orthogonal to
+ * every row of W (the last N-k columns of Q in the Householder QR of W^T).  oica_deflate_basis:
+ * G is d x N with orthonormal rows, b a unit d-vector; writes the (d-1) x N basis of the
+ * complement of w = G^T b inside span(G) (rows 2..d of H G, H the reflection taking b to -+e1). */
+oica_status oica_complement_basis(const double* W, int32_t k, int32_t N, double* G);
+oica_status oica_deflate_basis(double* G, int32_t d, int32_t N, const double* b, double* G_out);
+
 oica_status oica_merge_records(const oica_cluster_record* records, const double* w, int32_t n,
                                int32_t N, int32_t* winner, int64_t* merged_size,
                                uint8_t* near_tie);

@@ -50,6 +50,28 @@ __device__ __forceinline__ float warp_sumf(float v) {
   return v;
 }
 
+// Candidate generator (reading A7): coordinate n of the N(0,1) vector of component
+// i (1-based), global candidate id l: counter c = ((i 2^24 + l) 2^9 + n/2) 2 + h, SplitMix64
+// finaliser (Steele, Lea, Flood 2014) of seed + (c+1) phi64, u = ((z >> 11) + 1/2) 2^-53,
+// Box-Muller in fp64 (even n: cos, odd n: sin).
+__device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double uniform01(uint64_t seed, uint64_t c) {
+  uint64_t z = splitmix64_mix(seed + (c + 1ull) * 0x9E3779B97F4A7C15ull);
+  return ((double)(z >> 11) + 0.5) * 0x1.0p-53;
+}
+__device__ __forceinline__ double candidate_normal(uint64_t seed, int i, uint64_t l, int n) {
+  uint64_t p = (uint64_t)(n >> 1);
+  uint64_t c0 = ((((uint64_t)i << 24) + l) * 512ull + p) * 2ull;
+  double u0 = uniform01(seed, c0), u1 = uniform01(seed, c0 + 1ull);
+  double rad = sqrt(-2.0 * log(u0));
+  double ang = 2.0 * 3.141592653589793 * u1;
+  return (n & 1) ? rad * sin(ang) : rad * cos(ang);
+}
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 

@@ -9,16 +9,6 @@ namespace {
 
 constexpr int kMaxV = 8;  // 256 / 32 coordinates per lane
 
-// SplitMix64 finaliser (Steele, Lea, Flood 2014) -- DESIGN.md §2 A7 generator.
-__device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
-}
-__device__ __forceinline__ double uniform01(uint64_t seed, uint64_t c) {
-  uint64_t z = splitmix64_mix(seed + (c + 1ull) * 0x9E3779B97F4A7C15ull);
-  return ((double)(z >> 11) + 0.5) * 0x1.0p-53;
-}
 
 // v <- v - E v with E = Wacc^T Wacc: all coefficients w_k . v are
 // taken from the incoming v (one projection, as written in the paper).
@@ -59,15 +49,7 @@ __global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_loc
   for (int u = 0; u < kMaxV; ++u) {
     int n = lane + 32 * u;
     v[u] = 0.0;
-    if (n < N) {
-      // counter c = ((i 2^24 + l) 2^9 + p) 2 + h, p = n / 2  (DESIGN.md §2 A7)
-      uint64_t p = (uint64_t)(n >> 1);
-      uint64_t c0 = ((((uint64_t)i << 24) + l) * 512ull + p) * 2ull;
-      double u0 = uniform01(seed, c0), u1 = uniform01(seed, c0 + 1ull);
-      double rad = sqrt(-2.0 * log(u0));
-      double ang = 2.0 * 3.141592653589793 * u1;
-      v[u] = (n & 1) ? rad * sin(ang) : rad * cos(ang);
-    }
+    if (n < N) v[u] = candidate_normal(seed, i, l, n);   // A7
   }
   project_warp(v, Wacc, k, N, lane);
   double ss = 0.0;

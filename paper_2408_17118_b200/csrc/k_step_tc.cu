@@ -187,7 +187,8 @@ struct Cfg {
   static constexpr int MT = WIDE ? 64 : 128;                     // samples per chunk (GEMM1 N)
   static constexpr int XB = NP * 128;                            // bytes of one [NP][64] swizzled box
   static constexpr int X_STAGE = NP * MT * 2;                    // bytes per X stage
-  static constexpr int WLO_BYTES = WLO_SMEM ? 128 * NP * 2 : 0;
+  static constexpr int WLO_BOXES = (NP + 63) / 64;               // 64-column K-major boxes of W_lo
+  static constexpr int WLO_BYTES = WLO_SMEM ? 128 * WLO_BOXES * 128 : 0;
   static constexpr int X_BUDGET = WLO_SMEM ? 131072 : 196608;
   static constexpr int STAGES = X_BUDGET / X_STAGE >= 8 ? 8 : X_BUDGET / X_STAGE;
   static constexpr int C_WHI = 0;
@@ -273,7 +274,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (lane == 0) {
       if (C::WLO_SMEM && lo_pass) {
         mbar_expect_tx(wlo_full, C::WLO_BYTES);
-        for (int kb = 0; kb < NP / 64; ++kb) tma_load_2d(s_wlo + kb * 16384, &tmWlo, wlo_full, kb * 64, row0);
+        for (int kb = 0; kb < C::WLO_BOXES; ++kb) tma_load_2d(s_wlo + kb * 16384, &tmWlo, wlo_full, kb * 64, row0);
       }
       // CL > 1: this CTA loads rows [crank*SR, (crank+1)*SR) of every chunk and multicasts them
       // to the whole cluster (all CTAs of a cluster share the slot, hence the chunks)
@@ -578,6 +579,13 @@ void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP
     case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 144: launch_variant<144, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 160: launch_variant<160, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 176: launch_variant<176, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 192: launch_variant<192, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 208: launch_variant<208, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 224: launch_variant<224, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 240: launch_variant<240, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
   }
@@ -595,7 +603,7 @@ __global__ void k_x_prepare_f16(const float* __restrict__ X, int64_t ld, int N, 
 }  // namespace
 
 bool tc_supported(int N) { return N >= 1 && N <= 256; }
-int tc_np(int N) { return N <= 128 ? (int)round_up(N < 16 ? 16 : N, 16) : 256; }
+int tc_np(int N) { return (int)round_up(N < 16 ? 16 : N, 16); }
 
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
                    const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,

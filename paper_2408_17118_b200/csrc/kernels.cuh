@@ -118,6 +118,16 @@ int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, in
 int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP,
                          int64_t ldx, __half* Xh);
 
+// ---- §3.3 reduction of X (k_reduce.cu)
+// X~ = G X (Gf: d x N fp32 rows) into Xr (d x M, stride ldr) and, if Xh != null, the fp16 plane
+// Xh [NPd][ldx] (rows >= d and columns >= M zero).
+int launch_reduce_apply(cudaStream_t st, const float* Gf, int d, int N, const float* X, int64_t ld, int64_t M,
+                        float* Xr, int64_t ldr, __half* Xh, int NPd, int64_t ldx);
+// Candidates of component i in the reduced basis: W64 row j = G r_j / ||G r_j|| (d entries).
+int launch_cand_basis(cudaStream_t st, uint64_t seed, int i, int64_t id_base, int64_t L_local, int N,
+                      const double* G, int d, double* W64, uint8_t* state, uint8_t* keep, uint8_t* fine,
+                      uint8_t fine_init, double* dprev);
+
 // ---- boundary: whitening (k_whiten.cu)
 int launch_row_mean(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, double* mean);
 int launch_covariance(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, const double* mean,

@@ -68,6 +68,19 @@ struct oica_ctx {
   int precision = OICA_PREC_FP32;
   DevBuf<__half> Xh;   // TC operand plane
   int64_t ldx = 0;
+  // the data the current component iterates on (DESIGN.md §5 "reduced X"): the full whitened X,
+  // or X~ = G X in the d = N-k dimensional complement of the accepted rows (OICA_REDUCE_X)
+  const float* vX = nullptr;
+  int64_t vld = 0;
+  const __half* vXh = nullptr;
+  int vN = 0, vNP = 0;
+  bool reduced = false;
+  DevBuf<float> Xr, Gf;
+  DevBuf<__half> Xrh;
+  DevBuf<double> Gdev, Wacc_scratch;
+  std::vector<double> Gh;   // host basis, d x N (rows orthonormal, orthogonal to W_acc)
+  std::vector<double> Gh_last;   // basis of the last extracted component if it ran reduced
+  int last_vN = 0;
   bool tc_ready = false;
   // slots
   int S = 1;
@@ -104,7 +117,7 @@ struct oica_ctx {
   bool split() const { return precision == OICA_PREC_TC_SPLIT; }
   SlotPartials partials() const { return tc() ? SlotPartials{Gp32.p, true} : SlotPartials{Gp.p, false}; }
   EvalPoint eval_point() const {
-    return tc() ? EvalPoint{Whi.p, Wlo.p, nullptr, (int)NP} : EvalPoint{nullptr, nullptr, W32.p, (int)NP};
+    return tc() ? EvalPoint{Whi.p, Wlo.p, nullptr, vNP} : EvalPoint{nullptr, nullptr, W32.p, vNP};
   }
   Promotion promotion() const {
     return tc() ? Promotion{fine.p, dprev.p, kPromoteD, kPromoteT} : Promotion{nullptr, nullptr, 0.0, 0};
@@ -254,10 +267,10 @@ void ensure_candidate_buffers(oica_ctx* c) {
 // Build the step-kernel operand rows for the active list `act` (count in Lact_dev, <= cap).
 void build_operand(oica_ctx* c, const int* act, int cap) {
   if (c->tc())
-    c->count(launch_operand_f16x2(c->st, act, c->Lact_dev.p, cap, c->W64.p, (int)c->N, (int)c->NP, c->fine.p,
+    c->count(launch_operand_f16x2(c->st, act, c->Lact_dev.p, cap, c->W64.p, c->vN, c->vNP, c->fine.p,
                                   c->Whi.p, c->Wlo.p));
   else
-    c->count(launch_operand_f32(c->st, act, c->Lact_dev.p, cap, c->W64.p, (int)c->N, (int)c->NP, c->W32.p));
+    c->count(launch_operand_f32(c->st, act, c->Lact_dev.p, cap, c->W64.p, c->vN, c->vNP, c->W32.p));
 }
 
 // One fused contraction over the active rows (positions 0..L_act-1; rows >= n_coarse are fine)
@@ -271,10 +284,10 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, bool lo_capa
   }
   int n;
   if (c->tc())
-    n = launch_step_tc(c->st, c->Xh.p, c->ldx, c->M, (int)c->NP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
+    n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
                        c->S, c->Gp32.p, c->Ll, cnt, lo_capable);
   else
-    n = launch_step_simt(c->st, c->X, c->ld, c->M, (int)c->N, (int)c->NP, c->W32.p, L_act, c->slot_len, c->S, kFlush,
+    n = launch_step_simt(c->st, c->vX, c->vld, c->M, c->vN, c->vNP, c->W32.p, L_act, c->slot_len, c->S, kFlush,
                          c->Gp.p, c->s4p.p, c->Ll, cnt);
   OICA_CUDA(cudaGetLastError());
   c->count(n);
@@ -290,19 +303,120 @@ void account_iteration(oica_ctx* c, int L_act, int n_coarse) {
   double issued;
   if (c->tc()) {
     int64_t tiles = ceil_div(L_act, 128), lo_tiles = n_coarse < L_act ? tiles - n_coarse / 128 : 0;
-    issued = 128.0 * (double)c->NP * (double)c->M * 2.0 * (2.0 * (double)tiles + 2.0 * (double)lo_tiles);
+    issued = 128.0 * (double)c->vNP * (double)c->M * 2.0 * (2.0 * (double)tiles + 2.0 * (double)lo_tiles);
     c->stats.fine_rows += L_act - n_coarse;
   } else {
-    issued = (double)round_up(L_act, 64) * (double)c->NP * (double)c->M * 4.0;
+    issued = (double)round_up(L_act, 64) * (double)c->vNP * (double)c->M * 4.0;
   }
   c->stats.iterations += 1;
   c->stats.sum_active += L_act;
-  c->stats.step_flops += (double)L_act * (4.0 * (double)c->N * (double)c->Mg + 3.0 * (double)c->Mg) *
+  c->stats.step_flops += (double)L_act * (4.0 * (double)c->vN * (double)c->Mg + 3.0 * (double)c->Mg) *
                          ((double)c->M / (double)c->Mg);
   c->stats.step_issued_flops += issued;
 }
 
 void check_launch() { OICA_CUDA(cudaGetLastError()); }
+
+// ---- §3.3 reduction of X (Alg. 2 lines 4-12) ---------------------------
+// The paper builds the complement basis as G = (F~F~^T)^{-1/2} F~ with F = I - W^T W.  Any
+// orthonormal basis of the complement gives the same trajectories (w = G^T b; the update of
+// eq. (5) is equivariant under b -> U b, X~ -> U X~ for orthogonal U; reading A9),
+// so the runtime uses Householder reflections: O(N^2 k) once for a caller prefix, then one
+// reflection per accepted row, O(d N), instead of a d x d inverse square root per component.
+
+// Rows of G (N-k x N): the last N-k columns of Q in the Householder QR of W^T (W: k x N, rows
+// orthonormal).
+void complement_basis(const double* W, int k, int N, std::vector<double>& G) {
+  std::vector<double> A((size_t)N * std::max(k, 1));   // A[n][j] = W[j][n]
+  for (int j = 0; j < k; ++j)
+    for (int n = 0; n < N; ++n) A[(size_t)n * k + j] = W[(size_t)j * N + n];
+  std::vector<double> Q((size_t)N * N, 0.0), v(N), u(N);
+  for (int n = 0; n < N; ++n) Q[(size_t)n * N + n] = 1.0;
+  for (int j = 0; j < k; ++j) {
+    double nx = 0.0;
+    for (int r = j; r < N; ++r) nx += A[(size_t)r * k + j] * A[(size_t)r * k + j];
+    nx = std::sqrt(nx);
+    double a0 = A[(size_t)j * k + j];
+    double alpha = a0 >= 0 ? -nx : nx;
+    for (int r = j; r < N; ++r) v[r] = A[(size_t)r * k + j];
+    v[j] -= alpha;
+    double vn2 = 0.0;
+    for (int r = j; r < N; ++r) vn2 += v[r] * v[r];
+    if (vn2 <= 0.0) continue;
+    for (int cidx = j; cidx < k; ++cidx) {   // A <- H A
+      double sdot = 0.0;
+      for (int r = j; r < N; ++r) sdot += v[r] * A[(size_t)r * k + cidx];
+      sdot *= 2.0 / vn2;
+      for (int r = j; r < N; ++r) A[(size_t)r * k + cidx] -= sdot * v[r];
+    }
+    for (int n = 0; n < N; ++n) {             // Q <- Q H
+      double sdot = 0.0;
+      for (int r = j; r < N; ++r) sdot += Q[(size_t)n * N + r] * v[r];
+      sdot *= 2.0 / vn2;
+      for (int r = j; r < N; ++r) Q[(size_t)n * N + r] -= sdot * v[r];
+    }
+  }
+  int d = N - k;
+  G.assign((size_t)d * N, 0.0);
+  for (int r = 0; r < d; ++r)
+    for (int n = 0; n < N; ++n) G[(size_t)r * N + n] = Q[(size_t)n * N + (k + r)];
+}
+
+// G (d x N) -> rows 2..d of H G, H the reflection taking the unit vector b (reduced coordinates of
+// the accepted row) to -+e_1: the first row of H G is +-w, the rest span the new complement.
+void deflate_basis(std::vector<double>& G, int d, int N, const double* b) {
+  std::vector<double> v(b, b + d), u(N, 0.0);
+  double nb = 0.0;
+  for (int r = 0; r < d; ++r) nb += b[r] * b[r];
+  nb = std::sqrt(nb);
+  v[0] -= b[0] >= 0 ? -nb : nb;
+  double vn2 = 0.0;
+  for (int r = 0; r < d; ++r) vn2 += v[r] * v[r];
+  if (vn2 > 0.0) {
+    for (int r = 0; r < d; ++r)
+      for (int n = 0; n < N; ++n) u[n] += v[r] * G[(size_t)r * N + n];
+    for (int r = 0; r < d; ++r) {
+      double f = 2.0 * v[r] / vn2;
+      for (int n = 0; n < N; ++n) G[(size_t)r * N + n] -= f * u[n];
+    }
+  }
+  G.erase(G.begin(), G.begin() + N);
+}
+
+int simt_np(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+
+void use_full_view(oica_ctx* c) {
+  c->vX = c->X;
+  c->vld = c->ld;
+  c->vXh = c->Xh.p;
+  c->vN = (int)c->N;
+  c->vNP = (int)c->NP;
+  c->reduced = false;
+}
+
+// X~ = G X for the current host basis c->Gh (d = rows): fp32 copy (selection, FP32 step) and the
+// fp16 tensor-core plane.
+void use_reduced_view(oica_ctx* c, int d) {
+  const int N = (int)c->N;
+  c->Gdev.ensure((size_t)d * N);
+  c->Gf.ensure((size_t)d * N);
+  std::vector<float> gf(c->Gh.begin(), c->Gh.begin() + (size_t)d * N);
+  OICA_CUDA(cudaMemcpyAsync(c->Gdev.p, c->Gh.data(), sizeof(double) * d * N, cudaMemcpyHostToDevice, c->st));
+  OICA_CUDA(cudaMemcpyAsync(c->Gf.p, gf.data(), sizeof(float) * d * N, cudaMemcpyHostToDevice, c->st));
+  c->Xr.ensure((size_t)N * c->M);
+  int npd = c->tc() ? tc_np(d) : simt_np(d);
+  if (c->tc()) c->Xrh.ensure((size_t)c->NP * c->ldx);
+  c->count(launch_reduce_apply(c->st, c->Gf.p, d, N, c->X, c->ld, c->M, c->Xr.p, c->M, c->tc() ? c->Xrh.p : nullptr,
+                               npd, c->ldx));
+  check_launch();
+  OICA_CUDA(cudaStreamSynchronize(c->st));   // gf is a host temporary
+  c->vX = c->Xr.p;
+  c->vld = c->M;
+  c->vXh = c->tc() ? c->Xrh.p : nullptr;
+  c->vN = d;
+  c->vNP = npd;
+  c->reduced = true;
+}
 
 void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t flags, const double* W_prefix,
                   int32_t k_prefix, oica_result* out) {
@@ -320,14 +434,36 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     OICA_CUDA(cudaMemcpyAsync(c->Wacc.p, W_prefix, sizeof(double) * k_prefix * N, cudaMemcpyHostToDevice, st));
   out->n_extracted = k_prefix;
   out->stopped = 0;
-  std::vector<double> w_host(N);
+  std::vector<double> w_host(N), b_host(N);
   ComponentRecord rec_h{};
   c->hist.ensure(2 * ((size_t)K + 1));
+  const bool reduce = flags & OICA_REDUCE_X;
+  if (reduce) {   // complement basis of the prefix (identity when there is none)
+    if (k_prefix > 0) {
+      complement_basis(W_prefix, k_prefix, N, c->Gh);
+    } else {
+      c->Gh.assign((size_t)N * N, 0.0);
+      for (int n = 0; n < N; ++n) c->Gh[(size_t)n * N + n] = 1.0;
+    }
+    c->Wacc_scratch.ensure((size_t)N);
+  }
+  use_full_view(c);
   for (int k = k_prefix; k < N_out; ++k) {
     const int i = k + 1;  // 1-based component index
+    // Alg. 2 lines 4-12: iterate on X~ = G X in the d = N - k dimensional complement
+    if (reduce && k > 0)
+      use_reduced_view(c, N - k);
+    else
+      use_full_view(c);
+    const int vN = c->vN;
+    const int kk = c->reduced ? 0 : k;   // rows projected out per update (none in the reduced space)
     // a1: fresh candidates for this component (A8)
-    c->count(launch_cand_init(st, c->seed, i, c->id_base, c->Ll, N, c->Wacc.p, k, c->W64.p, c->state.p, c->keep.p,
-                              c->fine.p, c->split() ? 1 : 0, c->dprev.p));
+    if (c->reduced)
+      c->count(launch_cand_basis(st, c->seed, i, c->id_base, c->Ll, N, c->Gdev.p, vN, c->W64.p, c->state.p,
+                                 c->keep.p, c->fine.p, c->split() ? 1 : 0, c->dprev.p));
+    else
+      c->count(launch_cand_init(st, c->seed, i, c->id_base, c->Ll, N, c->Wacc.p, k, c->W64.p, c->state.p, c->keep.p,
+                                c->fine.p, c->split() ? 1 : 0, c->dprev.p));
     c->count(launch_compact(st, nullptr, c->keep.p, c->fine_flags(), (int)c->Ll, c->act0.p, c->Lact_dev.p,
                             c->Lact_host));
     OICA_CUDA(cudaStreamSynchronize(st));
@@ -355,16 +491,16 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         int S = c->S;
         int64_t cap = c->Ll;
         if (c->mshard()) {  // one fp64 allreduce of (G, s4) per iteration; B == 1 here
-          c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, (int)c->NP, L_ub, N, c->Gsum.p, (int)c->NP, c->s4sum.p));
+          c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, c->vNP, L_ub, vN, c->Gsum.p, c->vNP, c->s4sum.p));
           auto& nc = Nccl::get();
-          OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_ub * c->NP, ncclFloat64, ncclSum, c->comm, st));
+          OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_ub * c->vNP, ncclFloat64, ncclSum, c->comm, st));
           if (!tc) OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st));
           G = SlotPartials{c->Gsum.p, false};
           s4 = tc ? nullptr : c->s4sum.p;
           S = 1;
           cap = c->Ll;
         }
-        c->count(launch_epilogue(st, G, s4, S, cap, (int)c->NP, c->eval_point(), act, L_ub, c->Wacc.p, k, N,
+        c->count(launch_epilogue(st, G, s4, S, cap, c->vNP, c->eval_point(), act, L_ub, c->Wacc.p, kk, vN,
                                  (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p, c->keep.p,
                                  c->promotion(), cnt));
         c->count(launch_compact(st, act, c->keep.p, c->fine_flags(), L_ub, act_next, c->Lact_dev.p, c->Lact_host,
@@ -394,34 +530,61 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     }
     t = t_exec;
     // a7: selection and accept
-    c->count(launch_select_local(st, c->W64.p, c->alpha_old.p, c->state.p, c->iters.p, (int)c->Ll, c->id_base, N,
-                                 flags, c->X, c->ld, c->M, c->cluster.p, c->pc.p, c->qc.p, c->csize.p, c->ups_max.p,
+    c->count(launch_select_local(st, c->W64.p, c->alpha_old.p, c->state.p, c->iters.p, (int)c->Ll, c->id_base, vN,
+                                 flags, c->vX, c->vld, c->M, c->cluster.p, c->pc.p, c->qc.p, c->csize.p, c->ups_max.p,
                                  c->counts.p, c->part.p, c->nblk_alpha, c->s4c.p));
     if (c->mshard())
       OICA_NCCL(Nccl::get().AllReduce(c->s4c.p, c->s4c.p, kMaxClusters, ncclFloat64, ncclSum, c->comm, st));
     c->count(launch_select_finish(st, c->W64.p, c->iters.p, c->counts.p, c->pc.p, c->qc.p, c->csize.p, c->s4c.p,
-                                  c->id_base, N, (double)c->Mg, flags, sum_active, t, c->summary.p, c->wsum.p));
+                                  c->id_base, vN, (double)c->Mg, flags, sum_active, t, c->summary.p, c->wsum.p));
     const RankSummary* all = c->summary.p;
     const double* wall = c->wsum.p;
     int world = 1;
     if (c->world() > 1 && !c->mshard()) {  // L-shard: one exchange per component (C1)
       auto& nc = Nccl::get();
       OICA_NCCL(nc.AllGather(c->summary.p, c->summary_all.p, sizeof(RankSummary), ncclUint8, c->comm, st));
-      OICA_NCCL(nc.AllGather(c->wsum.p, c->wsum_all.p, (size_t)kMaxClusters * N, ncclFloat64, c->comm, st));
+      OICA_NCCL(nc.AllGather(c->wsum.p, c->wsum_all.p, (size_t)kMaxClusters * vN, ncclFloat64, c->comm, st));
       all = c->summary_all.p;
       wall = c->wsum_all.p;
       world = c->world();
     }
-    c->count(launch_merge_accept(st, all, wall, world, N, i, (double)c->Mg, flags, c->Wacc.p, k, c->rec.p, c->w_out.p));
+    // reduced: the merge works on b (vN-dim) with the Gaussianity threshold of the d-dimensional
+    // problem, 2(d+1)d/M = 2(N-i+2)(N-i+1)/M (i_eff = 1); the accepted row is w = G^T b (line 28)
+    c->count(launch_merge_accept(st, all, wall, world, vN, c->reduced ? 1 : i, (double)c->Mg, flags,
+                                 c->reduced ? c->Wacc_scratch.p : c->Wacc.p, c->reduced ? 0 : k, c->rec.p,
+                                 c->w_out.p));
     check_launch();
     OICA_CUDA(cudaMemcpyAsync(&rec_h, c->rec.p, sizeof(ComponentRecord), cudaMemcpyDeviceToHost, st));
-    OICA_CUDA(cudaMemcpyAsync(w_host.data(), c->w_out.p, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    OICA_CUDA(cudaMemcpyAsync(b_host.data(), c->w_out.p, sizeof(double) * vN, cudaMemcpyDeviceToHost, st));
     c->harvest_events();
     c->last_valid = true;
     if (rec_h.status != OICA_OK)
       throw Error((oica_status)rec_h.status,
                   rec_h.status == OICA_ERR_ALL_CANDIDATES_DEGENERATE ? "all candidates degenerate (A18)"
                                                                      : "no eligible candidate with alpha > -2 (A13)");
+    if (c->reduced) {   // w = G^T b, canonical sign (A17), appended to W_acc
+      for (int n = 0; n < N; ++n) {
+        double acc = 0.0;
+        for (int r = 0; r < vN; ++r) acc += c->Gh[(size_t)r * N + n] * b_host[r];
+        w_host[n] = acc;
+      }
+      double nw = 0.0;
+      for (int n = 0; n < N; ++n) nw += w_host[n] * w_host[n];
+      nw = std::sqrt(nw);
+      int jm = 0;
+      for (int n = 1; n < N; ++n)
+        if (std::fabs(w_host[n]) > std::fabs(w_host[jm])) jm = n;
+      double sg = w_host[jm] < 0 ? -1.0 : 1.0;
+      for (int n = 0; n < N; ++n) w_host[n] *= sg / nw;
+      OICA_CUDA(cudaMemcpyAsync(c->Wacc.p + (size_t)k * N, w_host.data(), sizeof(double) * N, cudaMemcpyHostToDevice,
+                                st));
+      OICA_CUDA(cudaStreamSynchronize(st));
+    } else {
+      std::copy(b_host.begin(), b_host.begin() + N, w_host.begin());
+    }
+    c->last_vN = vN;
+    if (c->reduced) c->Gh_last.assign(c->Gh.begin(), c->Gh.begin() + (size_t)vN * N);
+    if (reduce) deflate_basis(c->Gh, N - k, N, c->reduced ? b_host.data() : w_host.data());
     bool stop = (flags & OICA_STOP_ON_GAUSSIANITY) && rec_h.gaussian;
     if (out->W && !stop) std::memcpy(out->W + (size_t)k * N, w_host.data(), sizeof(double) * N);
     if (out->alpha) out->alpha[k] = rec_h.w_alpha;
@@ -436,12 +599,14 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     if (out->sum_active) out->sum_active[k] = rec_h.sum_active;
     if (out->gaussian_flag) out->gaussian_flag[k] = (uint8_t)rec_h.gaussian;
     if (out->near_tie) out->near_tie[k] = (uint8_t)rec_h.near_tie;
+    if (out->dim) out->dim[k] = vN;
     if (stop) {
       out->stopped = 1;
       break;
     }
     out->n_extracted = k + 1;
   }
+  use_full_view(c);
 }
 
 void set_data_impl(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int64_t ld, int64_t M_global) {
@@ -474,6 +639,7 @@ void set_data_impl(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int
     c->count(launch_x_prepare_f16(c->st, Xw, ld, (int)N, M_local, (int)c->NP, c->ldx, c->Xh.p));
     check_launch();
   }
+  use_full_view(c);
   if (c->have_cand) ensure_candidate_buffers(c);
 }
 
@@ -699,11 +865,26 @@ oica_status oica_get_candidates(oica_ctx* c, double* W, double* alpha, int32_t* 
     if (id_base) *id_base = c->id_base;
     if (!(W || alpha || iters || state)) return;
     OICA_REQUIRE(c->last_valid, OICA_ERR_STATE, "no extracted component yet");
-    if (W) OICA_CUDA(cudaMemcpyAsync(W, c->W64.p, sizeof(double) * c->Ll * c->N, cudaMemcpyDeviceToHost, c->st));
+    std::vector<double> Wb;
+    const bool red = c->last_vN != (int)c->N;   // rows are b in the reduced basis: return w = G^T b
+    if (W && !red) OICA_CUDA(cudaMemcpyAsync(W, c->W64.p, sizeof(double) * c->Ll * c->N, cudaMemcpyDeviceToHost, c->st));
+    if (W && red) {
+      Wb.resize((size_t)c->Ll * c->last_vN);
+      OICA_CUDA(cudaMemcpyAsync(Wb.data(), c->W64.p, sizeof(double) * Wb.size(), cudaMemcpyDeviceToHost, c->st));
+    }
     if (alpha) OICA_CUDA(cudaMemcpyAsync(alpha, c->alpha_old.p, sizeof(double) * c->Ll, cudaMemcpyDeviceToHost, c->st));
     if (iters) OICA_CUDA(cudaMemcpyAsync(iters, c->iters.p, sizeof(int32_t) * c->Ll, cudaMemcpyDeviceToHost, c->st));
     if (state) OICA_CUDA(cudaMemcpyAsync(state, c->state.p, c->Ll, cudaMemcpyDeviceToHost, c->st));
     OICA_CUDA(cudaStreamSynchronize(c->st));
+    if (W && red) {
+      const int N = (int)c->N, d = c->last_vN;
+      for (int64_t l = 0; l < c->Ll; ++l)
+        for (int n = 0; n < N; ++n) {
+          double acc = 0.0;
+          for (int r = 0; r < d; ++r) acc += Wb[(size_t)l * d + r] * c->Gh_last[(size_t)r * N + n];
+          W[(size_t)l * N + n] = acc;
+        }
+    }
   });
 }
 
@@ -725,6 +906,22 @@ oica_status oica_reset_stats(oica_ctx* c) {
 oica_status oica_synchronize(oica_ctx* c) {
   if (!c) return OICA_ERR_INVALID_ARGUMENT;
   return guard(c, [&] { OICA_CUDA(cudaStreamSynchronize(c->st)); });
+}
+
+oica_status oica_complement_basis(const double* W, int32_t k, int32_t N, double* G) {
+  if (!G || N < 1 || N > 4096 || k < 0 || k >= N || (k > 0 && !W)) return OICA_ERR_INVALID_ARGUMENT;
+  std::vector<double> g;
+  complement_basis(W, k, N, g);
+  std::memcpy(G, g.data(), sizeof(double) * g.size());
+  return OICA_OK;
+}
+
+oica_status oica_deflate_basis(double* G, int32_t d, int32_t N, const double* b, double* G_out) {
+  if (!G || !b || !G_out || d < 2 || N < d) return OICA_ERR_INVALID_ARGUMENT;
+  std::vector<double> g(G, G + (size_t)d * N);
+  deflate_basis(g, d, N, b);
+  std::memcpy(G_out, g.data(), sizeof(double) * g.size());
+  return OICA_OK;
 }
 
 oica_status oica_merge_records(const oica_cluster_record* records, const double* w, int32_t n, int32_t N,

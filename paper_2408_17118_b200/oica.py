@@ -26,7 +26,7 @@ STATUS = ["OK", "INVALID_ARGUMENT", "DIMENSION_MISMATCH", "RANK_DEFICIENT", "ALL
 
 PREC_AUTO, PREC_FP32, PREC_TC, PREC_TC_SPLIT = 0, 1, 2, 3
 SHARD_L, SHARD_M = 0, 1
-INCLUDE_UNCONVERGED, STOP_ON_GAUSSIANITY, RAW_ARGMAX = 0x1, 0x2, 0x4
+INCLUDE_UNCONVERGED, STOP_ON_GAUSSIANITY, RAW_ARGMAX, REDUCE_X = 0x1, 0x2, 0x4, 0x8
 MAX_CLUSTERS = 8
 
 
@@ -51,7 +51,8 @@ class Result(C.Structure):
                 ("index", _P(C.c_int64)), ("iters", _P(C.c_int32)), ("n_iter", _P(C.c_int32)),
                 ("cluster_size", _P(C.c_int32)), ("n_converged", _P(C.c_int32)), ("n_unconverged", _P(C.c_int32)),
                 ("n_degenerate", _P(C.c_int32)), ("sum_active", _P(C.c_int64)), ("gaussian_flag", _P(C.c_uint8)),
-                ("near_tie", _P(C.c_uint8)), ("n_extracted", C.c_int32), ("stopped", C.c_int32)]
+                ("near_tie", _P(C.c_uint8)), ("n_extracted", C.c_int32), ("stopped", C.c_int32),
+                ("dim", _P(C.c_int32))]
 
 
 class Stats(C.Structure):
@@ -89,6 +90,8 @@ SIGNATURES = {
     "oica_synchronize": (C.c_int, [C.c_void_p]),
     "oica_merge_records": (C.c_int, [_P(ClusterRecord), _P(C.c_double), C.c_int32, C.c_int32, _P(C.c_int32),
                                      _P(C.c_int64), _P(C.c_uint8)]),
+    "oica_complement_basis": (C.c_int, [_P(C.c_double), C.c_int32, C.c_int32, _P(C.c_double)]),
+    "oica_deflate_basis": (C.c_int, [_P(C.c_double), C.c_int32, C.c_int32, _P(C.c_double), _P(C.c_double)]),
 }
 
 _lib = None
@@ -161,6 +164,25 @@ def merge_records(records, W):
     return dict(status=st, winner=win.value, size=size.value, near_tie=bool(tie.value))
 
 
+def complement_basis(W, N):
+    """Host-only (oica_complement_basis): orthonormal basis (N-k x N) of the complement of W's rows."""
+    W = np.ascontiguousarray(np.asarray(W, dtype=np.float64).reshape(-1, N))
+    k = W.shape[0]
+    G = np.zeros((N - k, N))
+    _check(lib().oica_complement_basis(_np_ptr(W, C.c_double) if k else None, k, N, _np_ptr(G, C.c_double)))
+    return G
+
+
+def deflate_basis(G, b):
+    """Host-only (oica_deflate_basis): basis of the complement of w = G^T b inside span(G)."""
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    d, N = G.shape
+    out = np.zeros((d - 1, N))
+    _check(lib().oica_deflate_basis(_np_ptr(G, C.c_double), d, N, _np_ptr(b, C.c_double), _np_ptr(out, C.c_double)))
+    return out
+
+
 @dataclass
 class Extraction:
     W: np.ndarray
@@ -178,6 +200,7 @@ class Extraction:
     near_tie: np.ndarray
     n_extracted: int
     stopped: bool
+    dim: np.ndarray = None
 
     @property
     def objective(self):
@@ -266,12 +289,14 @@ class Context:
                  n_iter=np.zeros(N_out, np.int32), cluster_size=np.zeros(N_out, np.int32),
                  n_converged=np.zeros(N_out, np.int32), n_unconverged=np.zeros(N_out, np.int32),
                  n_degenerate=np.zeros(N_out, np.int32), sum_active=np.zeros(N_out, np.int64),
-                 gaussian_flag=np.zeros(N_out, np.uint8), near_tie=np.zeros(N_out, np.uint8))
+                 gaussian_flag=np.zeros(N_out, np.uint8), near_tie=np.zeros(N_out, np.uint8),
+                 dim=np.zeros(N_out, np.int32))
         if Wp is not None:
             a["W"][:k] = Wp
         ct = dict(W=C.c_double, alpha=C.c_double, upsilon=C.c_double, index=C.c_int64, iters=C.c_int32,
                   n_iter=C.c_int32, cluster_size=C.c_int32, n_converged=C.c_int32, n_unconverged=C.c_int32,
-                  n_degenerate=C.c_int32, sum_active=C.c_int64, gaussian_flag=C.c_uint8, near_tie=C.c_uint8)
+                  n_degenerate=C.c_int32, sum_active=C.c_int64, gaussian_flag=C.c_uint8, near_tie=C.c_uint8,
+                  dim=C.c_int32)
         res = Result(**{f: _np_ptr(a[f], ct[f]) for f in ct}, n_extracted=0, stopped=0)
         self._c(lib().oica_extract_components(self.h, N_out, max_iter, tol, flags,
                                               _np_ptr(Wp, C.c_double), k, C.byref(res)))

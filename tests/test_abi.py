@@ -74,3 +74,35 @@ def test_merge_records_cluster_rule():
     r = oica.merge_records(recs, W)
     assert r["near_tie"] and r["winner"] == 1
     assert oica.merge_records([dict(upsilon=1, alpha=1, q=0, size=1, valid=0)], W[:1])["status"] != 0
+
+
+@pytest.mark.parametrize("N,k", [(5, 0), (5, 2), (12, 7), (64, 1), (256, 31), (256, 255)])
+def test_complement_basis_host(N, k):
+    """OICA_REDUCE_X basis: rows orthonormal, orthogonal to W, and G^T G = I - W^T W
+    (the projection of Alg. 1, so b0 = G r/||G r|| starts the same trajectory as P r/||P r||, A9)."""
+    rs = np.random.default_rng(N * 100 + k)
+    W = np.linalg.qr(rs.standard_normal((N, max(k, 1))))[0][:, :k].T if k else np.zeros((0, N))
+    G = oica.complement_basis(W, N)
+    assert G.shape == (N - k, N)
+    assert np.abs(G @ G.T - np.eye(N - k)).max() < 1e-12
+    if k:
+        assert np.abs(G @ W.T).max() < 1e-12
+    assert np.abs(G.T @ G - (np.eye(N) - W.T @ W)).max() < 1e-12
+
+
+@pytest.mark.parametrize("N,d", [(6, 6), (6, 3), (40, 33), (256, 225)])
+def test_deflate_basis_host(N, d):
+    """One accepted row: the new basis spans exactly span(G) minus w = G^T b (Alg. 2 line 28)."""
+    rs = np.random.default_rng(N + d)
+    G = np.linalg.qr(rs.standard_normal((N, d)))[0].T               # d x N, orthonormal rows
+    b = rs.standard_normal(d)
+    b /= np.linalg.norm(b)
+    w = G.T @ b
+    G2 = oica.deflate_basis(G, b)
+    assert G2.shape == (d - 1, N)
+    assert np.abs(G2 @ G2.T - np.eye(d - 1)).max() < 1e-12
+    assert np.abs(G2 @ w).max() < 1e-12
+    # inside span(G): projecting onto span(G) changes nothing
+    assert np.abs(G2 - (G2 @ G.T) @ G).max() < 1e-12
+    # G2^T G2 = G^T G - w w^T
+    assert np.abs(G2.T @ G2 - (G.T @ G - np.outer(w, w))).max() < 1e-12

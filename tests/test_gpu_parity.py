@@ -239,3 +239,54 @@ def test_argument_errors():
     with oica.Context(0) as c2, pytest.raises(oica.OicaError) as e:
         c2.init_candidates(1, 10)
     assert e.value.name == "STATE"
+
+
+# ---- §3.3 reduction of X (OICA_REDUCE_X): same gates against the O1 oracle,
+# whose trajectories equal the reduced form's (O1 == O3 pinned in tests/test_oracle_ordering.py)
+@pytest.mark.parametrize("name,precision", [("p_ragged", oica.PREC_FP32), ("p_n40", oica.PREC_FP32),
+                                            ("p_n40", oica.PREC_TC), ("p_tc_n32", oica.PREC_AUTO),
+                                            ("p_tc_n128", oica.PREC_AUTO), ("p_tc_n256", oica.PREC_AUTO)])
+def test_extract_parity_reduced(name, precision):
+    cfg, ctx = ctx_for(name, precision)
+    _, _, X64 = prepared(name)
+    W_or, res_or, _ = oracle_run(name)
+    res = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=oica.REDUCE_X)
+    assert res.n_extracted == cfg.N_out
+    assert list(res.dim[: cfg.N_out]) == [cfg.N - k for k in range(cfg.N_out)]
+    rep = _compare(res, res_or, W_or, X64)
+    assert np.abs(res.W @ res.W.T - np.eye(cfg.N_out)).max() < 1e-10
+    for k, r in enumerate(res_or):
+        assert bool(res.gaussian_flag[k]) == r.gaussian_flag
+    print(name, "reduced", rep)
+
+
+def _random_prefix(N, k, seed):
+    Q = np.linalg.qr(np.random.default_rng(seed).standard_normal((N, k)))[0]
+    return np.ascontiguousarray(Q[:, :k].T)
+
+
+@pytest.mark.parametrize("N,k,precision", [(256, 20, oica.PREC_TC), (200, 50, oica.PREC_TC), (256, 20, oica.PREC_FP32)])
+def test_reduced_wide_tile_widths(N, k, precision):
+    """Reduced dimension d = N - k lands on the wide tensor-core tiles NP = 240 / 160 (and the FP32
+    path): a seeded random orthonormal prefix (an input to both sides) is continued for two
+    components by the oracle (projection form) and by the library (reduced form)."""
+    cfg = Config(f"wide{N}", N, 40000, 96, 200, 1e-10, k + 2, (("laplace", N // 2), ("gg_uniform", N - N // 2, 0.5, 1.5)),
+                 data_seed=7000 + N, cand_seed=8000 + N)
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X32 = np.ascontiguousarray(Xw.astype(np.float32))
+    X64 = X32.astype(np.float64)
+    Wp = _random_prefix(N, k, 99)
+    W_or, res_or = ordering.extract(X64, cfg.L, cfg.K, cfg.tol, k + 2, cfg.cand_seed, W_prefix=Wp)
+    with oica.Context(0, precision) as ctx:
+        ctx.set_data(torch.from_numpy(X32).cuda())
+        ctx.init_candidates(cfg.cand_seed, cfg.L)
+        res = ctx.extract(k + 2, cfg.K, cfg.tol, flags=oica.REDUCE_X, W_prefix=Wp)
+        full = ctx.extract(k + 2, cfg.K, cfg.tol, W_prefix=Wp)
+    assert list(res.dim[k:k + 2]) == [N - k, N - k - 1]
+    for j, r in enumerate(res_or):
+        for out in (res, full):
+            assert out.index[k + j] == r.index or r.near_tie, (j, out.index[k + j], r.index)
+            assert abs(out.W[k + j] @ W_or[k + j]) >= 0.9999
+            assert abs((out.alpha[k + j] + 3) - (r.alpha + 3)) <= 1e-4 * (r.alpha + 3)
+    assert np.abs(res.W[k:] @ Wp.T).max() < 1e-10
