@@ -157,3 +157,24 @@ PARITY = {
                         (("gg_uniform", 256, 0.5, 1.9),),
                         data_seed=3006, cand_seed=4006),
 }
+
+
+# The paper's artificial experiments (§4.2), SURVEY rows f3/f4.  Sources are
+# generalised Gaussians with rho = 2 * 2^(j/4), j = -10..-1 (positive kurtosis) and 1..10
+# (negative kurtosis), unit variance; M = 10^4; hyperparameters of
+# epsilon = 1e-6 (reading A1: tol = epsilon^2 / 2 = 5e-13), K = 30.  The mixing
+# matrix is not stated: A ~ iid N(0,1) as in BASELINE.json's configs.  L is swept 1..100 by the
+# harness; the value here is the default.
+PAPER_RHO = tuple(2.0 * 2.0 ** (j / 4.0) for j in list(range(-10, 0)) + list(range(1, 11)))
+EXPERIMENTS = {
+    # Exp. 1: N = 20 non-Gaussian sources, ordering error vs L
+    "exp1_ordering": Config("exp1_ordering", 20, 10_000, 20, 30, 5e-13, 20,
+                            tuple(("gg", 1, r) for r in PAPER_RHO), data_seed=5001, cand_seed=6001),
+    # Exp. 2: 20 non-Gaussian + 10 Gaussian sources, N = 30, the number of
+    # non-Gaussian sources estimated by the Gaussianity test (reading A26)
+    "exp2_gaussianity": Config("exp2_gaussianity", 30, 10_000, 20, 30, 5e-13, 30,
+                               tuple(("gg", 1, r) for r in PAPER_RHO) + (("gaussian", 10),),
+                               data_seed=5002, cand_seed=6002),
+}
+BY_NAME.update(EXPERIMENTS)
+

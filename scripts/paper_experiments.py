@@ -1,0 +1,150 @@
+#!/usr/bin/env python
+"""The paper's experiments re-run on the B200 path (§4).
+
+    python scripts/paper_experiments.py [--runs T] [--out profiles/r01/paper_experiments.json]
+
+  exp1  ordering error vs L: N = 20 generalised-Gaussian sources (rho grid),
+        M = 1e4, K = 30, epsilon = 1e-6; E = ||W V A - I||_0 / N^2 with the true sources sorted
+        by their non-Gaussianity Upsilon (entries |.| > tau = 0.1 count).
+  exp2  number of non-Gaussian sources estimated by the Gaussianity test (PAPER.md:316-319,
+        :116-120): 20 generalised Gaussian + 10 Gaussian sources, extraction with
+        OICA_STOP_ON_GAUSSIANITY; the count is n_extracted.
+  eeg   fluctuation over T runs on the EEG-shaped config (cfg 2 stands in for
+        the absent 5SUBJECT data), L = 10..120 step 10.
+
+"All the values were averaged over 10 runs of random initializations": run t uses
+candidate seed cand_seed + t on the same data.  The T runs of one L execute concurrently, one
+context and CUDA stream each (many tiny problems per GPU: each extraction alone is launch-bound).
+This is a harness: it uses only the product API (whitening included) and datagen, not the oracle.
+"""
+from __future__ import annotations
+
+import argparse
+import itertools
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import datagen  # noqa: E402
+from paper_2408_17118_b200 import oica  # noqa: E402
+
+
+def upsilon(a):
+    a = np.asarray(a, dtype=np.float64)
+    return a - 2.0 * np.log(a / 2.0 + 1.0)
+
+
+def ordering_error(W, V, A, S, tau=0.1):
+    """||P - I||_0 / N^2, P = W V A with the columns in decreasing Upsilon of the true sources."""
+    Sc = S - S.mean(axis=1, keepdims=True)
+    Sc /= Sc.std(axis=1, keepdims=True)
+    order = np.argsort(-upsilon(np.mean(Sc ** 4, axis=1) - 3.0), kind="stable")
+    P = W @ V @ A[:, order]
+    P /= np.linalg.norm(P, axis=1, keepdims=True)
+    for r in range(P.shape[0]):
+        j = int(np.argmax(np.abs(P[r])))
+        if P[r, j] < 0:
+            P[r] = -P[r]
+    k, N = P.shape
+    return float(np.count_nonzero(np.abs(P - np.eye(k, N)) > tau)) / (k * N)
+
+
+def fluctuation(runs):
+    """Mean over ordered run pairs of 1 - |cos(w_i^t, w_i^u)| per component."""
+    T = len(runs)
+    n = min(r.shape[0] for r in runs)
+    out = np.zeros(n)
+    for t, u in itertools.permutations(range(T), 2):
+        a, b = runs[t][:n], runs[u][:n]
+        out += 1.0 - np.abs(np.sum(a * b, axis=1)) / (np.linalg.norm(a, axis=1) * np.linalg.norm(b, axis=1))
+    return out / (T * (T - 1))
+
+
+def prepare(cfg):
+    ds = datagen.make_dataset(cfg, device="cuda", dtype=torch.float64, keep_sources=True)
+    X = ds.X.float().contiguous()
+    Xw = torch.empty_like(X)
+    with oica.Context(0) as ctx:
+        _, V, _ = ctx.whiten(X, Xw)
+    return Xw, V, ds.A.cpu().numpy(), ds.S.cpu().numpy()
+
+
+def run_batch(Xw, cfg, L, seeds, flags):
+    """One extraction per seed, concurrently (thread + context + stream each); device seconds."""
+    out = [None] * len(seeds)
+
+    def work(j, seed):
+        stream = torch.cuda.Stream()
+        with oica.Context(0, oica.PREC_AUTO, stream=stream) as ctx:
+            ctx.set_data(Xw)
+            ctx.init_candidates(seed, L)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=flags)
+            e1.record(stream)
+            e1.synchronize()
+            out[j] = (r, e0.elapsed_time(e1) / 1e3)
+
+    th = [threading.Thread(target=work, args=(j, s)) for j, s in enumerate(seeds)]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    return out, time.perf_counter() - t0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--runs", type=int, default=10)
+    ap.add_argument("--L", default="1,2,5,10,20,50,100")
+    ap.add_argument("--eeg-L", default="10,20,30,40,50,60,70,80,90,100,110,120")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "paper_experiments.json"))
+    ap.add_argument("--skip-eeg", action="store_true")
+    a = ap.parse_args()
+    Ls = [int(x) for x in a.L.split(",")]
+    res = {"runs": a.runs, "gpu": torch.cuda.get_device_name(0)}
+
+    for name, flags in (("exp1_ordering", 0), ("exp2_gaussianity", oica.STOP_ON_GAUSSIANITY)):
+        cfg = datagen.EXPERIMENTS[name]
+        Xw, V, A, S = prepare(cfg)
+        rows = []
+        for L in Ls:
+            out, wall = run_batch(Xw, cfg, L, [cfg.cand_seed + t for t in range(a.runs)], flags)
+            row = {"L": L, "device_s_mean": float(np.mean([o[1] for o in out])), "wall_s_all_runs": wall}
+            if name == "exp1_ordering":
+                row["ordering_error"] = float(np.mean([ordering_error(o[0].W, V, A, S) for o in out]))
+            else:
+                row["estimated_non_gaussian"] = [int(o[0].n_extracted) for o in out]
+            rows.append(row)
+            print(name, row, flush=True)
+        res[name] = rows
+
+    if not a.skip_eeg:
+        cfg = datagen.get("cfg2_eeg_shaped")
+        Xw, V, A, S = prepare(cfg)
+        rows = []
+        for L in [int(x) for x in a.eeg_L.split(",")]:
+            out, wall = run_batch(Xw, cfg, L, [cfg.cand_seed + t for t in range(a.runs)], 0)
+            fl = fluctuation([o[0].W for o in out])
+            row = {"L": L, "fluctuation_mean": float(fl.mean()), "fluctuation_first10": [float(x) for x in fl[:10]],
+                   "device_s_mean": float(np.mean([o[1] for o in out])), "wall_s_all_runs": wall}
+            rows.append(row)
+            print("eeg", {k: v for k, v in row.items() if k != "fluctuation_first10"}, flush=True)
+        res["eeg_fluctuation"] = rows
+
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    json.dump(res, open(a.out, "w"), indent=1)
+    print("wrote", a.out)
+
+
+if __name__ == "__main__":
+    main()

@@ -290,3 +290,47 @@ def test_reduced_wide_tile_widths(N, k, precision):
             assert abs(out.W[k + j] @ W_or[k + j]) >= 0.9999
             assert abs((out.alpha[k + j] + 3) - (r.alpha + 3)) <= 1e-4 * (r.alpha + 3)
     assert np.abs(res.W[k:] @ Wp.T).max() < 1e-10
+
+
+# ---- the paper's artificial experiments: generalised
+# Gaussian rho grid, M = 1e4, K = 30, epsilon = 1e-6 (tol 5e-13), L swept
+@functools.lru_cache(maxsize=None)
+def _exp_prepared(name):
+    cfg = datagen.EXPERIMENTS[name]
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X32 = np.ascontiguousarray(Xw.astype(np.float32))
+    return cfg, X32
+
+
+@pytest.mark.parametrize("name", ["exp1_ordering", "exp2_gaussianity"])
+@pytest.mark.parametrize("L", [5, 20, 100])
+def test_paper_experiment_parity(name, L):
+    """Exp. 2's estimate of the number of non-Gaussian sources (the Gaussianity stop, PAPER.md:116-120,
+    :260-262) and every accepted component match the oracle at the paper's hyperparameters."""
+    cfg, X32 = _exp_prepared(name)
+    X64 = X32.astype(np.float64)
+    W_or, res_or, st_or = ordering.extract(X64, L, cfg.K, cfg.tol, cfg.N_out, cfg.cand_seed, stop_on_gaussianity=True,
+                                           keep_candidates=True)
+    with oica.Context(0, oica.PREC_AUTO) as ctx:
+        ctx.set_data(torch.from_numpy(X32).cuda())
+        ctx.init_candidates(cfg.cand_seed, L)
+        res = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=oica.STOP_ON_GAUSSIANITY)
+        red = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=oica.STOP_ON_GAUSSIANITY | oica.REDUCE_X)
+    n = W_or.shape[0]
+    for out in (res, red):
+        assert out.n_extracted == n and out.stopped == res_or[-1].stopped
+        for k, r in enumerate(res_or[:n]):
+            cos = abs(out.W[k] @ W_or[k])
+            rel = abs((out.alpha[k] + 3.0) - (r.alpha + 3.0)) / (r.alpha + 3.0)
+            assert cos >= 0.9999 and rel <= 1e-4, (k, cos, rel)
+            if out.index[k] != r.index:
+                # K = 30 with tol = 5e-13 (the paper's setting): which members of the winning cluster
+                # count as converged at the cap is arithmetic-dependent (A4; SURVEY §8(c) unpinned
+                # outcome (ii)), so q = min C may differ; the cluster (direction) is unique: the
+                # GPU's q must end, in the oracle, on the accepted optimum.
+                wq = st_or[k].W[int(out.index[k])]
+                assert 1.0 - abs(wq @ W_or[k]) <= 1e-6 or r.near_tie or out.near_tie[k], (k, out.index[k], r.index)
+                assert st_or[k].iters[int(out.index[k])] >= cfg.K - 3 or st_or[k].iters[r.index] >= cfg.K - 3
+    print(name, L, "estimated non-Gaussian sources", res.n_extracted, "index matches",
+          int(np.sum(res.index[:n] == np.array([r.index for r in res_or[:n]]))), "/", n)
