@@ -21,9 +21,12 @@
 //
 // Layout (NP <= 128, MT = 128):  TMEM  [W_hi NP/2 | (W_lo NP/2) | G NP | Y0 128 | Y1 128]
 //                                 SMEM  X stages [NP][128] fp16, 128B-swizzled (2 TMA boxes)
-// Layout (NP = 256, MT = 64):    TMEM  [W_hi 128 | G 256 | Y0 64 | Y1 64]
-//                                 SMEM  (W_lo [128][256], 4 K-major SW128 boxes) + X stages [256][64]
+//   (variant RG = 0: 4 Y slots of 64 samples, [NP][64] stages; kept for A/B timing)
+// Layout (NP > 128, MT = 64):    TMEM  [W_hi <=128 | G NP | Y0 64 | Y1 64]
+//                                 SMEM  (W_lo [128][NP], K-major SW128 boxes) + X stages [NP][64]
 // (W_lo parts only in the LO-capable instantiation, launched when the list has fine rows.)
+// GEMM1 runs R-1 chunks ahead of GEMM2 (R = number of Y slots), so the tensor pipe has
+// (R-1) GEMM1s queued while the epilogue cubes a chunk.
 // Y3 is written in place per 32-column group g: y^3 of columns [32g, 32g+32) as fp16 pairs in
 // columns [32g, 32g+16), so the GEMM2 A-operand K-slice kk sits at column 32(kk/2) + 8(kk%2).
 // Warp roles: 0 = TMA producer + TMEM allocator, 1 = MMA issuer (one elected lane), 2..5 =
@@ -179,12 +182,15 @@ __host__ __device__ constexpr uint32_t idesc_f16(int N, int b_mn_major) {
   return (1u << 4) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-template <int NP, bool SPLIT>   // SPLIT = LO-capable layout
+// SPLIT = LO-capable layout.  RG = Y-ring variant: 0 = default (narrow: 4 slots of 64 samples,
+// wide: 2 slots of 64), 1 = narrow with 2 slots of 128 (the previous layout, for A/B timing).
+template <int NP, bool SPLIT, int RG = 0>
 struct Cfg {
-  static constexpr bool WIDE = NP > 128;                         // NP = 256 layout
+  static constexpr bool WIDE = NP > 128;                         // wide layout (W_lo in SMEM)
   static constexpr bool WLO_TMEM = SPLIT && !WIDE;               // W_lo as a TMEM A operand
   static constexpr bool WLO_SMEM = SPLIT && WIDE;                // W_lo as an SMEM A operand
-  static constexpr int MT = WIDE ? 64 : 128;                     // samples per chunk (GEMM1 N)
+  static constexpr int MT = (!WIDE && RG == 1) ? 128 : 64;       // samples per chunk (GEMM1 N)
+  static constexpr int R = (!WIDE && RG == 0) ? 4 : 2;           // Y slots in TMEM (GEMM1 look-ahead R-1)
   static constexpr int XB = NP * 128;                            // bytes of one [NP][64] swizzled box
   static constexpr int X_STAGE = NP * MT * 2;                    // bytes per X stage
   static constexpr int WLO_BOXES = (NP + 63) / 64;               // 64-column K-major boxes of W_lo
@@ -194,19 +200,19 @@ struct Cfg {
   static constexpr int C_WHI = 0;
   static constexpr int C_WLO = NP / 2;                           // WLO_TMEM only
   static constexpr int C_G = WLO_TMEM ? NP : (WIDE ? 128 : NP / 2);
-  static constexpr int C_Y0 = C_G + NP;
-  static constexpr int C_Y1 = C_Y0 + MT;
-  static_assert(C_Y1 + MT <= 512, "TMEM budget");
+  static constexpr int C_Y0 = C_G + NP;                          // slot b at C_Y0 + b * MT
+  static_assert(C_Y0 + R * MT <= 512, "TMEM budget");
   static constexpr int SMEM = 1024 + WLO_BYTES + STAGES * X_STAGE + 1024;
 };
 
-// CL = cluster size sharing each X chunk (multicast); NW = epilogue warps (4 or 8)
-template <int NP, bool SPLIT, int EPI, int CL, int NW>
-__global__ void __launch_bounds__(64 + 32 * NW, 1)
+// CL = cluster size sharing each X chunk (multicast); RG = Y-ring variant (Cfg)
+template <int NP, bool SPLIT, int EPI, int CL, int RG>
+__global__ void __launch_bounds__(192, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
           const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_ub, int64_t M, int64_t slot_len,
           float* __restrict__ Gp, int64_t cap, int n_tiles, int tile_lo0_h, int order, int S_, const int* __restrict__ cnt) {
-  using C = Cfg<NP, SPLIT>;
+  constexpr int NW = 4;   // epilogue warps
+  using C = Cfg<NP, SPLIT, RG>;
   constexpr int MT = C::MT;
   // MODE 0 = the step; timing experiments (scripts/tc_variants.py): 3 = no
   // epilogue (MMA + data), 4 = GEMM1 only, 5 = GEMM2 only, 6 = no MMA (X streaming only)
@@ -221,9 +227,9 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   uint64_t* empty = full + C::STAGES;        // [STAGES]
   uint64_t* wlo_full = empty + C::STAGES;    // 1
   uint64_t* w_ready = wlo_full + 1;          // 1
-  uint64_t* yfull = w_ready + 1;             // [2]
-  uint64_t* y3ready = yfull + 2;             // [2]
-  uint64_t* gdone = y3ready + 2;             // 1
+  uint64_t* yfull = w_ready + 1;             // [R]
+  uint64_t* y3ready = yfull + 4;             // [R]
+  uint64_t* gdone = y3ready + 4;             // 1
   uint32_t* tmem_slot = (uint32_t*)(gdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -248,7 +254,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     }
     mbar_init(wlo_full, 1);
     mbar_init(w_ready, EPI_ARRIVALS);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < C::R; ++b) {
       mbar_init(&yfull[b], 1);
       mbar_init(&y3ready[b], EPI_ARRIVALS);
     }
@@ -311,7 +317,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (C::WLO_SMEM && lo_pass) mbar_wait(wlo_full, 0);
     tc_fence_after();
     auto gemm1 = [&](int j) {
-      const int st = j % C::STAGES, b = j & 1;
+      const int st = j % C::STAGES, b = j % C::R;
       mbar_wait(&full[st], (j / C::STAGES) & 1);
       tc_fence_after();
       if (MODE == 5 || MODE == 6) {   // experiment: GEMM2 only / no MMA
@@ -321,7 +327,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       }
       if (elect_one()) {
         const uint64_t bx = dx0 + (uint64_t)((st * C::X_STAGE) >> 4);
-        const uint32_t t_y = tmem + (b ? C::C_Y1 : C::C_Y0);
+        const uint32_t t_y = tmem + C::C_Y0 + b * MT;
 #pragma unroll
         for (int kb = 0; kb < NP / 16; ++kb)   // pass 1: W_hi (TMEM) x X
           mma_ts(t_y, tmem + C::C_WHI + kb * 8, bx + (uint64_t)(kb * 128), id1, kb > 0 ? 1u : 0u);
@@ -340,8 +346,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       __syncwarp();
     };
     auto gemm2 = [&](int j) {
-      const int st = j % C::STAGES, b = j & 1;
-      mbar_wait(&y3ready[b], (j >> 1) & 1);
+      const int st = j % C::STAGES, b = j % C::R;
+      mbar_wait(&y3ready[b], (j / C::R) & 1);
       tc_fence_after();
       if (MODE == 4 || MODE == 6) {   // experiment: GEMM1 only / no MMA
         if (elect_one()) {
@@ -352,7 +358,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       }
       if (elect_one()) {
         const uint64_t bk = dk0 + (uint64_t)((st * C::X_STAGE) >> 4);
-        const uint32_t t_y3 = tmem + (b ? C::C_Y1 : C::C_Y0);
+        const uint32_t t_y3 = tmem + C::C_Y0 + b * MT;
 #pragma unroll
         for (int kk = 0; kk < MT / 16; ++kk)
           mma_ts(t_g, t_y3 + (kk >> 1) * 32 + (kk & 1) * 8, bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2,
@@ -370,9 +376,11 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       }
       __syncwarp();
     };
-    if (nchunk > 0) gemm1(0);
+    // GEMM1 runs R-1 chunks ahead of GEMM2: slot (j+R-1) % R was last read by GEMM2(j-1),
+    // issued earlier on the in-order tensor pipe
+    for (int j = 0; j < C::R - 1 && j < nchunk; ++j) gemm1(j);
     for (int j = 0; j < nchunk; ++j) {
-      if (j + 1 < nchunk) gemm1(j + 1);
+      if (j + C::R - 1 < nchunk) gemm1(j + C::R - 1);
       gemm2(j);
     }
     if (elect_one()) tc_commit(gdone);
@@ -411,9 +419,9 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     // column 32*(kk/2) + 8*(kk%2))
     constexpr int NG = MT / 32 / NH;   // groups per warp
     for (int j = 0; j < nchunk; ++j) {
-      const int b = j & 1;
-      const uint32_t t_y = tmem + lane_off + (b ? C::C_Y1 : C::C_Y0);
-      mbar_wait(&yfull[b], (j >> 1) & 1);
+      const int b = j % C::R;
+      const uint32_t t_y = tmem + lane_off + C::C_Y0 + b * MT;
+      mbar_wait(&yfull[b], (j / C::R) & 1);
       tc_fence_after();
       if (MODE >= 3) {   // experiment: no TMEM traffic (MMA pipeline upper bound)
         tc_fence_before();
@@ -508,11 +516,11 @@ CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld,
   return m;
 }
 
-template <int NP, bool SPLIT, int EPI, int CL, int NW>
+template <int NP, bool SPLIT, int EPI, int CL, int RG>
 void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt) {
-  using C = Cfg<NP, SPLIT>;
-  auto kern = k_step_tc<NP, SPLIT, EPI, CL, NW>;
+  using C = Cfg<NP, SPLIT, RG>;
+  auto kern = k_step_tc<NP, SPLIT, EPI, CL, RG>;
   static bool attr = false;
   if (!attr) {
     OICA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -526,7 +534,7 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   static int order = [] { const char* e = getenv("OICA_TC_ORDER"); return e ? atoi(e) : 0; }();
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(n_tiles * S));
-  lc.blockDim = dim3(64 + 32 * NW);
+  lc.blockDim = dim3(192);
   lc.dynamicSmemBytes = C::SMEM;
   lc.stream = st;
   cudaLaunchAttribute at[1];
@@ -547,11 +555,19 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
   // where X streaming through L2 (~6 TB/s) otherwise paces the kernel; OICA_TC_CL=1|2 overrides.
   static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
   const int cl = cl_env ? cl_env : (NP > 128 ? 2 : 1);
+  // narrow tiles: 2 Y slots of 128 samples (default) or, OICA_TC_RING=4, 4 slots of 64 samples
+  // (measured slower: 7.7 vs 7.0 ms per cfg-3 step, profiles/r01/tc_experiments)
+  static int rg = [] { const char* e = getenv("OICA_TC_RING"); return e && atoi(e) == 4 ? 0 : 1; }();
   constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
-  if (cl == 2)
-    launch_cl<NP, SPLIT, EPI, CL2, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
+  const bool r1 = NP <= 128 && rg == 1;
+  if (cl == 2 && r1)
+    launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
+  else if (cl == 2)
+    launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
+  else if (r1)
+    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
   else
-    launch_cl<NP, SPLIT, EPI, 1, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
+    launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
 }
 
 template <int NP, bool SPLIT>

@@ -41,7 +41,9 @@ struct DevBuf {
 
 // Split-M slot policy: S depends only on M, so per-row results are identical
 // for any GPU count in L-shard mode and any active-set size.
-constexpr int64_t kSlotTarget = 8192;   // samples per slot (lower bound)
+constexpr int64_t kSlotTarget = 32768;  // samples per slot (target) ...
+constexpr int64_t kSlotMin = 8192;      // ... but at least 30 slots of >= this many samples
+constexpr int kMinSlots = 30;
 constexpr int kMaxSlots = 128;
 constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
 constexpr int64_t kSlotAlign = 128;
@@ -213,7 +215,12 @@ void jacobi_eigh(std::vector<double>& A, int n, std::vector<double>& d, std::vec
 }
 
 void plan_slots(oica_ctx* c) {
-  int64_t S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, c->Mg / kSlotTarget));
+  // one CTA per (row tile, slot): long slots amortise each CTA's set-up (TMEM allocation, W
+  // load, pipeline fill, G flush: ~13% of the step at 8192-sample slots and N = 128), while
+  // >= 30 slots keep >= 30 CTAs per row tile for the wave quantisation of small L
+  static int64_t target = [] { const char* e = getenv("OICA_SLOT_TARGET"); return e ? atoll(e) : kSlotTarget; }();
+  int64_t S = std::max<int64_t>(std::min<int64_t>(kMinSlots, c->Mg / kSlotMin), c->Mg / target);
+  S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, S));
   // slot length is a function of the GLOBAL M only (determinism across GPU counts)
   int64_t len = round_up(ceil_div(c->Mg, S), kSlotAlign);
   c->slot_len = len;
