@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(256) k_reduce_apply(const float* __restrict__ 
     for (int j = 0; j < 8; ++j) {
       int64_t m = m0 + tm * 8 + j;
       if (r < d && m < M) Xr[(int64_t)r * ldr + m] = acc[i][j];
-      if (Xh && r < NPd && m < ldx) Xh[(int64_t)r * ldx + m] = __float2half_rn((r < d && m < M) ? acc[i][j] : 0.f);
+      if (Xh && r < NPd && m < ldx)
+        Xh[(int64_t)r * ldx + m] = __float2half_rn((r < d && m < M) ? acc[i][j] * kXScale : 0.f);
     }
   }
 }

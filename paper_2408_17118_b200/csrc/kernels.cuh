@@ -105,6 +105,11 @@ int launch_merge_accept(cudaStream_t st, const RankSummary* all, const double* w
                         double* w_out);
 
 // ---- fused tensor-core step (k_step_tc.cu)
+// The fp16 X plane holds x * 2^-6 and the operand rows 2^4 w, so the GEMM1 accumulator is y / 4
+// and its cube is directly the fp16 GEMM2 operand y^3 2^-6 (two multiplies per element); G is
+// unscaled (x 2^12, exact) at the slot flush.  |x| < 2^-8 becomes fp16-subnormal (absolute
+// error <= 2^-19 in x units, below the normal rounding of |x| ~ 2^-8).
+constexpr float kXScale = 0x1.0p-6f;
 struct TcPlan;
 bool tc_supported(int N);
 int tc_np(int N);
