@@ -177,6 +177,8 @@ oica_status oica_init_candidates(oica_ctx* ctx, uint64_t seed, int64_t L);
  * (A1/A2; the paper's chord eps corresponds to tol = eps^2/2).  W_prefix (host fp64
  * k_prefix x N, orthonormal rows, may be NULL when k_prefix == 0) seeds the accepted rows
  * (resume / teacher forcing).  Writes rows k_prefix .. n_extracted-1 of out (synchronous).
+ * With world > 1 the call is collective: every rank passes the same arguments (checked by a
+ * hash all-reduce; a mismatch returns INVALID_ARGUMENT on every rank).
  * Errors: ALL_CANDIDATES_DEGENERATE, DOMAIN, INVALID_ARGUMENT (N_out outside [k_prefix+1, N]). */
 oica_status oica_extract_components(oica_ctx* ctx, int32_t N_out, int32_t max_iter, double tol,
                                     uint32_t flags, const double* W_prefix, int32_t k_prefix,

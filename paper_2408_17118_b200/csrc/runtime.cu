@@ -96,6 +96,7 @@ struct oica_ctx {
   DevBuf<float> W32;
   DevBuf<__half> Whi, Wlo;
   DevBuf<int> act0, act1, iters, Lact_dev, hist;
+  DevBuf<int64_t> arghash;
   DevBuf<uint8_t> state, keep, fine;
   DevBuf<double> dprev;
   int* Lact_host = nullptr;   // mapped: [L_act, n_coarse]
@@ -437,6 +438,31 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
   OICA_REQUIRE(k_prefix == 0 || W_prefix, OICA_ERR_INVALID_ARGUMENT, "W_prefix is NULL");
   const int N = (int)c->N;
   cudaStream_t st = c->st;
+  if (c->world() > 1) {   // collective call: every rank must pass the same arguments
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* p, size_t n) {
+      const unsigned char* b = (const unsigned char*)p;
+      for (size_t q = 0; q < n; ++q) h = (h ^ b[q]) * 1099511628211ull;   // FNV-1a
+    };
+    mix(&N_out, sizeof N_out);
+    mix(&K, sizeof K);
+    mix(&tol, sizeof tol);
+    mix(&flags, sizeof flags);
+    mix(&k_prefix, sizeof k_prefix);
+    mix(&c->N, sizeof c->N);
+    mix(&c->Mg, sizeof c->Mg);
+    mix(&c->seed, sizeof c->seed);
+    mix(&c->L, sizeof c->L);
+    if (k_prefix > 0) mix(W_prefix, sizeof(double) * k_prefix * N);
+    int64_t v[2] = {(int64_t)(h >> 2), -(int64_t)(h >> 2)}, r[2] = {0, 0};
+    c->arghash.ensure(2);
+    OICA_CUDA(cudaMemcpyAsync(c->arghash.p, v, sizeof v, cudaMemcpyHostToDevice, st));
+    OICA_NCCL(Nccl::get().AllReduce(c->arghash.p, c->arghash.p, 2, ncclInt64, ncclMax, c->comm, st));
+    OICA_CUDA(cudaMemcpyAsync(r, c->arghash.p, sizeof r, cudaMemcpyDeviceToHost, st));
+    OICA_CUDA(cudaStreamSynchronize(st));
+    OICA_REQUIRE(r[0] == v[0] && r[1] == v[1], OICA_ERR_INVALID_ARGUMENT,
+                 "ranks called oica_extract_components with different arguments");
+  }
   if (k_prefix > 0)
     OICA_CUDA(cudaMemcpyAsync(c->Wacc.p, W_prefix, sizeof(double) * k_prefix * N, cudaMemcpyHostToDevice, st));
   out->n_extracted = k_prefix;
