@@ -42,7 +42,7 @@ struct DevBuf {
 // Split-M slot policy: S depends only on M, so per-row results are identical
 // for any GPU count in L-shard mode and any active-set size.
 constexpr int64_t kSlotTarget = 32768;  // samples per slot (target) ...
-constexpr int64_t kSlotMin = 8192;      // ... but at least 30 slots of >= this many samples
+constexpr int64_t kSlotMin = 1024;      // ... but up to 30 slots of >= this many samples
 constexpr int kMinSlots = 30;
 constexpr int kMaxSlots = 128;
 constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
@@ -126,7 +126,10 @@ struct oica_ctx {
     return tc() ? Promotion{fine.p, dprev.p, kPromoteD, kPromoteT} : Promotion{nullptr, nullptr, 0.0, 0};
   }
   const uint8_t* fine_flags() const { return tc() ? fine.p : nullptr; }
-  bool mshard() const { return cfg.world > 1 && cfg.shard_mode == OICA_SHARD_M; }
+  // a communicator exists for world > 1, or at world == 1 when a unique id is passed (the
+  // exchange / allreduce code paths then run over one rank: tests on a single GPU)
+  bool mshard() const { return comm && cfg.shard_mode == OICA_SHARD_M; }
+  bool collective() const { return comm != nullptr; }
 
   void count(int n) { stats.kernel_launches += n; }
   cudaEvent_t event() {
@@ -217,8 +220,8 @@ void jacobi_eigh(std::vector<double>& A, int n, std::vector<double>& d, std::vec
 
 void plan_slots(oica_ctx* c) {
   // one CTA per (row tile, slot): long slots amortise each CTA's set-up (TMEM allocation, W
-  // load, pipeline fill, G flush: ~13% of the step at 8192-sample slots and N = 128), while
-  // >= 30 slots keep >= 30 CTAs per row tile for the wave quantisation of small L
+  // load, pipeline fill, G flush: ~13% of the step at 8192-sample slots and N = 128), while up
+  // to 30 slots (of >= 1024 samples) keep enough CTAs per row tile for small L and small M
   static int64_t target = [] { const char* e = getenv("OICA_SLOT_TARGET"); return e ? atoll(e) : kSlotTarget; }();
   int64_t S = std::max<int64_t>(std::min<int64_t>(kMinSlots, c->Mg / kSlotMin), c->Mg / target);
   S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, S));
@@ -438,7 +441,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
   OICA_REQUIRE(k_prefix == 0 || W_prefix, OICA_ERR_INVALID_ARGUMENT, "W_prefix is NULL");
   const int N = (int)c->N;
   cudaStream_t st = c->st;
-  if (c->world() > 1) {   // collective call: every rank must pass the same arguments
+  if (c->collective()) {   // collective call: every rank must pass the same arguments
     uint64_t h = 1469598103934665603ull;
     auto mix = [&](const void* p, size_t n) {
       const unsigned char* b = (const unsigned char*)p;
@@ -573,7 +576,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     const RankSummary* all = c->summary.p;
     const double* wall = c->wsum.p;
     int world = 1;
-    if (c->world() > 1 && !c->mshard()) {  // L-shard: one exchange per component (C1)
+    if (c->collective() && !c->mshard()) {  // L-shard: one exchange per component (C1)
       auto& nc = Nccl::get();
       OICA_NCCL(nc.AllGather(c->summary.p, c->summary_all.p, sizeof(RankSummary), ncclUint8, c->comm, st));
       OICA_NCCL(nc.AllGather(c->wsum.p, c->wsum_all.p, (size_t)kMaxClusters * vN, ncclFloat64, c->comm, st));
@@ -733,7 +736,7 @@ oica_status oica_create(const oica_config* cfg, oica_ctx** out) {
       c->own_stream = true;
     }
     OICA_CUDA(cudaHostAlloc((void**)&c->Lact_host, 2 * sizeof(int), cudaHostAllocMapped));
-    if (cfg->world > 1) {
+    if (cfg->world > 1 || cfg->nccl_unique_id) {
       ncclUniqueId id;
       std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
       OICA_NCCL(Nccl::get().CommInitRank(&c->comm, cfg->world, id, cfg->rank));

@@ -212,7 +212,7 @@ class Context:
 
     def __init__(self, device: int = 0, precision: int = PREC_AUTO, rank: int = 0, world: int = 1,
                  shard_mode: int = SHARD_L, stream=None, nccl_id: Optional[bytes] = None):
-        if world > 1:
+        if world > 1 or nccl_id is not None:
             _point_to_torch_nccl()
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         cfg = Config(device, rank, world, shard_mode, precision, 0,

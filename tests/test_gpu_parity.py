@@ -334,3 +334,27 @@ def test_paper_experiment_parity(name, L):
                 assert st_or[k].iters[int(out.index[k])] >= cfg.K - 3 or st_or[k].iters[r.index] >= cfg.K - 3
     print(name, L, "estimated non-Gaussian sources", res.n_extracted, "index matches",
           int(np.sum(res.index[:n] == np.array([r.index for r in res_or[:n]]))), "/", n)
+
+
+# ---- the multi-rank code paths on one GPU: a one-rank NCCL communicator makes the L-shard
+# exchange (two all-gathers + device merge per component) and the M-shard per-iteration fp64
+# all-reduce run for real; the decisions must be those of the oracle
+@pytest.mark.parametrize("name,precision", [("p_n40", oica.PREC_FP32), ("p_tc_n128", oica.PREC_AUTO)])
+@pytest.mark.parametrize("shard", [oica.SHARD_L, oica.SHARD_M])
+def test_exchange_paths_single_rank(name, precision, shard):
+    cfg, X32, X64 = prepared(name)
+    W_or, res_or, _ = oracle_run(name)
+    nid = oica.nccl_unique_id()
+    with oica.Context(0, precision, rank=0, world=1, shard_mode=shard, nccl_id=nid) as ctx:
+        ctx.set_data(torch.from_numpy(X32).cuda(), M_global=cfg.M)
+        ctx.init_candidates(cfg.cand_seed, cfg.L)
+        res = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
+        red = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=oica.REDUCE_X)
+    for out in (res, red):
+        _compare(out, res_or, W_or, X64)
+    if shard == oica.SHARD_L:   # the exchange does not change the arithmetic: bitwise equal
+        with oica.Context(0, precision) as ctx:
+            ctx.set_data(torch.from_numpy(X32).cuda())
+            ctx.init_candidates(cfg.cand_seed, cfg.L)
+            plain = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
+        assert np.array_equal(plain.W, res.W) and np.array_equal(plain.index, res.index)
