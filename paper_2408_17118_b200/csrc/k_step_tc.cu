@@ -551,10 +551,11 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
 template <int NP, bool SPLIT, int EPI>
 void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
                     int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt) {
-  // Cluster multicast of the X chunks: on by default for the NP = 256 layout,
-  // where X streaming through L2 (~6 TB/s) otherwise paces the kernel; OICA_TC_CL=1|2 overrides.
+  // Cluster multicast of the X chunks: on by default for NP > 64, where the X
+  // stream through L2 (~6 TB/s) otherwise paces or co-limits the kernel (cfg-4 shape +20%, cfg-3
+  // shape +6%; neutral at NP = 64, which is latency-bound); OICA_TC_CL=1|2 overrides.
   static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
-  const int cl = cl_env ? cl_env : (NP > 128 ? 2 : 1);
+  const int cl = cl_env ? cl_env : (NP > 64 ? 2 : 1);
   // narrow tiles: 2 Y slots of 128 samples (default) or, OICA_TC_RING=4, 4 slots of 64 samples
   // (measured slower: 7.7 vs 7.0 ms per cfg-3 step, profiles/r01/tc_experiments)
   static int rg = [] { const char* e = getenv("OICA_TC_RING"); return e && atoi(e) == 4 ? 0 : 1; }();
