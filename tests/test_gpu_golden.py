@@ -1,0 +1,77 @@
+"""GPU parity against stored ORACLE results at full BASELINE sizes (SURVEY §8(c) tiers A and B).
+
+tests/golden/oracle_*.json are written by scripts/make_golden.py, which calls only oracle/ and
+datagen/: cfg 0 (3 seeds), cfg 1 and cfg 2 at full L with all N_out components (tier A) and
+cfg 3 at full N, M with the exact sub-problem L' = 256 (tier B).  The inputs are rebuilt here
+exactly (datagen on the CPU, oracle whitening, fp32; SHA-256 checked) and run through the C ABI
+in the bench's launch configuration (AUTO precision: tensor cores for M >= 131072).
+
+Gates (north_star): identical accepted indices, |cos| >= 0.9999, objective rel. error <= 1e-4.
+  * teacher-forced: component k is extracted with the oracle's accepted rows 1..k-1 as the
+    prefix (an oracle value, not a GPU one), so one near-tie cannot cascade;
+  * free-running: compared until the first component the oracle or the GPU flags as a near-tie.
+"""
+import glob
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import datagen
+from oracle import whiten
+from paper_2408_17118_b200 import oica
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = sorted(glob.glob(os.path.join(HERE, "golden", "oracle_*.json")))
+
+
+def _input(g):
+    cfg = datagen.get(g["config"]).with_(data_seed=g["data_seed"], cand_seed=g["cand_seed"], L=g["L"],
+                                         N_out=g["N_out"])
+    ds = datagen.make_dataset(cfg, keep_sources=False)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X32 = np.ascontiguousarray(Xw.astype(np.float32))
+    assert hashlib.sha256(X32.tobytes()).hexdigest() == g["x32_sha256"], "input drifted from the golden's"
+    return cfg, X32
+
+
+def _gate(k, idx, w, alpha, c):
+    cos = abs(float(np.asarray(w) @ np.asarray(c["w"])))
+    rel = abs((alpha + 3.0) - (c["alpha"] + 3.0)) / abs(c["alpha"] + 3.0)
+    assert idx == c["index"], (k, idx, c["index"])
+    assert cos >= 0.9999 and rel <= 1e-4, (k, cos, rel)
+    return 1.0 - cos, rel
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[7:-5] for p in GOLDEN])
+def test_gpu_matches_oracle_golden(path):
+    g = json.load(open(path))
+    cfg, X32 = _input(g)
+    comps = g["components"]
+    Wg = np.array([c["w"] for c in comps])
+    worst = [0.0, 0.0]
+    with oica.Context(0, oica.PREC_AUTO) as ctx:
+        ctx.set_data(torch.from_numpy(X32).cuda())
+        ctx.init_candidates(cfg.cand_seed, cfg.L)
+        # teacher-forced, one component per call
+        for k, c in enumerate(comps):
+            r = ctx.extract(k + 1, cfg.K, cfg.tol, W_prefix=Wg[:k] if k else None)
+            if r.index[k] != c["index"] and (c["near_tie"] or r.near_tie[k]):
+                continue
+            d, rel = _gate(k, int(r.index[k]), r.W[k], float(r.alpha[k]), c)
+            worst = [max(worst[0], d), max(worst[1], rel)]
+        # free-running
+        r = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
+        matched = 0
+        for k, c in enumerate(comps):
+            if c["near_tie"] or r.near_tie[k]:
+                break
+            _gate(k, int(r.index[k]), r.W[k], float(r.alpha[k]), c)
+            matched += 1
+        prec = ctx.stats()["precision"]
+    print(os.path.basename(path), "precision", prec, "components", len(comps), "free-running matched", matched,
+          "worst 1-cos", worst[0], "worst rel", worst[1])
