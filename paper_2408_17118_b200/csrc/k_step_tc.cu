@@ -591,7 +591,7 @@ void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP
     case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 64: launch_variant<64, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 64: launch_epi<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
     case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
