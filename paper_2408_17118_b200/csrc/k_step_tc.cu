@@ -434,22 +434,30 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       tmem_wait_ld();
 #pragma unroll
       for (int u = 0; u < NG; ++u) {
-        uint32_t pk[16], pl[16];
+        uint32_t pk[16];
+        if (SPLIT && lo_pass) {   // fine tile: also the fp16 residual y^3 2^-6 - hi (GEMM2 second pass)
+          uint32_t pl[16];
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          // accumulator = 2^4 y 2^-6 = y / 4 (W scaled by 2^4, X by 2^-6)  ->  acc^3 = 2^-6 y^3
-          float a0 = __uint_as_float(v[u][k]), a1 = __uint_as_float(v[u][k + 1]);
-          float c0 = a0 * a0 * a0, c1 = a1 * a1 * a1;
-          __half2 hh = __floats2half2_rn(c0, c1);
-          pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
-          if (SPLIT) {   // residual y^3 2^-6 - hi (fine tiles: GEMM2 second pass)
+          for (int k = 0; k < 32; k += 2) {
+            float a0 = __uint_as_float(v[u][k]), a1 = __uint_as_float(v[u][k + 1]);
+            float c0 = a0 * a0 * a0, c1 = a1 * a1 * a1;
+            __half2 hh = __floats2half2_rn(c0, c1);
+            pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
             float2 hf = __half22float2(hh);
             __half2 hl = __floats2half2_rn(c0 - hf.x, c1 - hf.y);
             pl[k / 2] = *reinterpret_cast<uint32_t*>(&hl);
           }
+          tmem_st16(t_y + 32 * (h + NH * u) + 16, pl);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            // accumulator = 2^4 y 2^-6 = y / 4 (W scaled by 2^4, X by 2^-6)  ->  acc^3 = 2^-6 y^3
+            float a0 = __uint_as_float(v[u][k]), a1 = __uint_as_float(v[u][k + 1]);
+            __half2 hh = __floats2half2_rn(a0 * a0 * a0, a1 * a1 * a1);
+            pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
+          }
         }
         tmem_st16(t_y + 32 * (h + NH * u), pk);   // Y^3 (fp16 pairs): A operand of GEMM2
-        if (lo_pass) tmem_st16(t_y + 32 * (h + NH * u) + 16, pl);
       }
       tmem_wait_st();
       tc_fence_before();
@@ -626,6 +634,8 @@ int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, in
                    const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
                    const int* cnt, bool lo_capable) {
   if (L_act <= 0) return 0;
+  static bool force_lo = getenv("OICA_TC_FORCE_LO") != nullptr;   // experiment: LO-capable layout always
+  lo_capable = lo_capable || force_lo;
   if (lo_capable || n_coarse < L_act)   // fine rows (possibly): LO-capable layout, 2nd pass from tile n_coarse/128
     launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse / 128, cnt);
   else
