@@ -162,7 +162,7 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
     state[l] = deg ? ST_DEGENERATE : (conv ? ST_CONVERGED : ST_ACTIVE);
     keep[a] = (deg || conv) ? 0 : 1;
     if (pr.fine && !deg && !conv) {                       // DESIGN.md §5 precision promotion
-      if (!pr.fine[l] && ((dd <= pr.d_promote && dd > 1e-3 * pr.dprev[l]) || t >= pr.t_force)) pr.fine[l] = 1;
+      if (!pr.fine[l] && ((dd <= pr.d_promote && dd > pr.ratio * pr.dprev[l]) || t >= pr.t_force)) pr.fine[l] = 1;
       pr.dprev[l] = dd;
     }
   }

@@ -55,11 +55,12 @@ struct EvalPoint {
 
 // ---- K3: fp64 epilogue: slot sum, /M - 3w, projection, normalise, convergence
 // Precision promotion (TC): an unconverged row becomes fine when its step
-// distance d <= d_promote stagnates (d > 1e-3 d_prev) or t >= t_force.  fine may be null.
+// distance d <= d_promote stagnates (d > ratio d_prev) or t >= t_force.  fine may be null.
 struct Promotion {
   uint8_t* fine;
   double* dprev;
   double d_promote;
+  double ratio;   // stagnation: d > ratio * d_prev
   int t_force;
 };
 int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,

@@ -49,6 +49,7 @@ constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
 constexpr int64_t kSlotAlign = 128;
 constexpr int64_t kTcMinSamples = 131072;   // OICA_PREC_AUTO switches to tensor cores at this M
 constexpr double kPromoteD = 1e-6;          // TC precision promotion: stagnating d below this ...
+constexpr double kPromoteRatio = 0.3;       // ... (d > this * d_prev: stagnating) ...
 constexpr int kPromoteT = 40;               // ... or t >= this
 constexpr int kBatchRows = 2048;            // below this many active rows, iterations are enqueued ...
 constexpr int kBatch = 8;                   // ... this many at a time without a host round trip
@@ -123,7 +124,10 @@ struct oica_ctx {
     return tc() ? EvalPoint{Whi.p, Wlo.p, nullptr, vNP} : EvalPoint{nullptr, nullptr, W32.p, vNP};
   }
   Promotion promotion() const {
-    return tc() ? Promotion{fine.p, dprev.p, kPromoteD, kPromoteT} : Promotion{nullptr, nullptr, 0.0, 0};
+    static const double pd = getenv("OICA_PROMOTE_D") ? atof(getenv("OICA_PROMOTE_D")) : kPromoteD;
+    static const double pr = getenv("OICA_PROMOTE_RATIO") ? atof(getenv("OICA_PROMOTE_RATIO")) : kPromoteRatio;
+    static const int pt = getenv("OICA_PROMOTE_T") ? atoi(getenv("OICA_PROMOTE_T")) : kPromoteT;
+    return tc() ? Promotion{fine.p, dprev.p, pd, pr, pt} : Promotion{nullptr, nullptr, 0.0, 0.0, 0};
   }
   const uint8_t* fine_flags() const { return tc() ? fine.p : nullptr; }
   // a communicator exists for world > 1, or at world == 1 when a unique id is passed (the
