@@ -616,13 +616,23 @@ void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP
   }
 }
 
-__global__ void k_x_prepare_f16(const float* __restrict__ X, int64_t ld, int N, int64_t M, int NP, int64_t ldx,
+// fp16 plane row n = fp16(x_n 2^-6), zero padded to NP rows and ldx columns.  One thread per 8
+// consecutive samples of a row (blockIdx.y = row): coalesced fp32 reads, one 16-byte store.
+__global__ void k_x_prepare_f16(const float* __restrict__ X, int64_t ld, int N, int64_t M, int64_t ldx,
                                 __half* __restrict__ Xh) {
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t n = idx / ldx, m = idx % ldx;
-  if (n >= NP) return;
-  float v = (n < N && m < M) ? X[n * ld + m] : 0.f;
-  Xh[idx] = __float2half_rn(v * kXScale);
+  const int n = blockIdx.y;
+  const int64_t m0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (m0 >= ldx) return;
+  const float* x = X + (int64_t)n * ld;
+  __align__(16) __half2 h[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t m = m0 + 2 * k;
+    float a = (n < N && m < M) ? __ldg(x + m) : 0.f;
+    float b = (n < N && m + 1 < M) ? __ldg(x + m + 1) : 0.f;
+    h[k] = __floats2half2_rn(a * kXScale, b * kXScale);
+  }
+  *reinterpret_cast<uint4*>(Xh + (int64_t)n * ldx + m0) = *reinterpret_cast<uint4*>(h);
 }
 
 }  // namespace
@@ -645,8 +655,8 @@ int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, in
 
 int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP, int64_t ldx,
                          __half* Xh) {
-  int64_t tot = (int64_t)NP * ldx;
-  k_x_prepare_f16<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(X, ld, N, M, NP, ldx, Xh);
+  dim3 grid((unsigned)ceil_div(ldx / 8, 256), (unsigned)NP);   // ldx is a multiple of 128
+  k_x_prepare_f16<<<grid, 256, 0, st>>>(X, ld, N, M, ldx, Xh);
   return 1;
 }
 

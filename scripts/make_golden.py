@@ -7,7 +7,8 @@ Calls only oracle/ and datagen/ (no CUDA path): the stored expected values are t
 Inputs: datagen's seeded raw signals on the CPU, whitened by the oracle in fp64 and cast to
 fp32 (the GPU tests rebuild exactly these fp32 values and check the stored SHA-256).
   tier A: cfg 0 (3 data/candidate seeds), cfg 1 and cfg 2 at full L, all N_out components
-  tier B: cfg 3 at full N, M with L' = 256 (candidate ids 0..255: an exact sub-problem)
+  tier B: cfgs 3 and 4 at full N, M with L' = 256 (candidate ids 0..255: an exact sub-problem),
+          the first 8 (cfg 3) / 4 (cfg 4) components
 """
 from __future__ import annotations
 
@@ -30,6 +31,7 @@ JOBS = {
     "cfg1": ("cfg1_artificial", 0, None, None),
     "cfg2": ("cfg2_eeg_shaped", 0, None, None),
     "cfg3_L256": ("cfg3_large", 0, 256, 8),
+    "cfg4_L256": ("cfg4_scaling", 0, 256, 4),
 }
 
 
