@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -42,7 +44,7 @@ struct DevBuf {
 // Split-M slot policy: S depends only on M, so per-row results are identical
 // for any GPU count in L-shard mode and any active-set size.
 constexpr int64_t kSlotTarget = 32768;  // samples per slot (target) ...
-constexpr int64_t kSlotMin = 1024;      // ... but up to 30 slots of >= this many samples
+constexpr int64_t kSlotMin = 128;       // ... but up to 30 slots of >= this many samples
 constexpr int kMinSlots = 30;
 constexpr int kMaxSlots = 128;
 constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
@@ -225,7 +227,7 @@ void jacobi_eigh(std::vector<double>& A, int n, std::vector<double>& d, std::vec
 void plan_slots(oica_ctx* c) {
   // one CTA per (row tile, slot): long slots amortise each CTA's set-up (TMEM allocation, W
   // load, pipeline fill, G flush: ~13% of the step at 8192-sample slots and N = 128), while up
-  // to 30 slots (of >= 1024 samples) keep enough CTAs per row tile for small L and small M
+  // to 30 slots (of >= 128 samples) keep enough CTAs per row tile for small L and small M
   static int64_t target = [] { const char* e = getenv("OICA_SLOT_TARGET"); return e ? atoll(e) : kSlotTarget; }();
   int64_t S = std::max<int64_t>(std::min<int64_t>(kMinSlots, c->Mg / kSlotMin), c->Mg / target);
   S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, S));
@@ -331,6 +333,24 @@ void account_iteration(oica_ctx* c, int L_act, int n_coarse) {
 }
 
 void check_launch() { OICA_CUDA(cudaGetLastError()); }
+
+// OICA_TRACE=1: per-component host wall-clock phases on stderr (development aid)
+struct PhaseTrace {
+  bool on = getenv("OICA_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  std::string line;
+  void mark(const char* what) {
+    if (!on) return;
+    auto t1 = std::chrono::steady_clock::now();
+    line += std::string(" ") + what + "=" +
+            std::to_string(std::chrono::duration<double, std::micro>(t1 - t0).count()).substr(0, 7) + "us";
+    t0 = t1;
+  }
+  void flush(int i) {
+    if (on) fprintf(stderr, "[oica] component %d:%s\n", i, line.c_str());
+    line.clear();
+  }
+};
 
 // ---- §3.3 reduction of X (Alg. 2 lines 4-12) ---------------------------
 // The paper builds the complement basis as G = (F~F~^T)^{-1/2} F~ with F = I - W^T W.  Any
@@ -488,6 +508,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     c->Wacc_scratch.ensure((size_t)N);
   }
   use_full_view(c);
+  PhaseTrace trace;
   for (int k = k_prefix; k < N_out; ++k) {
     const int i = k + 1;  // 1-based component index
     // Alg. 2 lines 4-12: iterate on X~ = G X in the d = N - k dimensional complement
@@ -507,6 +528,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     c->count(launch_compact(st, nullptr, c->keep.p, c->fine_flags(), (int)c->Ll, c->act0.p, c->Lact_dev.p,
                             c->Lact_host));
     OICA_CUDA(cudaStreamSynchronize(st));
+    trace.mark("init");
     int L_act = ((volatile int*)c->Lact_host)[0];
     int n_coarse = ((volatile int*)c->Lact_host)[1];
     int* act = c->act0.p;
@@ -553,6 +575,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
       L_ub = ((volatile int*)c->Lact_host)[0];
       nc_ub = ((volatile int*)c->Lact_host)[1];
     }
+    trace.mark("iterate");
     // per-iteration counts: entering iteration t' the active set had hist[t'-1] rows (t' >= 2)
     std::vector<int> hist(2 * (size_t)(t + 1), 0);
     if (t > 0) {
@@ -597,6 +620,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     OICA_CUDA(cudaMemcpyAsync(&rec_h, c->rec.p, sizeof(ComponentRecord), cudaMemcpyDeviceToHost, st));
     OICA_CUDA(cudaMemcpyAsync(b_host.data(), c->w_out.p, sizeof(double) * vN, cudaMemcpyDeviceToHost, st));
     c->harvest_events();
+    trace.mark("select");
     c->last_valid = true;
     if (rec_h.status != OICA_OK)
       throw Error((oica_status)rec_h.status,
@@ -645,6 +669,8 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
       break;
     }
     out->n_extracted = k + 1;
+    trace.mark("accept");
+    trace.flush(i);
   }
   use_full_view(c);
 }
