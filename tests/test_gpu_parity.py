@@ -358,3 +358,27 @@ def test_exchange_paths_single_rank(name, precision, shard):
             ctx.init_candidates(cfg.cand_seed, cfg.L)
             plain = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
         assert np.array_equal(plain.W, res.W) and np.array_equal(plain.index, res.index)
+
+
+# ---- shape edge cases: N = 1 and 2 (the feasible set is tiny), N just above a tile width (NP
+# 144 / 256 wide tiles with padding), L below one row tile, M not a multiple of anything
+@pytest.mark.parametrize("N,M,L,N_out,precision", [
+    (1, 1001, 7, 1, oica.PREC_FP32), (2, 3001, 33, 2, oica.PREC_FP32), (2, 3001, 33, 2, oica.PREC_TC),
+    (129, 20011, 64, 2, oica.PREC_TC), (129, 20011, 64, 2, oica.PREC_FP32), (255, 30001, 40, 2, oica.PREC_TC)])
+def test_shape_edge_cases(N, M, L, N_out, precision):
+    half = max(1, N // 2)
+    recipe = (("laplace", half),) + ((("gg_uniform", N - half, 0.5, 1.5),) if N - half else ())
+    cfg = Config(f"edge{N}", N, M, L, 200, 1e-10, N_out, recipe, data_seed=9000 + N, cand_seed=9100 + N)
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X32 = np.ascontiguousarray(Xw.astype(np.float32))
+    X64 = X32.astype(np.float64)
+    W_or, res_or = ordering.extract(X64, L, cfg.K, cfg.tol, N_out, cfg.cand_seed)
+    with oica.Context(0, precision) as ctx:
+        ctx.set_data(torch.from_numpy(X32).cuda())
+        ctx.init_candidates(cfg.cand_seed, L)
+        res = ctx.extract(N_out, cfg.K, cfg.tol)
+        red = ctx.extract(N_out, cfg.K, cfg.tol, flags=oica.REDUCE_X)
+    for out in (res, red):
+        assert out.n_extracted == N_out
+        _compare(out, res_or, W_or, X64)
