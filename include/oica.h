@@ -55,7 +55,7 @@ typedef enum {
 
 /* Arithmetic of the fixed-point contraction (the two products of PAPER.md:243-245). */
 typedef enum {
-  OICA_PREC_AUTO = 0,   /* TC when M_global >= 131072, else FP32              */
+  OICA_PREC_AUTO = 0,   /* TC when M_global >= 16384, else FP32               */
   OICA_PREC_FP32 = 1,   /* FP32 FFMA on CUDA cores, fp32 accumulate per flush, fp64 slots    */
   OICA_PREC_TC = 2,     /* tcgen05 tensor cores: fp16 X, one-pass fp16 GEMM1 on w_h =        */
                         /* fp16(2^4 w)/2^4 with eq. (5)'s -3w evaluated at w_h (consistent),  */

@@ -49,7 +49,7 @@ constexpr int kMinSlots = 30;
 constexpr int kMaxSlots = 128;
 constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
 constexpr int64_t kSlotAlign = 128;
-constexpr int64_t kTcMinSamples = 131072;   // OICA_PREC_AUTO switches to tensor cores at this M
+constexpr int64_t kTcMinSamples = 16384;    // OICA_PREC_AUTO switches to tensor cores at this M
 constexpr double kPromoteD = 1e-6;          // TC precision promotion: stagnating d below this ...
 constexpr double kPromoteRatio = 0.3;       // ... (d > this * d_prev: stagnating) ...
 constexpr int kPromoteT = 40;               // ... or t >= this

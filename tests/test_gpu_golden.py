@@ -4,7 +4,7 @@ tests/golden/oracle_*.json are written by scripts/make_golden.py, which calls on
 datagen/: cfg 0 (3 seeds), cfg 1 and cfg 2 at full L with all N_out components (tier A) and
 cfg 3 at full N, M with the exact sub-problem L' = 256 (tier B).  The inputs are rebuilt here
 exactly (datagen on the CPU, oracle whitening, fp32; SHA-256 checked) and run through the C ABI
-in the bench's launch configuration (AUTO precision: tensor cores for M >= 131072).
+in the bench's launch configuration (AUTO precision: tensor cores for M >= 16384).
 
 Gates (north_star): identical accepted indices, |cos| >= 0.9999, objective rel. error <= 1e-4.
   * teacher-forced: component k is extracted with the oracle's accepted rows 1..k-1 as the
