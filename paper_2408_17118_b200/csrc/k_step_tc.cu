@@ -189,7 +189,9 @@ struct Cfg {
   static constexpr bool WIDE = NP > 128;                         // wide layout (W_lo in SMEM)
   static constexpr bool WLO_TMEM = SPLIT && !WIDE;               // W_lo as a TMEM A operand
   static constexpr bool WLO_SMEM = SPLIT && WIDE;                // W_lo as an SMEM A operand
-  static constexpr int MT = (!WIDE && RG == 1) ? 128 : 64;       // samples per chunk (GEMM1 N)
+  // RG = 3 (NP <= 64): 2 slots of 192 samples -- more tensor work per chunk hand-off where the
+  // narrow MMAs are short (the hand-offs, not the MMAs, pace small NP)
+  static constexpr int MT = WIDE ? 64 : RG == 1 ? 128 : RG == 3 ? 192 : 64;   // samples per chunk (GEMM1 N)
   static constexpr int R = (!WIDE && RG == 0) ? 4 : 2;           // Y slots in TMEM (GEMM1 look-ahead R-1)
   static constexpr int XB = NP * 128;                            // bytes of one [NP][64] swizzled box
   static constexpr int X_STAGE = NP * MT * 2;                    // bytes per X stage
@@ -428,36 +430,41 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         mbar_arrive(&y3ready[b]);
         continue;
       }
-      uint32_t v[NG][32];
+      constexpr int GB = NG > 4 ? NG / 2 : NG;   // groups per TMEM-load batch (register budget)
 #pragma unroll
-      for (int u = 0; u < NG; ++u) tmem_ld32(t_y + 32 * (h + NH * u), v[u]);
-      tmem_wait_ld();
+      for (int g0 = 0; g0 < NG; g0 += GB) {
+        uint32_t v[GB][32];
 #pragma unroll
-      for (int u = 0; u < NG; ++u) {
-        uint32_t pk[16];
-        if (SPLIT && lo_pass) {   // fine tile: also the fp16 residual y^3 2^-6 - hi (GEMM2 second pass)
-          uint32_t pl[16];
+        for (int w = 0; w < GB; ++w) tmem_ld32(t_y + 32 * (h + NH * (g0 + w)), v[w]);
+        tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            float a0 = __uint_as_float(v[u][k]), a1 = __uint_as_float(v[u][k + 1]);
-            float c0 = a0 * a0 * a0, c1 = a1 * a1 * a1;
-            __half2 hh = __floats2half2_rn(c0, c1);
-            pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
-            float2 hf = __half22float2(hh);
-            __half2 hl = __floats2half2_rn(c0 - hf.x, c1 - hf.y);
-            pl[k / 2] = *reinterpret_cast<uint32_t*>(&hl);
+        for (int w = 0; w < GB; ++w) {
+          const int u = g0 + w;
+          uint32_t pk[16];
+          if (SPLIT && lo_pass) {   // fine tile: also the fp16 residual y^3 2^-6 - hi (GEMM2 second pass)
+            uint32_t pl[16];
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              float a0 = __uint_as_float(v[w][k]), a1 = __uint_as_float(v[w][k + 1]);
+              float c0 = a0 * a0 * a0, c1 = a1 * a1 * a1;
+              __half2 hh = __floats2half2_rn(c0, c1);
+              pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
+              float2 hf = __half22float2(hh);
+              __half2 hl = __floats2half2_rn(c0 - hf.x, c1 - hf.y);
+              pl[k / 2] = *reinterpret_cast<uint32_t*>(&hl);
+            }
+            tmem_st16(t_y + 32 * (h + NH * u) + 16, pl);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              // accumulator = 2^4 y 2^-6 = y / 4 (W scaled by 2^4, X by 2^-6)  ->  acc^3 = 2^-6 y^3
+              float a0 = __uint_as_float(v[w][k]), a1 = __uint_as_float(v[w][k + 1]);
+              __half2 hh = __floats2half2_rn(a0 * a0 * a0, a1 * a1 * a1);
+              pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
+            }
           }
-          tmem_st16(t_y + 32 * (h + NH * u) + 16, pl);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            // accumulator = 2^4 y 2^-6 = y / 4 (W scaled by 2^4, X by 2^-6)  ->  acc^3 = 2^-6 y^3
-            float a0 = __uint_as_float(v[u][k]), a1 = __uint_as_float(v[u][k + 1]);
-            __half2 hh = __floats2half2_rn(a0 * a0 * a0, a1 * a1 * a1);
-            pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
-          }
+          tmem_st16(t_y + 32 * (h + NH * u), pk);   // Y^3 (fp16 pairs): A operand of GEMM2
         }
-        tmem_st16(t_y + 32 * (h + NH * u), pk);   // Y^3 (fp16 pairs): A operand of GEMM2
       }
       tmem_wait_st();
       tc_fence_before();
@@ -568,7 +575,13 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
   // narrow tiles: 2 Y slots of 128 samples (default) or, OICA_TC_RING=4, 4 slots of 64 samples
   // (measured slower: 7.7 vs 7.0 ms per cfg-3 step, profiles/r01/tc_experiments)
   static int rg = [] { const char* e = getenv("OICA_TC_RING"); return e && atoi(e) == 4 ? 0 : 1; }();
+  static bool r192 = [] { const char* e = getenv("OICA_TC_RING"); return !(e && atoi(e) == 2); }();
   constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
+  if (NP <= 64 && r192 && cl == 1) {   // small NP: 2 Y slots of 192 samples (OICA_TC_RING=2: 2 x 128)
+    launch_cl<NP, SPLIT, EPI, 1, (NP <= 64 ? 3 : 1)>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0,
+                                                    cnt);
+    return;
+  }
   const bool r1 = NP <= 128 && rg == 1;
   if (cl == 2 && r1)
     launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);

@@ -48,7 +48,7 @@ constexpr int64_t kSlotMin = 128;       // ... but up to 30 slots of >= this man
 constexpr int kMinSlots = 30;
 constexpr int kMaxSlots = 128;
 constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
-constexpr int64_t kSlotAlign = 128;
+constexpr int64_t kSlotAlign = 384;       // multiple of every TC chunk width (64, 128, 192 samples)
 constexpr int64_t kTcMinSamples = 16384;    // OICA_PREC_AUTO switches to tensor cores at this M
 constexpr double kPromoteD = 1e-6;          // TC precision promotion: stagnating d below this ...
 constexpr double kPromoteRatio = 0.3;       // ... (d > this * d_prev: stagnating) ...
