@@ -322,6 +322,15 @@ def run_oica(args, cfg):
                  "traffic_launch": tr if tr else None,
                  "kernel": "fused fixed-point step (GEMM-cube-GEMM)", "launches": st["step_launches"],
                  "kernel_ms": st["step_ms"], "share_of_step": st["step_ms"] / ms if ms else None})
+    if precision.startswith("tc") and kern_tflops:
+        # transparency: the sustained figure is cuBLAS bf16 under the power cap (at its own, lower
+        # clock); also the burst figure and the dense peak at the clock sampled in this run
+        burst = peaks.get("bf16_tflops") or 1635.4
+        mhz = clocks.get("sm_mhz") or 0
+        per_clock = 148 * 8192 * mhz * 1e6 / 1e12 if mhz else None   # fp16 dense: 8192 flop/clk/SM
+        roof.update({"peak_burst": burst, "frac_burst": kern_tflops / burst,
+                     "peak_at_sampled_clock": per_clock,
+                     "frac_at_sampled_clock": (kern_tflops / per_clock) if per_clock else None})
     cb = None
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(cfg, 1, args.ref_M, args.ref_L)

@@ -43,7 +43,7 @@ struct DevBuf {
 
 // Split-M slot policy: S depends only on M, so per-row results are identical
 // for any GPU count in L-shard mode and any active-set size.
-constexpr int64_t kSlotTarget = 32768;  // samples per slot (target) ...
+constexpr int64_t kSlotTarget = 65536;  // samples per slot (target) ...
 constexpr int64_t kSlotMin = 128;       // ... but up to 30 slots of >= this many samples
 constexpr int kMinSlots = 30;
 constexpr int kMaxSlots = 128;
@@ -229,7 +229,8 @@ void plan_slots(oica_ctx* c) {
   // load, pipeline fill, G flush: ~13% of the step at 8192-sample slots and N = 128), while up
   // to 30 slots (of >= 128 samples) keep enough CTAs per row tile for small L and small M
   static int64_t target = [] { const char* e = getenv("OICA_SLOT_TARGET"); return e ? atoll(e) : kSlotTarget; }();
-  int64_t S = std::max<int64_t>(std::min<int64_t>(kMinSlots, c->Mg / kSlotMin), c->Mg / target);
+  static int64_t min_slots = [] { const char* e = getenv("OICA_MIN_SLOTS"); return e ? atoll(e) : (int64_t)kMinSlots; }();
+  int64_t S = std::max<int64_t>(std::min<int64_t>(min_slots, c->Mg / kSlotMin), c->Mg / target);
   S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, S));
   // slot length is a function of the GLOBAL M only (determinism across GPU counts)
   int64_t len = round_up(ceil_div(c->Mg, S), kSlotAlign);
