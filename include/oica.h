@@ -232,6 +232,11 @@ typedef struct {
  * G is d x N with orthonormal rows, b a unit d-vector; writes the (d-1) x N basis of the
  * complement of w = G^T b inside span(G) (rows 2..d of H G, H the reflection taking b to -+e1). */
 oica_status oica_complement_basis(const double* W, int32_t k, int32_t N, double* G);
+/* Host-only: the split-M slot plan of the step kernels (DESIGN.md §5 "HBM layout").  Slot length
+ * depends on M_global only (so every row's fp32-per-slot / fp64-across-slot arithmetic is the
+ * same for any GPU count, tiling or active-set size) and is a multiple of 384 samples; S_local
+ * = ceil(M_local / slot_len) slots cover this rank's samples. */
+oica_status oica_slot_plan(int64_t M_global, int64_t M_local, int64_t* slot_len, int32_t* S_local);
 oica_status oica_deflate_basis(double* G, int32_t d, int32_t N, const double* b, double* G_out);
 
 oica_status oica_merge_records(const oica_cluster_record* records, const double* w, int32_t n,

@@ -224,20 +224,21 @@ void jacobi_eigh(std::vector<double>& A, int n, std::vector<double>& d, std::vec
   for (int i = 0; i < n; ++i) d[i] = a(i, i);
 }
 
-void plan_slots(oica_ctx* c) {
+// Split-M slot plan: slot length is a function of the GLOBAL M only (determinism across GPU
+// counts, tilings and active-set sizes); the local slot count follows from the local M.
+void plan_slots_for(int64_t M_global, int64_t M_local, int64_t* slot_len, int* S_local) {
   // one CTA per (row tile, slot): long slots amortise each CTA's set-up (TMEM allocation, W
   // load, pipeline fill, G flush: ~13% of the step at 8192-sample slots and N = 128), while up
   // to 30 slots (of >= 128 samples) keep enough CTAs per row tile for small L and small M
   static int64_t target = [] { const char* e = getenv("OICA_SLOT_TARGET"); return e ? atoll(e) : kSlotTarget; }();
   static int64_t min_slots = [] { const char* e = getenv("OICA_MIN_SLOTS"); return e ? atoll(e) : (int64_t)kMinSlots; }();
-  int64_t S = std::max<int64_t>(std::min<int64_t>(min_slots, c->Mg / kSlotMin), c->Mg / target);
+  int64_t S = std::max<int64_t>(std::min<int64_t>(min_slots, M_global / kSlotMin), M_global / target);
   S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, S));
-  // slot length is a function of the GLOBAL M only (determinism across GPU counts)
-  int64_t len = round_up(ceil_div(c->Mg, S), kSlotAlign);
-  c->slot_len = len;
-  c->S = (int)ceil_div(c->M, len);
-  if (c->S < 1) c->S = 1;
+  *slot_len = round_up(ceil_div(M_global, S), kSlotAlign);
+  *S_local = std::max(1, (int)ceil_div(M_local, *slot_len));
 }
+
+void plan_slots(oica_ctx* c) { plan_slots_for(c->Mg, c->M, &c->slot_len, &c->S); }
 
 void ensure_candidate_buffers(oica_ctx* c) {
   size_t Ll = (size_t)c->Ll, N = (size_t)c->N, NP = (size_t)c->NP;
@@ -973,6 +974,14 @@ oica_status oica_reset_stats(oica_ctx* c) {
 oica_status oica_synchronize(oica_ctx* c) {
   if (!c) return OICA_ERR_INVALID_ARGUMENT;
   return guard(c, [&] { OICA_CUDA(cudaStreamSynchronize(c->st)); });
+}
+
+oica_status oica_slot_plan(int64_t M_global, int64_t M_local, int64_t* slot_len, int32_t* S_local) {
+  if (!slot_len || !S_local || M_global < 1 || M_local < 1 || M_local > M_global) return OICA_ERR_INVALID_ARGUMENT;
+  int s = 0;
+  plan_slots_for(M_global, M_local, slot_len, &s);
+  *S_local = s;
+  return OICA_OK;
 }
 
 oica_status oica_complement_basis(const double* W, int32_t k, int32_t N, double* G) {

@@ -91,6 +91,7 @@ SIGNATURES = {
     "oica_merge_records": (C.c_int, [_P(ClusterRecord), _P(C.c_double), C.c_int32, C.c_int32, _P(C.c_int32),
                                      _P(C.c_int64), _P(C.c_uint8)]),
     "oica_complement_basis": (C.c_int, [_P(C.c_double), C.c_int32, C.c_int32, _P(C.c_double)]),
+    "oica_slot_plan": (C.c_int, [C.c_int64, C.c_int64, _P(C.c_int64), _P(C.c_int32)]),
     "oica_deflate_basis": (C.c_int, [_P(C.c_double), C.c_int32, C.c_int32, _P(C.c_double), _P(C.c_double)]),
 }
 
@@ -171,6 +172,13 @@ def complement_basis(W, N):
     G = np.zeros((N - k, N))
     _check(lib().oica_complement_basis(_np_ptr(W, C.c_double) if k else None, k, N, _np_ptr(G, C.c_double)))
     return G
+
+
+def slot_plan(M_global, M_local=None):
+    """Host-only (oica_slot_plan): (slot_len, S_local) of the step kernels' split-M slots."""
+    ln, S = C.c_int64(), C.c_int32()
+    _check(lib().oica_slot_plan(M_global, M_global if M_local is None else M_local, C.byref(ln), C.byref(S)))
+    return ln.value, S.value
 
 
 def deflate_basis(G, b):

@@ -106,3 +106,16 @@ def test_deflate_basis_host(N, d):
     assert np.abs(G2 - (G2 @ G.T) @ G).max() < 1e-12
     # G2^T G2 = G^T G - w w^T
     assert np.abs(G2.T @ G2 - (G.T @ G - np.outer(w, w))).max() < 1e-12
+
+
+@pytest.mark.parametrize("M", [1, 2000, 5003, 20000, 150001, 250000, 1_000_000, 4_000_000, 40_000_000])
+def test_slot_plan_host(M):
+    """Slots (the fixed fp32-accumulation units of every row): a function of the global M only,
+    384-aligned (a multiple of every kernel chunk width), covering M; an M-sharded rank's slots
+    have the same length and cover its samples."""
+    ln, S = oica.slot_plan(M)
+    assert ln % 384 == 0 and 1 <= S <= 128 and (S - 1) * ln < M <= S * ln
+    for world in (2, 8):
+        ml = -(-M // world)
+        ln2, S2 = oica.slot_plan(M, min(ml, M))
+        assert ln2 == ln and (S2 - 1) * ln2 < min(ml, M) <= S2 * ln2
