@@ -212,7 +212,8 @@ template <int NP, bool SPLIT, int EPI, int CL, int RG>
 __global__ void __launch_bounds__(192, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
           const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_ub, int64_t M, int64_t slot_len,
-          float* __restrict__ Gp, int64_t cap, int n_tiles, int tile_lo0_h, int order, int S_, const int* __restrict__ cnt) {
+          float* __restrict__ Gp, int64_t cap, int n_tiles, int tile_lo0_h, int order, int S_, const int* __restrict__ cnt,
+          int s_base) {
   constexpr int NW = 4;   // epilogue warps
   using C = Cfg<NP, SPLIT, RG>;
   constexpr int MT = C::MT;
@@ -235,7 +236,9 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   uint32_t* tmem_slot = (uint32_t*)(gdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = order ? blockIdx.x / S_ : blockIdx.x % n_tiles, s = order ? blockIdx.x % S_ : blockIdx.x / n_tiles;
+  // slots [s_base, s_base + gridDim.x / n_tiles) (a launch may cover a slot range: pipelined upload)
+  const int tile = order ? blockIdx.x / S_ : blockIdx.x % n_tiles,
+            s = s_base + (order ? blockIdx.x % S_ : blockIdx.x / n_tiles);
   // active-row count and coarse/fine split: from the device counters when the grid was sized
   // from an upper bound (iterations enqueued without a host round trip)
   const int L_act = cnt ? min(L_ub, cnt[0]) : L_ub;
@@ -291,8 +294,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       for (int j = 0; j < nchunk; ++j) {
         int st = j % C::STAGES;
         if (j >= C::STAGES) mbar_wait(&empty[st], ((j / C::STAGES) - 1) & 1);
-        mbar_expect_tx(&full[st], C::X_STAGE);
         int m0 = (int)(m_begin + (int64_t)j * MT);
+        mbar_expect_tx(&full[st], C::X_STAGE);
         uint8_t* dst = s_x + st * C::X_STAGE;
         for (int h = 0; h < MT / 64; ++h) {
           if (CL == 1)
@@ -534,7 +537,8 @@ CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld,
 
 template <int NP, bool SPLIT, int EPI, int CL, int RG>
 void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt) {
+               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt,
+               const Upload& up) {
   using C = Cfg<NP, SPLIT, RG>;
   auto kern = k_step_tc<NP, SPLIT, EPI, CL, RG>;
   static bool attr = false;
@@ -549,7 +553,6 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   int n_tiles = (int)round_up(ceil_div(L_act, 128), CL);   // a cluster = CL tiles of one slot
   static int order = [] { const char* e = getenv("OICA_TC_ORDER"); return e ? atoi(e) : 0; }();
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)(n_tiles * S));
   lc.blockDim = dim3(192);
   lc.dynamicSmemBytes = C::SMEM;
   lc.stream = st;
@@ -560,13 +563,15 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
+  lc.gridDim = dim3((unsigned)(n_tiles * up.s_count));
   OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_tiles, tile_lo0,
-                               CL > 1 ? 0 : order, S, cnt));
+                               CL > 1 ? 0 : order, up.s_count, cnt, up.s_base));
 }
 
 template <int NP, bool SPLIT, int EPI>
 void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt) {
+                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt,
+                    const Upload& up) {
   // Cluster multicast of the X chunks: on by default for NP > 64, where the X
   // stream through L2 (~6 TB/s) otherwise paces or co-limits the kernel (cfg-4 shape +20%, cfg-3
   // shape +6%; neutral at NP = 64, which is latency-bound); OICA_TC_CL=1|2 overrides.
@@ -579,64 +584,65 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
   constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
   if (NP <= 64 && r192 && cl == 1) {   // small NP: 2 Y slots of 192 samples (OICA_TC_RING=2: 2 x 128)
     launch_cl<NP, SPLIT, EPI, 1, (NP <= 64 ? 3 : 1)>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0,
-                                                    cnt);
+                                                    cnt, up);
     return;
   }
   const bool r1 = NP <= 128 && rg == 1;
   if (cl == 2 && r1)
-    launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
+    launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt, up);
   else if (cl == 2)
-    launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
+    launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt, up);
   else if (r1)
-    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
+    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt, up);
   else
-    launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt);
+    launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt, up);
 }
 
 template <int NP, bool SPLIT>
 void launch_epi(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt) {
+                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up) {
   static int epi = [] { const char* e = getenv("OICA_TC_EPI"); return e ? atoi(e) : 0; }();
   switch (epi) {
-    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
   }
 }
 
 template <bool SPLIT>
 void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi, const __half* Wlo,
-               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt) {
+               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up) {
   switch (NP) {
-    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 64: launch_epi<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 144: launch_variant<144, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 160: launch_variant<160, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 176: launch_variant<176, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 192: launch_variant<192, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 208: launch_variant<208, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 224: launch_variant<224, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 240: launch_variant<240, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
-    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt); break;
+    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 64: launch_epi<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 144: launch_variant<144, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 160: launch_variant<160, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 176: launch_variant<176, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 192: launch_variant<192, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 208: launch_variant<208, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 224: launch_variant<224, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 240: launch_variant<240, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
   }
 }
 
-// fp16 plane row n = fp16(x_n 2^-6), zero padded to NP rows and ldx columns.  One thread per 8
-// consecutive samples of a row (blockIdx.y = row): coalesced fp32 reads, one 16-byte store.
+// fp16 plane row n = fp16(x_n 2^-6), zero padded to NP rows and ldx columns, for the columns
+// [m_lo, m_hi) (multiples of 8).  One thread per 8 consecutive samples of a row (blockIdx.y =
+// row): coalesced fp32 reads, one 16-byte store.
 __global__ void k_x_prepare_f16(const float* __restrict__ X, int64_t ld, int N, int64_t M, int64_t ldx,
-                                __half* __restrict__ Xh) {
+                                __half* __restrict__ Xh, int64_t m_lo, int64_t m_hi) {
   const int n = blockIdx.y;
-  const int64_t m0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (m0 >= ldx) return;
+  const int64_t m0 = m_lo + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (m0 >= m_hi) return;
   const float* x = X + (int64_t)n * ld;
   __align__(16) __half2 h[4];
 #pragma unroll
@@ -649,6 +655,7 @@ __global__ void k_x_prepare_f16(const float* __restrict__ X, int64_t ld, int N, 
   *reinterpret_cast<uint4*>(Xh + (int64_t)n * ldx + m0) = *reinterpret_cast<uint4*>(h);
 }
 
+
 }  // namespace
 
 bool tc_supported(int N) { return N >= 1 && N <= 256; }
@@ -656,22 +663,25 @@ int tc_np(int N) { return (int)round_up(N < 16 ? 16 : N, 16); }
 
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
                    const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
-                   const int* cnt, bool lo_capable) {
+                   const int* cnt, bool lo_capable, const Upload& up) {
   if (L_act <= 0) return 0;
   static bool force_lo = getenv("OICA_TC_FORCE_LO") != nullptr;   // experiment: LO-capable layout always
   lo_capable = lo_capable || force_lo;
   if (lo_capable || n_coarse < L_act)   // fine rows (possibly): LO-capable layout, 2nd pass from tile n_coarse/128
-    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse / 128, cnt);
+    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse / 128, cnt, up);
   else
-    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0, cnt);
+    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0, cnt, up);
   return 1;
 }
 
 int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP, int64_t ldx,
-                         __half* Xh) {
-  dim3 grid((unsigned)ceil_div(ldx / 8, 256), (unsigned)NP);   // ldx is a multiple of 128
-  k_x_prepare_f16<<<grid, 256, 0, st>>>(X, ld, N, M, ldx, Xh);
+                         __half* Xh, int64_t m_lo, int64_t m_hi) {
+  if (m_hi < 0) m_hi = ldx;
+  if (m_hi <= m_lo) return 0;
+  dim3 grid((unsigned)ceil_div((m_hi - m_lo) / 8, 256), (unsigned)NP);   // ldx, m_lo, m_hi multiples of 8
+  k_x_prepare_f16<<<grid, 256, 0, st>>>(X, ld, N, M, ldx, Xh, m_lo, m_hi);
   return 1;
 }
+
 
 }  // namespace oica

@@ -118,11 +118,20 @@ int tc_np(int N);
 // L_act / n_coarse size the grid; when cnt (device [L_act, n_coarse]) is given they are upper
 // bounds and the kernel takes the true values from cnt (tiles beyond exit at once).
 // lo_capable: launch the LO-capable layout even if n_coarse == L_act (fine rows may appear).
+// Slot range of one step launch: [s_base, s_base + s_count).  The whole step is one launch over
+// all S slots; while a pipelined host upload is in flight the first step is launched piece by
+// piece (each launch after its piece's copy event), which gives bitwise the same slot partials.
+struct Upload {
+  int s_base;
+  int s_count;
+};
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
                    const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
-                   const int* cnt, bool lo_capable);
+                   const int* cnt, bool lo_capable, const Upload& up);
+// fp16 plane columns [m_lo, m_hi) (m_hi < 0: ldx); multiples of 8.
 int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP,
-                         int64_t ldx, __half* Xh);
+                         int64_t ldx, __half* Xh, int64_t m_lo = 0, int64_t m_hi = -1);
+
 
 // ---- §3.3 reduction of X (k_reduce.cu)
 // X~ = G X (Gf: d x N fp32 rows) into Xr (d x M, stride ldr) and, if Xh != null, the fp16 plane

@@ -69,6 +69,14 @@ struct oica_ctx {
   // data
   const float* X = nullptr;
   DevBuf<float> Xown;
+  // pipelined host upload (oica_set_data_host): copy + fp16 conversion on a second stream, piece
+  // by piece; the tensor-core step of the first iteration waits per piece (DESIGN.md §7 e2e)
+  cudaStream_t cst = nullptr;
+  cudaEvent_t x_ready_ev = nullptr, st_ev = nullptr;
+  std::vector<cudaEvent_t> piece_ev;   // piece p of the upload is on the device (and converted)
+  int pieces = 0;
+  bool x_pending = false;
+  int64_t piece_len = 0;
   int64_t N = 0, NP = 0, M = 0, ld = 0, Mg = 0;
   int precision = OICA_PREC_FP32;
   DevBuf<__half> Xh;   // TC operand plane
@@ -283,6 +291,15 @@ void ensure_candidate_buffers(oica_ctx* c) {
   c->Wacc.ensure(N * N);
 }
 
+// Every consumer of the data other than the first tensor-core step orders itself after a
+// pending pipelined upload.
+void sync_x(oica_ctx* c) {
+  if (!c->x_pending) return;
+  OICA_CUDA(cudaStreamWaitEvent(c->st, c->x_ready_ev, 0));
+  c->x_pending = false;
+}
+
+
 // Build the step-kernel operand rows for the active list `act` (count in Lact_dev, <= cap).
 void build_operand(oica_ctx* c, const int* act, int cap) {
   if (c->tc())
@@ -302,12 +319,28 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, bool lo_capa
     OICA_CUDA(cudaEventRecord(e0, c->st));
   }
   int n;
-  if (c->tc())
+  if (c->tc() && c->x_pending && !c->reduced) {
+    // pipelined host upload in flight: one launch per piece of whole slots, each after its
+    // piece's copy + conversion (same slot partials as one launch over all slots)
+    const int spp = (int)(c->piece_len / c->slot_len);
+    n = 0;
+    for (int p = 0; p < c->pieces; ++p) {
+      OICA_CUDA(cudaStreamWaitEvent(c->st, c->piece_ev[p], 0));
+      const int s0 = p * spp, s1 = std::min(c->S, s0 + spp);
+      if (s1 > s0)
+        n += launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
+                            c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{s0, s1 - s0});
+    }
+    sync_x(c);
+  } else if (c->tc()) {
+    sync_x(c);
     n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
-                       c->S, c->Gp32.p, c->Ll, cnt, lo_capable);
-  else
+                       c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, c->S});
+  } else {
+    sync_x(c);
     n = launch_step_simt(c->st, c->vX, c->vld, c->M, c->vN, c->vNP, c->W32.p, L_act, c->slot_len, c->S, kFlush,
                          c->Gp.p, c->s4p.p, c->Ll, cnt);
+  }
   OICA_CUDA(cudaGetLastError());
   c->count(n);
   c->stats.step_launches += n;
@@ -435,6 +468,7 @@ void use_full_view(oica_ctx* c) {
 // fp16 tensor-core plane.
 void use_reduced_view(oica_ctx* c, int d) {
   const int N = (int)c->N;
+  sync_x(c);
   c->Gdev.ensure((size_t)d * N);
   c->Gf.ensure((size_t)d * N);
   std::vector<float> gf(c->Gh.begin(), c->Gh.begin() + (size_t)d * N);
@@ -677,8 +711,10 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
   use_full_view(c);
 }
 
-void set_data_impl(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int64_t ld, int64_t M_global) {
+void set_data_impl(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int64_t ld, int64_t M_global,
+                   bool prepare = true) {
   OICA_REQUIRE(Xw, OICA_ERR_INVALID_ARGUMENT, "Xw is NULL");
+  sync_x(c);   // a pending upload still writes the planes
   OICA_REQUIRE(N >= 1 && N <= 256, OICA_ERR_INVALID_ARGUMENT, "need 1 <= N <= 256");
   OICA_REQUIRE(M_local >= 1 && ld >= M_local, OICA_ERR_INVALID_ARGUMENT, "need M_local >= 1 and ld >= M_local");
   OICA_REQUIRE(M_global > N, OICA_ERR_INVALID_ARGUMENT, "need M_global > N");
@@ -704,8 +740,10 @@ void set_data_impl(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int
   if (tc) {
     c->ldx = round_up(M_local, 128);
     c->Xh.ensure((size_t)c->NP * c->ldx);
-    c->count(launch_x_prepare_f16(c->st, Xw, ld, (int)N, M_local, (int)c->NP, c->ldx, c->Xh.p));
-    check_launch();
+    if (prepare) {
+      c->count(launch_x_prepare_f16(c->st, Xw, ld, (int)N, M_local, (int)c->NP, c->ldx, c->Xh.p));
+      check_launch();
+    }
   }
   use_full_view(c);
   if (c->have_cand) ensure_candidate_buffers(c);
@@ -789,6 +827,13 @@ oica_status oica_destroy(oica_ctx* c) {
   if (c->comm) Nccl::get().CommDestroy(c->comm);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->Lact_host) cudaFreeHost(c->Lact_host);
+  if (c->cst) {
+    cudaStreamSynchronize(c->cst);
+    cudaStreamDestroy(c->cst);
+  }
+  if (c->x_ready_ev) cudaEventDestroy(c->x_ready_ev);
+  for (auto e : c->piece_ev) cudaEventDestroy(e);
+  if (c->st_ev) cudaEventDestroy(c->st_ev);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
   return OICA_OK;
@@ -857,9 +902,40 @@ oica_status oica_set_data_host(oica_ctx* c, const float* Xh, int64_t N, int64_t 
   return guard(c, [&] {
     OICA_REQUIRE(Xh && N >= 1 && M_local >= 1 && ld >= M_local, OICA_ERR_INVALID_ARGUMENT, "bad host data");
     c->Xown.ensure((size_t)N * M_local);
-    OICA_CUDA(cudaMemcpy2DAsync(c->Xown.p, sizeof(float) * M_local, Xh, sizeof(float) * ld, sizeof(float) * M_local,
-                                (size_t)N, cudaMemcpyHostToDevice, c->st));
-    set_data_impl(c, c->Xown.p, N, M_local, M_local, M_global);
+    set_data_impl(c, c->Xown.p, N, M_local, M_local, M_global, /*prepare=*/false);
+    if (!c->cst) {
+      OICA_CUDA(cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking));
+      OICA_CUDA(cudaEventCreateWithFlags(&c->x_ready_ev, cudaEventDisableTiming));
+      OICA_CUDA(cudaEventCreateWithFlags(&c->st_ev, cudaEventDisableTiming));
+    }
+    // the upload may overwrite X and its plane only after all work already queued on the
+    // context stream (which may still read them)
+    OICA_CUDA(cudaEventRecord(c->st_ev, c->st));
+    OICA_CUDA(cudaStreamWaitEvent(c->cst, c->st_ev, 0));
+    // pieces of whole slots (~16 per upload) so the first step can start on the first piece
+    const int64_t M = M_local;
+    // (and >= ~2 waves of CTAs per piece launch at the first iteration's row count)
+    int64_t spp = std::max<int64_t>(1, c->S / 16);
+    if (c->have_cand) spp = std::max<int64_t>(spp, ceil_div(2 * c->num_sms, ceil_div(c->Ll, 128)));
+    c->piece_len = c->tc() ? c->slot_len * std::min<int64_t>(spp, c->S) : M;
+    c->pieces = (int)ceil_div(M, c->piece_len);
+    while ((int)c->piece_ev.size() < c->pieces) {
+      cudaEvent_t e;
+      OICA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->piece_ev.push_back(e);
+    }
+    for (int p = 0; p < c->pieces; ++p) {
+      const int64_t m0 = p * c->piece_len, m1 = std::min(M, m0 + c->piece_len);
+      OICA_CUDA(cudaMemcpy2DAsync(c->Xown.p + m0, sizeof(float) * M, Xh + m0, sizeof(float) * ld, sizeof(float) * (m1 - m0),
+                                  (size_t)N, cudaMemcpyHostToDevice, c->cst));
+      if (c->tc())
+        c->count(launch_x_prepare_f16(c->cst, c->Xown.p, M, (int)N, M, (int)c->NP, c->ldx, c->Xh.p, m0,
+                                      p == c->pieces - 1 ? c->ldx : m1));
+      OICA_CUDA(cudaEventRecord(c->piece_ev[p], c->cst));
+    }
+    check_launch();
+    OICA_CUDA(cudaEventRecord(c->x_ready_ev, c->cst));
+    c->x_pending = true;
   });
 }
 

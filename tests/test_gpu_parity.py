@@ -382,3 +382,27 @@ def test_shape_edge_cases(N, M, L, N_out, precision):
     for out in (res, red):
         assert out.n_extracted == N_out
         _compare(out, res_or, W_or, X64)
+
+
+# ---- the end-to-end entry point: host data uploaded piece by piece on a second stream while the
+# first tensor-core step consumes it (pipelined oica_set_data_host) gives bitwise the result of
+# device-resident data, also when uploads follow each other and in the reduced form
+@pytest.mark.parametrize("name,precision", [("p_tc_n256", oica.PREC_AUTO), ("p_tc_n128", oica.PREC_AUTO),
+                                            ("p_n40", oica.PREC_FP32)])
+def test_host_upload_bitwise(name, precision):
+    cfg, X32, _ = prepared(name)
+    with oica.Context(0, precision) as ctx:
+        ctx.set_data(torch.from_numpy(X32).cuda())
+        ctx.init_candidates(cfg.cand_seed, cfg.L)
+        dev = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
+        dev_red = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=oica.REDUCE_X)
+        pinned = torch.from_numpy(X32).pin_memory()
+        outs = []
+        for rep in range(2):   # back-to-back uploads (epochs) and extractions
+            ctx.set_data_host_ptr(pinned.data_ptr(), cfg.N, cfg.M, cfg.M)
+            outs.append(ctx.extract(cfg.N_out, cfg.K, cfg.tol))
+        ctx.set_data_host(X32)
+        red = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=oica.REDUCE_X)
+    for o in outs:
+        assert np.array_equal(o.W, dev.W) and np.array_equal(o.index, dev.index) and np.array_equal(o.alpha, dev.alpha)
+    assert np.array_equal(red.W, dev_red.W) and np.array_equal(red.index, dev_red.index)
