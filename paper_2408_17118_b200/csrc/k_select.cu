@@ -122,6 +122,27 @@ __global__ void k_assign(const double* __restrict__ W64, const double* __restric
   }
 }
 
+// acc[c] += sum over this thread's samples of (w_c . x_m)^4 for the first CC rows, y in fp64.
+template <int CC>
+__device__ __forceinline__ void alpha_accumulate(const double (*ws)[256], const float* __restrict__ X, int64_t ld,
+                                                 int N, int64_t mb, int64_t me, double (&acc)[kMaxClusters]) {
+  for (int64_t m = mb + threadIdx.x; m < me; m += blockDim.x) {
+    double y[CC];
+#pragma unroll
+    for (int c = 0; c < CC; ++c) y[c] = 0.0;
+    for (int n = 0; n < N; ++n) {
+      double x = (double)__ldg(X + (int64_t)n * ld + m);
+#pragma unroll
+      for (int c = 0; c < CC; ++c) y[c] = fma(ws[c][n], x, y[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < CC; ++c) {
+      double y2 = y[c] * y[c];
+      acc[c] = fma(y2, y2, acc[c]);
+    }
+  }
+}
+
 // part[c][b] = sum over block b's samples of (w_c . x_m)^4, y in fp64 (fixed order).
 __global__ void __launch_bounds__(256) k_alpha_exact(const double* __restrict__ W64, const float* __restrict__ X,
                                                      int64_t ld, int64_t M, int N, const int* __restrict__ pc,
@@ -153,22 +174,15 @@ __global__ void __launch_bounds__(256) k_alpha_exact(const double* __restrict__ 
   double acc[kMaxClusters];
 #pragma unroll
   for (int c = 0; c < kMaxClusters; ++c) acc[c] = 0.0;
-  for (int64_t m = mb + threadIdx.x; m < me; m += blockDim.x) {
-    double y[kMaxClusters];
-#pragma unroll
-    for (int c = 0; c < kMaxClusters; ++c) y[c] = 0.0;
-    for (int n = 0; n < N; ++n) {
-      double x = (double)__ldg(X + (int64_t)n * ld + m);
-#pragma unroll
-      for (int c = 0; c < kMaxClusters; ++c)
-        if (c < C) y[c] = fma(ws[c][n], x, y[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < kMaxClusters; ++c) {
-      double y2 = y[c] * y[c];
-      acc[c] = fma(y2, y2, acc[c]);
-    }
-  }
+  // usually one or two clusters are refined: the row count is a block-uniform template choice
+  if (C <= 1)
+    alpha_accumulate<1>(ws, X, ld, N, mb, me, acc);
+  else if (C <= 2)
+    alpha_accumulate<2>(ws, X, ld, N, mb, me, acc);
+  else if (C <= 4)
+    alpha_accumulate<4>(ws, X, ld, N, mb, me, acc);
+  else
+    alpha_accumulate<kMaxClusters>(ws, X, ld, N, mb, me, acc);
   int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int c = 0; c < kMaxClusters; ++c) {
