@@ -103,6 +103,16 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// (a0^3, a1^3) with packed fp32x2 multiplies (FMUL2): (a*a)*a per lane, exactly as two scalar
+// FMULs would round it
+__device__ __forceinline__ float2 cube2(uint32_t a0, uint32_t a1) {
+  const unsigned long long av = ((unsigned long long)a1 << 32) | a0;
+  unsigned long long sq, cu;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(sq) : "l"(av), "l"(av));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(cu) : "l"(sq), "l"(av));
+  return make_float2(__uint_as_float((uint32_t)cu), __uint_as_float((uint32_t)(cu >> 32)));
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -448,8 +458,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
             uint32_t pl[16];
 #pragma unroll
             for (int k = 0; k < 32; k += 2) {
-              float a0 = __uint_as_float(v[w][k]), a1 = __uint_as_float(v[w][k + 1]);
-              float c0 = a0 * a0 * a0, c1 = a1 * a1 * a1;
+              const float2 cc = cube2(v[w][k], v[w][k + 1]);
+              const float c0 = cc.x, c1 = cc.y;
               __half2 hh = __floats2half2_rn(c0, c1);
               pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
               float2 hf = __half22float2(hh);
@@ -461,8 +471,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
             for (int k = 0; k < 32; k += 2) {
               // accumulator = 2^4 y 2^-6 = y / 4 (W scaled by 2^4, X by 2^-6)  ->  acc^3 = 2^-6 y^3
-              float a0 = __uint_as_float(v[w][k]), a1 = __uint_as_float(v[w][k + 1]);
-              __half2 hh = __floats2half2_rn(a0 * a0 * a0, a1 * a1 * a1);
+              const float2 cc = cube2(v[w][k], v[w][k + 1]);
+              __half2 hh = __floats2half2_rn(cc.x, cc.y);
               pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
             }
           }
