@@ -68,7 +68,13 @@ typedef enum {
 /* Multi-GPU partitioning.  world == 1 ignores it. */
 typedef enum {
   OICA_SHARD_L = 0,     /* candidates split over ranks, X replicated, one exchange/component */
-  OICA_SHARD_M = 1      /* samples split over ranks, fp64 allreduce of G, s4 per iteration   */
+  OICA_SHARD_M = 1,     /* samples split over ranks, fp64 allreduce of G, s4 per iteration   */
+  OICA_SHARD_HYBRID = 2 /* L-shard until the global active count falls to OICA_HYBRID_ROWS     */
+                        /* (env; default 128 x world): the remaining runs are all-gathered,    */
+                        /* iterated M-sharded over the replicated X (fp64 allreduce per         */
+                        /* iteration) and handed back to their owners.   */
+                        /* Equal to L-shard within tolerance (the tail sums ranks in NCCL       */
+                        /* order), not bitwise.                                                 */
 } oica_shard_mode;
 
 typedef struct {
@@ -127,6 +133,7 @@ typedef struct {
   double step_issued_flops;  /* flops the step launches issued to the tensor pipe / FMA units,*/
                              /* padding and second passes included (row tiles x NP)         */
   int64_t fine_rows;         /* sum over step launches of rows run with the two-pass GEMM1   */
+  int64_t tail_iterations;   /* iterations run in the hybrid tail (OICA_SHARD_HYBRID)        */
 } oica_stats;
 
 /* ---- lifetime ---------------------------------------------------------------------- */
@@ -192,6 +199,12 @@ oica_status oica_extract_components(oica_ctx* ctx, int32_t N_out, int32_t max_it
  * and slot order.  (Uses the context's workspace; L <= the L of init_candidates.) */
 oica_status oica_fixed_point_step(oica_ctx* ctx, const double* W_dev, int64_t L,
                                   double* G_dev, double* s4_dev);
+/* The same contraction with a per-row precision (tensor-core contexts): fine_host
+ * (host, L bytes) marks the rows evaluated in two-pass "fine" precision; they must follow every
+ * coarse row (the order the runtime's compaction keeps), else INVALID_ARGUMENT.  A row's result
+ * does not depend on the rows it shares a 128-row tile with.  FP32 contexts ignore fine_host. */
+oica_status oica_fixed_point_step_mixed(oica_ctx* ctx, const double* W_dev, int64_t L, const uint8_t* fine_host,
+                                        double* G_dev, double* s4_dev);
 /* The candidate generator + projection + normalisation
  * for component i (1-based) against host W_acc (k x N, may be NULL if k == 0):
  * writes this rank's L_local x N fp64 rows to W_dev (device).  Degenerate rows are zero. */

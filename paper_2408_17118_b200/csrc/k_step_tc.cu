@@ -12,8 +12,9 @@
 // as TF32).  The operand row is w_h = fp16(2^4 w) (one GEMM1 pass) or, for "fine" rows, w_h + w_l
 // with w_l = fp16(2^4 w - w_h) (two passes, w to ~2^-22); fine tiles also run GEMM2 twice, on
 // y^3 2^-6 rounded to fp16 and on its fp16 residual (y^3 to ~2^-22).  Fine rows are grouped at the end of
-// the active list; tiles >= tile_lo0 run the second pass (coarse rows in such a tile carry
-// w_l = 0, which adds exact zeros).  K3 evaluates the -3w term of eq. (5) at the SAME operand
+// the active list; tiles >= n_coarse/128 run the second passes (a coarse row in such a tile carries
+// w_l = 0 and a zero y^3 residual, which add exact zeros: a row's result never depends on the
+// rows it shares a tile with, so L-shard results are identical for any GPU count).  K3 evaluates the -3w term of eq. (5) at the SAME operand
 // (consistent evaluation of the fixed-point map at the rounded point, whose tangent Jacobian
 // vanishes at a fixed point).  y^3 2^-6 is rounded to fp16 for GEMM2 (1 pass).  Accumulation
 // fp32 in TMEM per slot (stored as exact fp32 x 2^12), fp64 across slots (K3).  Issued tensor
@@ -222,7 +223,7 @@ template <int NP, bool SPLIT, int EPI, int CL, int RG>
 __global__ void __launch_bounds__(192, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
           const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_ub, int64_t M, int64_t slot_len,
-          float* __restrict__ Gp, int64_t cap, int n_tiles, int tile_lo0_h, int order, int S_, const int* __restrict__ cnt,
+          float* __restrict__ Gp, int64_t cap, int n_tiles, int n_coarse_h, int order, int S_, const int* __restrict__ cnt,
           int s_base) {
   constexpr int NW = 4;   // epilogue warps
   using C = Cfg<NP, SPLIT, RG>;
@@ -252,7 +253,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   // active-row count and coarse/fine split: from the device counters when the grid was sized
   // from an upper bound (iterations enqueued without a host round trip)
   const int L_act = cnt ? min(L_ub, cnt[0]) : L_ub;
-  const int tile_lo0 = cnt ? cnt[1] / 128 : tile_lo0_h;
+  const int n_coarse = cnt ? cnt[1] : n_coarse_h;
+  const int tile_lo0 = n_coarse / 128;
   if ((tile - tile % CL) * 128 >= L_act) return;   // cluster-uniform: no barrier was touched
   const int row0 = tile * 128;
   const int64_t m_begin = (int64_t)s * slot_len;
@@ -407,6 +409,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     const int q = warp & 3, h = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     const int row = row0 + r;
+    const bool coarse_row = row < n_coarse;   // (fine tiles only: rows before the coarse/fine boundary)
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     // W operand rows -> TMEM (A operand of GEMM1, fp16 pairs per 32-bit column)
     {
@@ -455,7 +458,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           const int u = g0 + w;
           uint32_t pk[16];
           if (SPLIT && lo_pass) {   // fine tile: also the fp16 residual y^3 2^-6 - hi (GEMM2 second pass)
-            uint32_t pl[16];
+            uint32_t pl[16];   // (zero for a coarse row sharing the tile: its result must not depend on its tile)
 #pragma unroll
             for (int k = 0; k < 32; k += 2) {
               const float2 cc = cube2(v[w][k], v[w][k + 1]);
@@ -464,7 +467,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
               pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
               float2 hf = __half22float2(hh);
               __half2 hl = __floats2half2_rn(c0 - hf.x, c1 - hf.y);
-              pl[k / 2] = *reinterpret_cast<uint32_t*>(&hl);
+              pl[k / 2] = coarse_row ? 0u : *reinterpret_cast<uint32_t*>(&hl);
             }
             tmem_st16(t_y + 32 * (h + NH * u) + 16, pl);
           } else {
@@ -547,7 +550,7 @@ CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld,
 
 template <int NP, bool SPLIT, int EPI, int CL, int RG>
 void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt,
+               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
                const Upload& up) {
   using C = Cfg<NP, SPLIT, RG>;
   auto kern = k_step_tc<NP, SPLIT, EPI, CL, RG>;
@@ -574,13 +577,13 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   lc.attrs = at;
   lc.numAttrs = 1;
   lc.gridDim = dim3((unsigned)(n_tiles * up.s_count));
-  OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_tiles, tile_lo0,
+  OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_tiles, n_coarse,
                                CL > 1 ? 0 : order, up.s_count, cnt, up.s_base));
 }
 
 template <int NP, bool SPLIT, int EPI>
 void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int tile_lo0, const int* cnt,
+                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
                     const Upload& up) {
   // Cluster multicast of the X chunks: on by default for NP > 64, where the X
   // stream through L2 (~6 TB/s) otherwise paces or co-limits the kernel (cfg-4 shape +20%, cfg-3
@@ -593,19 +596,19 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
   static bool r192 = [] { const char* e = getenv("OICA_TC_RING"); return !(e && atoi(e) == 2); }();
   constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
   if (NP <= 64 && r192 && cl == 1) {   // small NP: 2 Y slots of 192 samples (OICA_TC_RING=2: 2 x 128)
-    launch_cl<NP, SPLIT, EPI, 1, (NP <= 64 ? 3 : 1)>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0,
+    launch_cl<NP, SPLIT, EPI, 1, (NP <= 64 ? 3 : 1)>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse,
                                                     cnt, up);
     return;
   }
   const bool r1 = NP <= 128 && rg == 1;
   if (cl == 2 && r1)
-    launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt, up);
+    launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
   else if (cl == 2)
-    launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt, up);
+    launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
   else if (r1)
-    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt, up);
+    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
   else
-    launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, tile_lo0, cnt, up);
+    launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
 }
 
 template <int NP, bool SPLIT>
@@ -678,7 +681,7 @@ int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, in
   static bool force_lo = getenv("OICA_TC_FORCE_LO") != nullptr;   // experiment: LO-capable layout always
   lo_capable = lo_capable || force_lo;
   if (lo_capable || n_coarse < L_act)   // fine rows (possibly): LO-capable layout, 2nd pass from tile n_coarse/128
-    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse / 128, cnt, up);
+    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
   else
     launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0, cnt, up);
   return 1;

@@ -76,6 +76,18 @@ int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int 
 int launch_s4_from_g(cudaStream_t st, EvalPoint ev, const double* W, const double* G, int ldg, int L, int N,
                      double* s4);
 
+// ---- C4: hybrid L -> M tail: pack this rank's active rows as records
+// [w (d) | alpha_old | dprev | fine | global id] (dprev, fine may be null), unpack the gathered
+// records into the tail's arrays, scatter finished tail rows back to their owner by global id.
+int launch_tail_pack(cudaStream_t st, const int* act, const int* cnt, int L_ub, const double* W64,
+                     const double* alpha_old, const double* dprev, const uint8_t* fine, int64_t id_base, int d,
+                     double* out);
+int launch_tail_unpack(cudaStream_t st, const double* in, int T, int d, double* W64, double* alpha_old,
+                       double* dprev, uint8_t* fine, uint8_t* state, uint8_t* keep, int64_t* ids);
+int launch_tail_scatter(cudaStream_t st, int T, const int64_t* ids, const double* tW64, const double* t_alpha,
+                        const int* t_iters, const uint8_t* t_state, int64_t id_base, int64_t L_local, int d,
+                        double* W64, double* alpha_old, int* iters, uint8_t* state);
+
 // ---- K5: device-side argmax, cluster assignment, exact alpha, merge + accept
 struct SelectWork;  // defined in k_select.cu
 struct ComponentRecord {

@@ -55,6 +55,8 @@ constexpr double kPromoteRatio = 0.3;       // ... (d > this * d_prev: stagnatin
 constexpr int kPromoteT = 40;               // ... or t >= this
 constexpr int kBatchRows = 2048;            // below this many active rows, iterations are enqueued ...
 constexpr int kBatch = 8;                   // ... this many at a time without a host round trip
+constexpr int kHybridRowsPerRank = 128;     // OICA_SHARD_HYBRID: tail once global L_act <= this x world
+constexpr int kTailMaxSlots = 1024;
 
 }  // namespace
 
@@ -121,6 +123,16 @@ struct oica_ctx {
   bool last_valid = false;
   // whitening scratch
   DevBuf<double> wh_mean, wh_part, wh_C, wh_V;
+  // hybrid L -> M tail (OICA_SHARD_HYBRID): the gathered runs, identical on all ranks
+  struct Tail {
+    DevBuf<double> pack, pack_all, dense, W64, alpha, dprev, Gsum, s4sum, Gp, s4p;
+    DevBuf<float> Gp32, W32;
+    DevBuf<__half> Whi, Wlo;
+    DevBuf<int64_t> ids;
+    DevBuf<int> iters, act0, act1, hist, cnt_all;
+    DevBuf<uint8_t> state, keep, fine;
+  } tail;
+
   // stats
   oica_stats stats{};
   std::vector<cudaEvent_t> ev;
@@ -143,6 +155,7 @@ struct oica_ctx {
   // a communicator exists for world > 1, or at world == 1 when a unique id is passed (the
   // exchange / allreduce code paths then run over one rank: tests on a single GPU)
   bool mshard() const { return comm && cfg.shard_mode == OICA_SHARD_M; }
+  bool hybrid() const { return comm && cfg.shard_mode == OICA_SHARD_HYBRID; }
   bool collective() const { return comm != nullptr; }
 
   void count(int n) { stats.kernel_launches += n; }
@@ -351,19 +364,20 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, bool lo_capa
 }
 
 // Work counters of one executed iteration with L_act rows, n_coarse of them coarse.
-void account_iteration(oica_ctx* c, int L_act, int n_coarse) {
+void account_iteration(oica_ctx* c, int L_act, int n_coarse, int64_t M_work = -1) {
+  if (M_work < 0) M_work = c->M;
   double issued;
   if (c->tc()) {
     int64_t tiles = ceil_div(L_act, 128), lo_tiles = n_coarse < L_act ? tiles - n_coarse / 128 : 0;
-    issued = 128.0 * (double)c->vNP * (double)c->M * 2.0 * (2.0 * (double)tiles + 2.0 * (double)lo_tiles);
+    issued = 128.0 * (double)c->vNP * (double)M_work * 2.0 * (2.0 * (double)tiles + 2.0 * (double)lo_tiles);
     c->stats.fine_rows += L_act - n_coarse;
   } else {
-    issued = (double)round_up(L_act, 64) * (double)c->vNP * (double)c->M * 4.0;
+    issued = (double)round_up(L_act, 64) * (double)c->vNP * (double)M_work * 4.0;
   }
   c->stats.iterations += 1;
   c->stats.sum_active += L_act;
   c->stats.step_flops += (double)L_act * (4.0 * (double)c->vN * (double)c->Mg + 3.0 * (double)c->Mg) *
-                         ((double)c->M / (double)c->Mg);
+                         ((double)M_work / (double)c->Mg);
   c->stats.step_issued_flops += issued;
 }
 
@@ -489,6 +503,164 @@ void use_reduced_view(oica_ctx* c, int d) {
   c->reduced = true;
 }
 
+// Active counts of every rank (hybrid mode): one all-gather of the device counter.
+std::vector<int> gather_counts(oica_ctx* c) {
+  const int W = c->world();
+  c->tail.cnt_all.ensure((size_t)W);
+  OICA_NCCL(Nccl::get().AllGather(c->Lact_dev.p, c->tail.cnt_all.p, 1, ncclInt32, c->comm, c->st));
+  std::vector<int> v((size_t)W);
+  OICA_CUDA(cudaMemcpyAsync(v.data(), c->tail.cnt_all.p, sizeof(int) * W, cudaMemcpyDeviceToHost, c->st));
+  OICA_CUDA(cudaStreamSynchronize(c->st));
+  return v;
+}
+
+int hybrid_rows(const oica_ctx* c) {
+  static const int env = [] { const char* e = getenv("OICA_HYBRID_ROWS"); return e ? atoi(e) : -1; }();
+  return env >= 0 ? env : kHybridRowsPerRank * c->world();
+}
+
+// Hybrid tail: the T runs still active on all ranks (this rank's are
+// act[0..L_local)) are all-gathered in rank order (C4) and iterated M-sharded: every rank runs
+// all T rows over its share of the slots of its replicated X, one fp64 all-reduce of G per
+// iteration, identical epilogue decisions everywhere; finished rows go back to
+// their owners by global id.  Iterations t+1.. continue the component's count; returns this
+// rank's share of the sum of active rows (rank 0 reports the tail).
+int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vector<int>& counts, int& t, int K,
+                        double tol, int kk, int vN) {
+  cudaStream_t st = c->st;
+  auto& tb = c->tail;
+  auto& nc = Nccl::get();
+  const int W = c->world(), NP = c->vNP, R = vN + 4;
+  const bool tc = c->tc();
+  int T = 0, Pmax = 0;
+  for (int v : counts) {
+    T += v;
+    Pmax = std::max(Pmax, v);
+  }
+  sync_x(c);
+  tb.pack.ensure((size_t)Pmax * R);
+  tb.pack_all.ensure((size_t)W * Pmax * R);
+  tb.dense.ensure((size_t)T * R);
+  tb.W64.ensure((size_t)T * vN);
+  tb.alpha.ensure(T);
+  tb.dprev.ensure(T);
+  tb.ids.ensure(T);
+  tb.iters.ensure(T);
+  tb.act0.ensure(T);
+  tb.act1.ensure(T);
+  tb.state.ensure(T);
+  tb.keep.ensure(T);
+  tb.fine.ensure(T);
+  tb.Gsum.ensure((size_t)T * NP);
+  tb.s4sum.ensure(T);
+  tb.hist.ensure(2 * ((size_t)K + 1));
+  // C4: records of this rank's active rows, all-gathered; dense in rank order
+  c->count(launch_tail_pack(st, act, c->Lact_dev.p, L_local, c->W64.p, c->alpha_old.p, tc ? c->dprev.p : nullptr,
+                            c->fine_flags(), c->id_base, vN, tb.pack.p));
+  OICA_NCCL(nc.AllGather(tb.pack.p, tb.pack_all.p, (size_t)Pmax * R, ncclFloat64, c->comm, st));
+  size_t off = 0;
+  for (int r = 0; r < W; ++r) {
+    if (counts[r] > 0)
+      OICA_CUDA(cudaMemcpyAsync(tb.dense.p + off * R, tb.pack_all.p + (size_t)r * Pmax * R,
+                                sizeof(double) * counts[r] * R, cudaMemcpyDeviceToDevice, st));
+    off += counts[r];
+  }
+  c->count(launch_tail_unpack(st, tb.dense.p, T, vN, tb.W64.p, tb.alpha.p, tb.dprev.p, tb.fine.p, tb.state.p,
+                              tb.keep.p, tb.ids.p));
+  c->count(launch_compact(st, nullptr, tb.keep.p, tc ? tb.fine.p : nullptr, T, tb.act0.p, c->Lact_dev.p,
+                          c->Lact_host));
+  OICA_CUDA(cudaMemsetAsync(tb.hist.p, 0, sizeof(int) * 2 * ((size_t)K + 1), st));
+  // tail slot plan: ~2 CTAs per SM on every rank for T rows; rank r owns slots [S r/W, S (r+1)/W)
+  int tiles = (int)ceil_div(T, 128);
+  if (tc && NP > 64) tiles = (int)round_up(tiles, 2);
+  const int64_t S_want = std::min<int64_t>(kTailMaxSlots, (int64_t)W * std::max<int64_t>(1, ceil_div(2 * c->num_sms, tiles)));
+  const int64_t slot_len = std::max<int64_t>(kSlotAlign, round_up(ceil_div(c->M, S_want), kSlotAlign));
+  const int S_all = (int)ceil_div(c->M, slot_len);
+  const int s0 = (int)((int64_t)S_all * c->cfg.rank / W), s1 = (int)((int64_t)S_all * (c->cfg.rank + 1) / W);
+  const int s_cnt = s1 - s0;
+  const int64_t m0 = (int64_t)s0 * slot_len, m1 = std::min<int64_t>(c->M, (int64_t)s1 * slot_len);
+  const int64_t M_r = std::max<int64_t>(0, m1 - m0);
+  if (tc) {
+    tb.Gp32.ensure((size_t)std::max(S_all, 1) * T * NP);
+    tb.Whi.ensure((size_t)T * NP);
+    tb.Wlo.ensure((size_t)T * NP);
+  } else {
+    tb.Gp.ensure((size_t)std::max(s_cnt, 1) * T * NP);
+    tb.s4p.ensure((size_t)std::max(s_cnt, 1) * T);
+    tb.W32.ensure((size_t)T * NP);
+  }
+  EvalPoint ev = tc ? EvalPoint{tb.Whi.p, tb.Wlo.p, nullptr, NP} : EvalPoint{nullptr, nullptr, tb.W32.p, NP};
+  Promotion pr = c->promotion();
+  if (tc) {
+    pr.fine = tb.fine.p;
+    pr.dprev = tb.dprev.p;
+  }
+  OICA_CUDA(cudaStreamSynchronize(st));
+  int L_ub = ((volatile int*)c->Lact_host)[0], nc_ub = ((volatile int*)c->Lact_host)[1];
+  const int nc_first = nc_ub;
+  int* a_cur = tb.act0.p;
+  int* a_nxt = tb.act1.p;
+  const int t_start = t;
+  while (L_ub > 0 && t < K) {
+    const int B = std::min(K - t, L_ub <= kBatchRows ? kBatch : 1);   // identical on every rank
+    for (int b = 0; b < B; ++b) {
+      ++t;
+      const int* cnt = c->Lact_dev.p;
+      if (tc)
+        c->count(launch_operand_f16x2(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.fine.p, tb.Whi.p, tb.Wlo.p));
+      else
+        c->count(launch_operand_f32(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.W32.p));
+      cudaEvent_t e0 = c->event();
+      OICA_CUDA(cudaEventRecord(e0, st));
+      int n = 0;
+      if (s_cnt > 0 && tc)
+        n = launch_step_tc(st, c->vXh, c->ldx, c->M, NP, tb.Whi.p, tb.Wlo.p, nc_ub, L_ub, slot_len, S_all, tb.Gp32.p, T,
+                           cnt, B > 1 && !c->split(), Upload{s0, s_cnt});
+      else if (s_cnt > 0)
+        n = launch_step_simt(st, c->vX + m0, c->vld, M_r, vN, NP, tb.W32.p, L_ub, slot_len, s_cnt, kFlush, tb.Gp.p,
+                             tb.s4p.p, T, cnt);
+      check_launch();
+      c->count(n);
+      c->stats.step_launches += n;
+      cudaEvent_t e1 = c->event();
+      OICA_CUDA(cudaEventRecord(e1, st));
+      SlotPartials part = tc ? SlotPartials{tb.Gp32.p + (size_t)s0 * T * NP, true} : SlotPartials{tb.Gp.p, false};
+      c->count(launch_slot_reduce(st, part, tc ? nullptr : tb.s4p.p, s_cnt, T, NP, L_ub, vN, tb.Gsum.p, NP,
+                                  tb.s4sum.p));
+      OICA_NCCL(nc.AllReduce(tb.Gsum.p, tb.Gsum.p, (size_t)L_ub * NP, ncclFloat64, ncclSum, c->comm, st));
+      if (!tc) OICA_NCCL(nc.AllReduce(tb.s4sum.p, tb.s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st));
+      c->count(launch_epilogue(st, SlotPartials{tb.Gsum.p, false}, tc ? nullptr : tb.s4sum.p, 1, T, NP, ev, a_cur,
+                               L_ub, c->Wacc.p, kk, vN, (double)c->Mg, tol, t, tb.W64.p, tb.alpha.p, tb.iters.p,
+                               tb.state.p, tb.keep.p, pr, cnt));
+      c->count(launch_compact(st, a_cur, tb.keep.p, tc ? tb.fine.p : nullptr, L_ub, a_nxt, c->Lact_dev.p,
+                              c->Lact_host, cnt, tb.hist.p + 2 * t));
+      std::swap(a_cur, a_nxt);
+      check_launch();
+    }
+    OICA_CUDA(cudaStreamSynchronize(st));
+    L_ub = ((volatile int*)c->Lact_host)[0];
+    nc_ub = ((volatile int*)c->Lact_host)[1];
+  }
+  // finished (or capped) runs back to their owners
+  c->count(launch_tail_scatter(st, T, tb.ids.p, tb.W64.p, tb.alpha.p, tb.iters.p, tb.state.p, c->id_base, c->Ll, vN,
+                               c->W64.p, c->alpha_old.p, c->iters.p, c->state.p));
+  check_launch();
+  // work counters: rows entering tail iteration t' (T for the first)
+  std::vector<int> hist(2 * ((size_t)K + 1), 0);
+  OICA_CUDA(cudaMemcpyAsync(hist.data(), tb.hist.p, sizeof(int) * hist.size(), cudaMemcpyDeviceToHost, st));
+  OICA_CUDA(cudaStreamSynchronize(st));
+  int64_t sum_active = 0;
+  for (int tt = t_start + 1; tt <= t; ++tt) {
+    const int Lin = tt == t_start + 1 ? T : hist[2 * (tt - 1)];
+    const int ncin = tt == t_start + 1 ? nc_first : hist[2 * (tt - 1) + 1];
+    if (Lin <= 0) break;
+    account_iteration(c, Lin, ncin, M_r);
+    sum_active += Lin;
+    ++c->stats.tail_iterations;
+  }
+  return c->cfg.rank == 0 ? sum_active : 0;
+}
+
 void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t flags, const double* W_prefix,
                   int32_t k_prefix, oica_result* out) {
   OICA_REQUIRE(c->X, OICA_ERR_STATE, "oica_set_data has not been called");
@@ -577,10 +749,24 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     const int L0 = L_act, nc0 = n_coarse;
     int t = 0;
     int L_ub = L_act, nc_ub = n_coarse;
-    while (L_ub > 0 && t < K) {
-      const int B = std::min(K - t, (L_ub <= kBatchRows && !c->mshard()) ? kBatch : 1);
+    // OICA_SHARD_HYBRID: the loop runs on the GLOBAL active count (ranks stay in step; a rank
+    // without active rows idles) until it falls to hybrid_rows(), then the tail takes over
+    const bool hyb = c->hybrid();
+    std::vector<int> counts;
+    int G_ub = L_ub;
+    auto tail_now = [&]() {
+      counts = gather_counts(c);
+      G_ub = std::accumulate(counts.begin(), counts.end(), 0);
+      return G_ub > 0 && G_ub <= hybrid_rows(c) && t < K;
+    };
+    if (hyb) OICA_CUDA(cudaMemsetAsync(c->hist.p, 0, sizeof(int) * 2 * ((size_t)K + 1), st));
+    bool to_tail = hyb && tail_now();
+    while (!to_tail && (hyb ? G_ub : L_ub) > 0 && t < K) {
+      const int B = std::min(K - t, ((hyb ? G_ub : L_ub) <= kBatchRows * (hyb ? c->world() : 1) && !c->mshard())
+                                        ? kBatch : 1);
       for (int b = 0; b < B; ++b) {
         ++t;
+        if (L_ub == 0) continue;   // hybrid: this rank idles while others iterate
         const int* cnt = c->Lact_dev.p;
         run_step(c, L_ub, nc_ub, cnt, B > 1 && c->tc() && !c->split(), true);
         const bool tc = c->tc();
@@ -610,22 +796,31 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
       OICA_CUDA(cudaStreamSynchronize(st));
       L_ub = ((volatile int*)c->Lact_host)[0];
       nc_ub = ((volatile int*)c->Lact_host)[1];
+      if (hyb) to_tail = tail_now();
     }
+    const int t_bulk = t;
+    int64_t tail_active = 0;
+    if (to_tail) tail_active = run_hybrid_tail(c, act, L_ub, counts, t, K, tol, kk, vN);
     trace.mark("iterate");
     // per-iteration counts: entering iteration t' the active set had hist[t'-1] rows (t' >= 2)
-    std::vector<int> hist(2 * (size_t)(t + 1), 0);
-    if (t > 0) {
-      OICA_CUDA(cudaMemcpyAsync(hist.data(), c->hist.p, sizeof(int) * 2 * (size_t)(t + 1), cudaMemcpyDeviceToHost, st));
+    std::vector<int> hist(2 * (size_t)(t_bulk + 1), 0);
+    if (t_bulk > 0) {
+      OICA_CUDA(cudaMemcpyAsync(hist.data(), c->hist.p, sizeof(int) * 2 * (size_t)(t_bulk + 1), cudaMemcpyDeviceToHost,
+                                st));
       OICA_CUDA(cudaStreamSynchronize(st));
     }
     int64_t sum_active = 0;
     int t_exec = 0;
-    for (int tt = 1; tt <= t; ++tt) {
+    for (int tt = 1; tt <= t_bulk; ++tt) {
       int Lin = tt == 1 ? L0 : hist[2 * (tt - 1)], ncin = tt == 1 ? nc0 : hist[2 * (tt - 1) + 1];
       if (Lin <= 0) break;
       account_iteration(c, Lin, ncin);
       sum_active += Lin;
       t_exec = tt;
+    }
+    if (to_tail) {   // the tail's rows were counted by rank 0 (the merge sums ranks)
+      sum_active += tail_active;
+      t_exec = t;
     }
     t = t_exec;
     // a7: selection and accept
@@ -789,6 +984,7 @@ oica_status oica_create(const oica_config* cfg, oica_ctx** out) {
   if (!cfg || !out) return OICA_ERR_INVALID_ARGUMENT;
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world || cfg->world > 64) return OICA_ERR_INVALID_ARGUMENT;
   if (cfg->world > 1 && !cfg->nccl_unique_id) return OICA_ERR_INVALID_ARGUMENT;
+  if (cfg->shard_mode < OICA_SHARD_L || cfg->shard_mode > OICA_SHARD_HYBRID) return OICA_ERR_INVALID_ARGUMENT;
   *out = nullptr;
   oica_ctx* c = new (std::nothrow) oica_ctx();
   if (!c) return OICA_ERR_OUT_OF_MEMORY;
@@ -963,18 +1159,36 @@ oica_status oica_extract_components(oica_ctx* c, int32_t N_out, int32_t K, doubl
 }
 
 oica_status oica_fixed_point_step(oica_ctx* c, const double* W_dev, int64_t L, double* G_dev, double* s4_dev) {
+  return oica_fixed_point_step_mixed(c, W_dev, L, nullptr, G_dev, s4_dev);
+}
+
+oica_status oica_fixed_point_step_mixed(oica_ctx* c, const double* W_dev, int64_t L, const uint8_t* fine_host,
+                                        double* G_dev, double* s4_dev) {
   if (!c) return OICA_ERR_INVALID_ARGUMENT;
   return guard(c, [&] {
     OICA_REQUIRE(c->X && c->have_cand, OICA_ERR_STATE, "set_data and init_candidates first");
     OICA_REQUIRE(W_dev && G_dev && s4_dev && L >= 1 && L <= c->Ll, OICA_ERR_INVALID_ARGUMENT, "bad arguments");
+    // per-row precision: coarse rows first (the compaction's order), n_coarse of them
+    int n_coarse = c->split() ? 0 : (int)L;
+    std::vector<uint8_t> fl;
+    if (fine_host && c->tc()) {
+      fl.assign(fine_host, fine_host + L);
+      for (auto& f : fl) f = f ? 1 : 0;
+      n_coarse = (int)(std::find(fl.begin(), fl.end(), (uint8_t)1) - fl.begin());
+      OICA_REQUIRE(std::find(fl.begin() + n_coarse, fl.end(), (uint8_t)0) == fl.end(), OICA_ERR_INVALID_ARGUMENT,
+                   "fine rows must follow every coarse row");
+    }
     // stage caller rows through the fp64 master (identity active list)
     OICA_CUDA(cudaMemcpyAsync(c->W64.p, W_dev, sizeof(double) * L * c->N, cudaMemcpyDeviceToDevice, c->st));
     OICA_CUDA(cudaMemsetAsync(c->keep.p, 1, L, c->st));
-    OICA_CUDA(cudaMemsetAsync(c->fine.p, c->split() ? 1 : 0, L, c->st));   // one precision for all rows
+    if (!fl.empty())
+      OICA_CUDA(cudaMemcpyAsync(c->fine.p, fl.data(), L, cudaMemcpyHostToDevice, c->st));
+    else
+      OICA_CUDA(cudaMemsetAsync(c->fine.p, c->split() ? 1 : 0, L, c->st));   // one precision for all rows
     c->count(launch_compact(c->st, nullptr, c->keep.p, nullptr, (int)L, c->act0.p, c->Lact_dev.p, nullptr));
     build_operand(c, c->act0.p, (int)L);
-    run_step(c, (int)L, c->split() ? 0 : (int)L, nullptr, false, true);
-    account_iteration(c, (int)L, c->split() ? 0 : (int)L);
+    run_step(c, (int)L, n_coarse, nullptr, false, true);
+    account_iteration(c, (int)L, n_coarse);
     bool tc = c->tc();
     c->count(launch_slot_reduce(c->st, c->partials(), tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L,
                                 (int)c->N, G_dev, (int)c->N, s4_dev));

@@ -25,7 +25,7 @@ STATUS = ["OK", "INVALID_ARGUMENT", "DIMENSION_MISMATCH", "RANK_DEFICIENT", "ALL
           "DOMAIN", "STATE", "UNSUPPORTED_DEVICE", "OUT_OF_MEMORY", "CUDA", "NCCL"]
 
 PREC_AUTO, PREC_FP32, PREC_TC, PREC_TC_SPLIT = 0, 1, 2, 3
-SHARD_L, SHARD_M = 0, 1
+SHARD_L, SHARD_M, SHARD_HYBRID = 0, 1, 2
 INCLUDE_UNCONVERGED, STOP_ON_GAUSSIANITY, RAW_ARGMAX, REDUCE_X = 0x1, 0x2, 0x4, 0x8
 MAX_CLUSTERS = 8
 
@@ -59,7 +59,7 @@ class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("step_launches", C.c_int64), ("step_ms", C.c_double),
                 ("step_flops", C.c_double), ("iterations", C.c_int64), ("sum_active", C.c_int64),
                 ("precision", C.c_int32), ("slots", C.c_int32), ("step_issued_flops", C.c_double),
-                ("fine_rows", C.c_int64)]
+                ("fine_rows", C.c_int64), ("tail_iterations", C.c_int64)]
 
 
 class ClusterRecord(C.Structure):
@@ -82,6 +82,8 @@ SIGNATURES = {
     "oica_extract_components": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_uint32,
                                           _P(C.c_double), C.c_int32, _P(Result)]),
     "oica_fixed_point_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "oica_fixed_point_step_mixed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, _P(C.c_uint8), C.c_void_p,
+                                              C.c_void_p]),
     "oica_draw_candidates": (C.c_int, [C.c_void_p, C.c_int32, _P(C.c_double), C.c_int32, C.c_void_p]),
     "oica_get_candidates": (C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_double), _P(C.c_int32), _P(C.c_uint8),
                                       _P(C.c_int64), _P(C.c_int64)]),
@@ -313,9 +315,15 @@ class Context:
                           stopped=bool(res.stopped))
 
     # -- test / bench entry points
-    def fixed_point_step(self, W, G_out, s4_out):
+    def fixed_point_step(self, W, G_out, s4_out, fine: Optional[np.ndarray] = None):
+        """One contraction; `fine` (host uint8 per row, fine rows last): per-row precision."""
         L = W.shape[0]
-        self._c(lib().oica_fixed_point_step(self.h, _dptr(W), L, _dptr(G_out), _dptr(s4_out)))
+        if fine is None:
+            self._c(lib().oica_fixed_point_step(self.h, _dptr(W), L, _dptr(G_out), _dptr(s4_out)))
+        else:
+            f = np.ascontiguousarray(fine, dtype=np.uint8)
+            self._c(lib().oica_fixed_point_step_mixed(self.h, _dptr(W), L, _np_ptr(f, C.c_uint8), _dptr(G_out),
+                                                      _dptr(s4_out)))
 
     def draw_candidates(self, i: int, W_acc: Optional[np.ndarray], W_out):
         k = 0 if W_acc is None else W_acc.shape[0]

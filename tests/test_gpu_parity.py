@@ -100,6 +100,39 @@ def test_step_is_row_independent_and_deterministic():
     assert np.array_equal(outs[0][0][:37], outs[2][0])
 
 
+@pytest.mark.parametrize("name,boundary", [("p_n40", 200), ("p_tc_n128", 100), ("p_tc_n256", 100)])
+def test_step_mixed_precision_tile_independent(name, boundary):
+    """A row's contraction does not depend on the rows sharing its 128-row tile:
+    coarse rows inside a two-pass ("fine") tile equal the all-coarse result bitwise, fine rows the
+    all-fine result; the fine rows are the more accurate ones against the fp64 oracle."""
+    cfg, ctx = ctx_for(name, oica.PREC_TC)
+    _, _, X64 = prepared(name)
+    L = cfg.L
+    W = rng.candidates(11, 1, np.arange(L), cfg.N)
+    W /= np.linalg.norm(W, axis=1, keepdims=True)
+    Wd = torch.from_numpy(W).cuda()
+
+    def step(fine):
+        G = torch.zeros(L, cfg.N, dtype=torch.float64, device="cuda")
+        s4 = torch.zeros(L, dtype=torch.float64, device="cuda")
+        ctx.fixed_point_step(Wd, G, s4, fine=fine)
+        return G.cpu().numpy(), s4.cpu().numpy()
+
+    mixed = np.zeros(L, np.uint8)
+    mixed[boundary:] = 1
+    Gm, sm = step(mixed)
+    Gc, sc = step(np.zeros(L, np.uint8))
+    Gf, sf = step(np.ones(L, np.uint8))
+    assert np.array_equal(Gm[:boundary], Gc[:boundary]) and np.array_equal(sm[:boundary], sc[:boundary])
+    assert np.array_equal(Gm[boundary:], Gf[boundary:]) and np.array_equal(sm[boundary:], sf[boundary:])
+    with pytest.raises(oica.OicaError):
+        step(1 - mixed)   # fine rows must follow the coarse rows
+    Gref, _ = ordering.batch_step(W, X64)
+    Graw = (Gref + 3.0 * W) * X64.shape[1]
+    ec, ef = np.abs(Gc - Graw).mean(), np.abs(Gf - Graw).mean()
+    assert ef < 0.5 * ec, (ef, ec)
+
+
 def _compare(res_gpu, res_or, W_or, X64, allow_near_tie=True):
     idx_g = list(res_gpu.index[: res_gpu.n_extracted])
     idx_o = [r.index for r in res_or]
@@ -340,7 +373,7 @@ def test_paper_experiment_parity(name, L):
 # exchange (two all-gathers + device merge per component) and the M-shard per-iteration fp64
 # all-reduce run for real; the decisions must be those of the oracle
 @pytest.mark.parametrize("name,precision", [("p_n40", oica.PREC_FP32), ("p_tc_n128", oica.PREC_AUTO)])
-@pytest.mark.parametrize("shard", [oica.SHARD_L, oica.SHARD_M])
+@pytest.mark.parametrize("shard", [oica.SHARD_L, oica.SHARD_M, oica.SHARD_HYBRID])
 def test_exchange_paths_single_rank(name, precision, shard):
     cfg, X32, X64 = prepared(name)
     W_or, res_or, _ = oracle_run(name)
@@ -350,6 +383,10 @@ def test_exchange_paths_single_rank(name, precision, shard):
         ctx.init_candidates(cfg.cand_seed, cfg.L)
         res = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
         red = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=oica.REDUCE_X)
+        tail = ctx.stats()["tail_iterations"]
+    # hybrid: the last <= 128 active runs of every component go through the gather / M-sharded
+    # tail / scatter path (tail slot plan: within tolerance of the L-shard result)
+    assert (tail > 0) == (shard == oica.SHARD_HYBRID)
     for out in (res, red):
         _compare(out, res_or, W_or, X64)
     if shard == oica.SHARD_L:   # the exchange does not change the arithmetic: bitwise equal
