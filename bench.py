@@ -194,7 +194,7 @@ def run_oica(args, cfg):
     stream = torch.cuda.Stream(device=dev)
     prec = {"auto": oica.PREC_AUTO, "fp32": oica.PREC_FP32, "tc": oica.PREC_TC,
             "tc_split": oica.PREC_TC_SPLIT}[args.precision]
-    shard = oica.SHARD_M if args.shard == "m" else oica.SHARD_L
+    shard = {"l": oica.SHARD_L, "m": oica.SHARD_M, "hybrid": oica.SHARD_HYBRID}[args.shard]
     ctx = oica.Context(local, prec, rank, world, shard, stream=stream, nccl_id=nid)
 
     # synthetic inputs of the config's recipe, generated and whitened on the device (not timed)
@@ -342,7 +342,7 @@ def run_oica(args, cfg):
            "vs_baseline": None, "dtype": "f16" if precision.startswith("tc") else "f32", "data": "synthetic",
            "config": {"workload": cfg.name, "N": cfg.N, "M": cfg.M, "L": cfg.L, "K": cfg.K, "tol": cfg.tol,
                       "N_out": cfg.N_out, "components_timed": [r["i"] for r in timed],
-                      "parallelism": f"{'m' if shard == oica.SHARD_M else 'l'}shard{world}",
+                      "parallelism": f"{args.shard}shard{world}",
                       "l2": f"inputs larger than L2 (X = {4 * cfg.N * cfg.M / 1e9:.2f} GB fp32), no flush",
                       "precision": precision, "slots": st["slots"],
                       "reduced_x": bool(args.reduce)},
@@ -363,7 +363,7 @@ def main():
     ap.add_argument("--impl", default="oica", choices=["oica", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tc", "tc_split"])
-    ap.add_argument("--shard", default="l", choices=["l", "m"])
+    ap.add_argument("--shard", default="l", choices=["l", "m", "hybrid"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--reduce", action="store_true",
                     help="iterate on the reduced data X~ = G X (PAPER.md §3.3, OICA_REDUCE_X)")
