@@ -215,6 +215,20 @@ oica_status oica_draw_candidates(oica_ctx* ctx, int32_t i, const double* W_acc, 
  * iterations, state (0 active/unconverged, 1 converged, 2 degenerate). */
 oica_status oica_get_candidates(oica_ctx* ctx, double* W, double* alpha, int32_t* iters,
                                 uint8_t* state, int64_t* L_local, int64_t* id_base);
+/* Per-iteration log of the last oica_extract_components call: one record per
+ * executed fixed-point iteration of every component on this rank.  step_ms is the CUDA-event
+ * time of that iteration's step launch(es) on the context stream; flops its algorithmic work
+ * L_act (4 d + 3) M_local (d = the dimension iterated on).  Copies min(cap, *n) records;
+ * *n = the number available (call with cap = 0 to size). */
+typedef struct {
+  int32_t component;   /* 1-based i                                                           */
+  int32_t iteration;   /* t (1-based)                                                         */
+  int32_t L_act;       /* active runs entering the iteration                                  */
+  int32_t fine_rows;   /* of which run in two-pass precision                                  */
+  double step_ms;
+  double flops;
+} oica_iteration_record;
+oica_status oica_get_iteration_log(oica_ctx* ctx, oica_iteration_record* out, int64_t cap, int64_t* n);
 oica_status oica_get_stats(oica_ctx* ctx, oica_stats* out);
 oica_status oica_reset_stats(oica_ctx* ctx);
 /* Synchronise the context's stream (for host-side timing). */

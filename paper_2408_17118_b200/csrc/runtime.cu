@@ -167,14 +167,23 @@ struct oica_ctx {
     }
     return ev[ev_used++];
   }
+  // per-iteration log (oica_get_iteration_log): the iteration each timed event pair belongs to
+  int cur_t = 0;
+  std::vector<int> ev_t;
+  std::vector<std::pair<int, float>> pairs;   // (iteration, ms) of the last harvest
+  std::vector<oica_iteration_record> iter_log;
+  void mark_pair() { ev_t.push_back(cur_t); }
   void harvest_events() {
     OICA_CUDA(cudaStreamSynchronize(st));
+    pairs.clear();
     for (size_t k = 0; k + 1 < ev_used; k += 2) {
       float ms = 0.f;
       OICA_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
       stats.step_ms += ms;
+      pairs.emplace_back(k / 2 < ev_t.size() ? ev_t[k / 2] : 0, ms);
     }
     ev_used = 0;
+    ev_t.clear();
   }
 };
 
@@ -329,6 +338,7 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, bool lo_capa
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
     e0 = c->event();
+    c->mark_pair();
     OICA_CUDA(cudaEventRecord(e0, c->st));
   }
   int n;
@@ -526,7 +536,7 @@ int hybrid_rows(const oica_ctx* c) {
 // their owners by global id.  Iterations t+1.. continue the component's count; returns this
 // rank's share of the sum of active rows (rank 0 reports the tail).
 int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vector<int>& counts, int& t, int K,
-                        double tol, int kk, int vN) {
+                        double tol, int kk, int vN, std::vector<std::pair<int, int>>& rows_at) {
   cudaStream_t st = c->st;
   auto& tb = c->tail;
   auto& nc = Nccl::get();
@@ -611,6 +621,8 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
       else
         c->count(launch_operand_f32(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.W32.p));
       cudaEvent_t e0 = c->event();
+      c->cur_t = t;
+      c->mark_pair();
       OICA_CUDA(cudaEventRecord(e0, st));
       int n = 0;
       if (s_cnt > 0 && tc)
@@ -656,6 +668,7 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
     if (Lin <= 0) break;
     account_iteration(c, Lin, ncin, M_r);
     sum_active += Lin;
+    rows_at[tt] = {Lin, ncin};
     ++c->stats.tail_iterations;
   }
   return c->cfg.rank == 0 ? sum_active : 0;
@@ -716,6 +729,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     c->Wacc_scratch.ensure((size_t)N);
   }
   use_full_view(c);
+  c->iter_log.clear();
   PhaseTrace trace;
   for (int k = k_prefix; k < N_out; ++k) {
     const int i = k + 1;  // 1-based component index
@@ -768,6 +782,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         ++t;
         if (L_ub == 0) continue;   // hybrid: this rank idles while others iterate
         const int* cnt = c->Lact_dev.p;
+        c->cur_t = t;
         run_step(c, L_ub, nc_ub, cnt, B > 1 && c->tc() && !c->split(), true);
         const bool tc = c->tc();
         SlotPartials G = c->partials();
@@ -800,7 +815,8 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     }
     const int t_bulk = t;
     int64_t tail_active = 0;
-    if (to_tail) tail_active = run_hybrid_tail(c, act, L_ub, counts, t, K, tol, kk, vN);
+    std::vector<std::pair<int, int>> rows_at((size_t)K + 2, {0, 0});   // (L_act, n_coarse) entering iteration t
+    if (to_tail) tail_active = run_hybrid_tail(c, act, L_ub, counts, t, K, tol, kk, vN, rows_at);
     trace.mark("iterate");
     // per-iteration counts: entering iteration t' the active set had hist[t'-1] rows (t' >= 2)
     std::vector<int> hist(2 * (size_t)(t_bulk + 1), 0);
@@ -816,6 +832,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
       if (Lin <= 0) break;
       account_iteration(c, Lin, ncin);
       sum_active += Lin;
+      rows_at[tt] = {Lin, ncin};
       t_exec = tt;
     }
     if (to_tail) {   // the tail's rows were counted by rank 0 (the merge sums ranks)
@@ -851,6 +868,19 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     OICA_CUDA(cudaMemcpyAsync(&rec_h, c->rec.p, sizeof(ComponentRecord), cudaMemcpyDeviceToHost, st));
     OICA_CUDA(cudaMemcpyAsync(b_host.data(), c->w_out.p, sizeof(double) * vN, cudaMemcpyDeviceToHost, st));
     c->harvest_events();
+    for (const auto& pr : c->pairs) {   // per-iteration log: launches of executed iterations
+      const int tt = pr.first;
+      if (tt < 1 || tt > K || rows_at[tt].first <= 0) continue;
+      const int Lin = rows_at[tt].first, ncin = rows_at[tt].second;
+      oica_iteration_record r{};
+      r.component = i;
+      r.iteration = tt;
+      r.L_act = Lin;
+      r.fine_rows = Lin - ncin;
+      r.step_ms = pr.second;
+      r.flops = (double)Lin * (4.0 * vN + 3.0) * (double)c->M;
+      c->iter_log.push_back(r);
+    }
     trace.mark("select");
     c->last_valid = true;
     if (rec_h.status != OICA_OK)
@@ -1244,6 +1274,13 @@ oica_status oica_get_candidates(oica_ctx* c, double* W, double* alpha, int32_t* 
         }
     }
   });
+}
+
+oica_status oica_get_iteration_log(oica_ctx* c, oica_iteration_record* out, int64_t cap, int64_t* n) {
+  if (!c || !n || (cap > 0 && !out)) return OICA_ERR_INVALID_ARGUMENT;
+  *n = (int64_t)c->iter_log.size();
+  for (int64_t k = 0; k < std::min<int64_t>(cap, *n); ++k) out[k] = c->iter_log[(size_t)k];
+  return OICA_OK;
 }
 
 oica_status oica_get_stats(oica_ctx* c, oica_stats* out) {

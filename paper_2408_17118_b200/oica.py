@@ -62,6 +62,11 @@ class Stats(C.Structure):
                 ("fine_rows", C.c_int64), ("tail_iterations", C.c_int64)]
 
 
+class IterationRecord(C.Structure):
+    _fields_ = [("component", C.c_int32), ("iteration", C.c_int32), ("L_act", C.c_int32), ("fine_rows", C.c_int32),
+                ("step_ms", C.c_double), ("flops", C.c_double)]
+
+
 class ClusterRecord(C.Structure):
     _fields_ = [("upsilon", C.c_double), ("alpha", C.c_double), ("q", C.c_int64), ("size", C.c_int64),
                 ("iters", C.c_int32), ("valid", C.c_int32)]
@@ -88,6 +93,7 @@ SIGNATURES = {
     "oica_get_candidates": (C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_double), _P(C.c_int32), _P(C.c_uint8),
                                       _P(C.c_int64), _P(C.c_int64)]),
     "oica_get_stats": (C.c_int, [C.c_void_p, _P(Stats)]),
+    "oica_get_iteration_log": (C.c_int, [C.c_void_p, _P(IterationRecord), C.c_int64, _P(C.c_int64)]),
     "oica_reset_stats": (C.c_int, [C.c_void_p]),
     "oica_synchronize": (C.c_int, [C.c_void_p]),
     "oica_merge_records": (C.c_int, [_P(ClusterRecord), _P(C.c_double), C.c_int32, C.c_int32, _P(C.c_int32),
@@ -341,6 +347,15 @@ class Context:
         self._c(lib().oica_get_candidates(self.h, _np_ptr(W, C.c_double), _np_ptr(alpha, C.c_double),
                                           _np_ptr(iters, C.c_int32), _np_ptr(state, C.c_uint8), None, None))
         return dict(W=W, alpha=alpha, iters=iters, state=state, id_base=base.value)
+
+    def iteration_log(self) -> list:
+        """Per-iteration records of the last extract call (component, iteration, L_act, fine_rows,
+        step_ms, flops)."""
+        n = C.c_int64()
+        self._c(lib().oica_get_iteration_log(self.h, None, 0, C.byref(n)))
+        buf = (IterationRecord * max(1, n.value))()
+        self._c(lib().oica_get_iteration_log(self.h, buf, n.value, C.byref(n)))
+        return [{f: getattr(buf[k], f) for f, _ in IterationRecord._fields_} for k in range(n.value)]
 
     def stats(self) -> dict:
         s = Stats()

@@ -133,6 +133,26 @@ def test_step_mixed_precision_tile_independent(name, boundary):
     assert ef < 0.5 * ec, (ef, ec)
 
 
+@pytest.mark.parametrize("name,flags", [("p_tc_n128", 0), ("p_n40", 0), ("p_tc_n128", oica.REDUCE_X)])
+def test_iteration_log(name, flags):
+    """oica_get_iteration_log (SURVEY §8(d) per-iteration logs): one record per executed iteration,
+    consistent with the per-component result counters."""
+    cfg, ctx = ctx_for(name)
+    with ctx:
+        res = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=flags)
+        log = ctx.iteration_log()
+    assert log
+    for k in range(res.n_extracted):
+        recs = [r for r in log if r["component"] == k + 1]
+        assert [r["iteration"] for r in recs] == list(range(1, len(recs) + 1))
+        assert len(recs) == res.n_iter[k]
+        assert sum(r["L_act"] for r in recs) == res.sum_active[k]
+        assert all(r["L_act"] >= max(1, r["fine_rows"]) and r["step_ms"] > 0 for r in recs)
+        assert all(a["L_act"] >= b["L_act"] for a, b in zip(recs, recs[1:]))   # runs only leave
+        d = cfg.N - k if flags & oica.REDUCE_X and k else cfg.N
+        assert all(r["flops"] == pytest.approx(r["L_act"] * (4 * d + 3) * cfg.M) for r in recs)
+
+
 def _compare(res_gpu, res_or, W_or, X64, allow_near_tie=True):
     idx_g = list(res_gpu.index[: res_gpu.n_extracted])
     idx_o = [r.index for r in res_or]
