@@ -75,6 +75,18 @@ __device__ __forceinline__ double candidate_normal(uint64_t seed, int i, uint64_
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
+// Split-slot parts (DESIGN.md §5 "few active rows"): when the active row tiles x slots cannot
+// fill the GPU, the chunks of every slot are divided among P CTAs, each with its own fp32 partial
+// (summed in fp64, slot-major).  P depends only on the GLOBAL active count and the slot count, so
+// a row's arithmetic is the same for any GPU count.
+constexpr int kSplitTarget = 296;   // work units wanted per launch (2 per SM)
+constexpr int kSplitMax = 8;
+__host__ __device__ inline int split_parts(int L_global, int S) {
+  const int64_t tiles = round_up(ceil_div(L_global > 0 ? L_global : 1, 128), 2);
+  const int64_t P = kSplitTarget / (tiles * (int64_t)(S > 0 ? S : 1));
+  return (int)(P < 1 ? 1 : (P > kSplitMax ? kSplitMax : P));
+}
+
 // Upsilon of eq. (1), natural log (A14); -inf outside the domain (A13).
 __host__ __device__ inline double upsilon_of(double a) {
   return a > kAlphaFloor ? a - 2.0 * log(a * 0.5 + 1.0) : -INFINITY;

@@ -72,6 +72,14 @@ __global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_loc
 
 __device__ __forceinline__ double slot_sum(SlotPartials Gp, int S, int64_t cap, int ldg, int a, int n) {
   double acc = 0.0;   // fixed slot order
+  if (Gp.f32 && Gp.sub) {   // split-slot parts (common.cuh split_parts): slot-major, part-minor
+    const int P = split_parts(Gp.cnt_g ? Gp.cnt_g[0] : Gp.L_g_host, S);
+    if (P > 1) {
+      for (int s = 0; s < S; ++s)
+        for (int q = 0; q < P; ++q) acc += (double)Gp.sub[(((int64_t)s * kSplitMax + q) * Gp.sub_cap + a) * ldg + n];
+      return acc;
+    }
+  }
   if (Gp.f32) {
     const float* g = (const float*)Gp.p;
     for (int s = 0; s < S; ++s) acc += (double)g[((int64_t)s * cap + a) * ldg + n];

@@ -130,7 +130,17 @@ __device__ __forceinline__ void alpha_accumulate(const double (*ws)[256], const 
     double y[CC];
 #pragma unroll
     for (int c = 0; c < CC; ++c) y[c] = 0.0;
-    for (int n = 0; n < N; ++n) {
+    int n = 0;
+    for (; n + 8 <= N; n += 8) {   // 8 independent loads in flight per thread (latency-bound otherwise)
+      float xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = __ldg(X + (int64_t)(n + u) * ld + m);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int c = 0; c < CC; ++c) y[c] = fma(ws[c][n + u], (double)xv[u], y[c]);
+    }
+    for (; n < N; ++n) {
       double x = (double)__ldg(X + (int64_t)n * ld + m);
 #pragma unroll
       for (int c = 0; c < CC; ++c) y[c] = fma(ws[c][n], x, y[c]);

@@ -223,8 +223,8 @@ template <int NP, bool SPLIT, int EPI, int CL, int RG>
 __global__ void __launch_bounds__(192, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
           const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_ub, int64_t M, int64_t slot_len,
-          float* __restrict__ Gp, int64_t cap, int n_tiles, int n_coarse_h, int order, int S_, const int* __restrict__ cnt,
-          int s_base) {
+          float* __restrict__ Gp, int64_t cap, int n_coarse_h, int S_, const int* __restrict__ cnt, int s_base,
+          int S_total, float* __restrict__ Gsub, int64_t sub_cap, const int* __restrict__ cnt_g, int split) {
   constexpr int NW = 4;   // epilogue warps
   using C = Cfg<NP, SPLIT, RG>;
   constexpr int MT = C::MT;
@@ -247,19 +247,27 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   uint32_t* tmem_slot = (uint32_t*)(gdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // slots [s_base, s_base + gridDim.x / n_tiles) (a launch may cover a slot range: pipelined upload)
-  const int tile = order ? blockIdx.x / S_ : blockIdx.x % n_tiles,
-            s = s_base + (order ? blockIdx.x % S_ : blockIdx.x / n_tiles);
   // active-row count and coarse/fine split: from the device counters when the grid was sized
   // from an upper bound (iterations enqueued without a host round trip)
   const int L_act = cnt ? min(L_ub, cnt[0]) : L_ub;
   const int n_coarse = cnt ? cnt[1] : n_coarse_h;
   const int tile_lo0 = n_coarse / 128;
+  if (L_act <= 0) return;   // grid-uniform
+  // work unit (row tile, slot s of [s_base, s_base + S_), part of P): the grid was sized for the
+  // largest tiles x P the device counts can ask for; P = split_parts of the global count
+  // (common.cuh) divides a slot's chunks among P CTAs when few row tiles are active
+  const int P = split ? split_parts(cnt_g ? cnt_g[0] : L_ub, S_total) : 1;
+  const int n_t = (int)round_up(ceil_div(L_act, 128), CL);
+  const int tile = (int)(blockIdx.x % n_t), rest = (int)(blockIdx.x / n_t);
+  const int s = s_base + rest / P, part = rest % P;
+  if (s >= s_base + S_) return;                      // cluster-uniform (n_t is a multiple of CL)
   if ((tile - tile % CL) * 128 >= L_act) return;   // cluster-uniform: no barrier was touched
   const int row0 = tile * 128;
-  const int64_t m_begin = (int64_t)s * slot_len;
-  const int64_t m_end = min(M, m_begin + slot_len);
-  const int nchunk = (int)ceil_div(m_end - m_begin, MT);
+  const int64_t m_slot = (int64_t)s * slot_len;
+  const int nch_slot = (int)ceil_div(min(M, m_slot + slot_len) - m_slot, MT);
+  const int c_lo = (int)((int64_t)nch_slot * part / P), c_hi = (int)((int64_t)nch_slot * (part + 1) / P);
+  const int64_t m_begin = m_slot + (int64_t)c_lo * MT;
+  const int nchunk = c_hi - c_lo;
   const bool lo_pass = SPLIT && tile >= tile_lo0;   // CTA-uniform
 
   constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
@@ -489,7 +497,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     // G (fp32, scaled 2^-12: y^3 by 2^-6, X by 2^-6) -> fp32 slot partial (x 2^12: exact)
     mbar_wait(gdone, 0);
     tc_fence_after();
-    float* out = Gp + ((int64_t)s * cap + row) * NP;
+    float* out = P > 1 ? Gsub + (((int64_t)s * kSplitMax + part) * sub_cap + row) * NP : Gp + ((int64_t)s * cap + row) * NP;
     bool ok = row < L_act && nchunk > 0;
 #pragma unroll 1
     for (int c = 32 * h; c < NP; c += 32 * NH) {
@@ -551,7 +559,7 @@ CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld,
 template <int NP, bool SPLIT, int EPI, int CL, int RG>
 void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
-               const Upload& up) {
+               const Upload& up, const SplitOut& so) {
   using C = Cfg<NP, SPLIT, RG>;
   auto kern = k_step_tc<NP, SPLIT, EPI, CL, RG>;
   static bool attr = false;
@@ -563,8 +571,10 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   CUtensorMap tx = make_map(Xh, NP, ldx, ldx, NP / CL);
   CUtensorMap tw = tx;
   if (C::WLO_SMEM) tw = make_map(Wlo, cap, NP, NP, 128);
-  int n_tiles = (int)round_up(ceil_div(L_act, 128), CL);   // a cluster = CL tiles of one slot
-  static int order = [] { const char* e = getenv("OICA_TC_ORDER"); return e ? atoi(e) : 0; }();
+  // a cluster = CL tiles of one slot (part); units per slot cover any device count <= L_act:
+  // n_t <= n_tiles, and n_t P <= kSplitTarget / S whenever P > 1 (split_parts)
+  int n_tiles = (int)round_up(ceil_div(L_act, 128), CL);
+  if (so.enable) n_tiles = std::max<int>(n_tiles, (int)round_up(std::max(1, kSplitTarget / std::max(S, 1)), CL));
   cudaLaunchConfig_t lc = {};
   lc.blockDim = dim3(192);
   lc.dynamicSmemBytes = C::SMEM;
@@ -577,14 +587,14 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   lc.attrs = at;
   lc.numAttrs = 1;
   lc.gridDim = dim3((unsigned)(n_tiles * up.s_count));
-  OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_tiles, n_coarse,
-                               CL > 1 ? 0 : order, up.s_count, cnt, up.s_base));
+  OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_coarse, up.s_count, cnt,
+                               up.s_base, S, so.sub, so.sub_cap, so.cnt_g, so.enable));
 }
 
 template <int NP, bool SPLIT, int EPI>
 void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
                     int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
-                    const Upload& up) {
+                    const Upload& up, const SplitOut& so) {
   // Cluster multicast of the X chunks: on by default for NP > 64, where the X
   // stream through L2 (~6 TB/s) otherwise paces or co-limits the kernel (cfg-4 shape +20%, cfg-3
   // shape +6%; neutral at NP = 64, which is latency-bound); OICA_TC_CL=1|2 overrides.
@@ -597,53 +607,53 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
   constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
   if (NP <= 64 && r192 && cl == 1) {   // small NP: 2 Y slots of 192 samples (OICA_TC_RING=2: 2 x 128)
     launch_cl<NP, SPLIT, EPI, 1, (NP <= 64 ? 3 : 1)>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse,
-                                                    cnt, up);
+                                                    cnt, up, so);
     return;
   }
   const bool r1 = NP <= 128 && rg == 1;
   if (cl == 2 && r1)
-    launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
+    launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
   else if (cl == 2)
-    launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
+    launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
   else if (r1)
-    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
+    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
   else
-    launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
+    launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
 }
 
 template <int NP, bool SPLIT>
 void launch_epi(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up) {
+                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so) {
   static int epi = [] { const char* e = getenv("OICA_TC_EPI"); return e ? atoi(e) : 0; }();
   switch (epi) {
-    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
   }
 }
 
 template <bool SPLIT>
 void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi, const __half* Wlo,
-               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up) {
+               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so) {
   switch (NP) {
-    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 64: launch_epi<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 144: launch_variant<144, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 160: launch_variant<160, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 176: launch_variant<176, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 192: launch_variant<192, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 208: launch_variant<208, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 224: launch_variant<224, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 240: launch_variant<240, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
-    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up); break;
+    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 64: launch_epi<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 144: launch_variant<144, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 160: launch_variant<160, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 176: launch_variant<176, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 192: launch_variant<192, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 208: launch_variant<208, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 224: launch_variant<224, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 240: launch_variant<240, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
   }
 }
@@ -676,14 +686,14 @@ int tc_np(int N) { return (int)round_up(N < 16 ? 16 : N, 16); }
 
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
                    const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
-                   const int* cnt, bool lo_capable, const Upload& up) {
+                   const int* cnt, bool lo_capable, const Upload& up, const SplitOut& so) {
   if (L_act <= 0) return 0;
   static bool force_lo = getenv("OICA_TC_FORCE_LO") != nullptr;   // experiment: LO-capable layout always
   lo_capable = lo_capable || force_lo;
   if (lo_capable || n_coarse < L_act)   // fine rows (possibly): LO-capable layout, 2nd pass from tile n_coarse/128
-    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up);
+    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
   else
-    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0, cnt, up);
+    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0, cnt, up, so);
   return 1;
 }
 

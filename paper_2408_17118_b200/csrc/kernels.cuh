@@ -42,6 +42,13 @@ int launch_step_simt(cudaStream_t st, const float* X, int64_t ld, int64_t M, int
 struct SlotPartials {
   const void* p;
   bool f32;
+  // split-slot parts (f32 only, common.cuh split_parts): when P = split_parts(L_g, S) > 1 the
+  // partial of (slot s, part q, row a) is sub[((s kSplitMax + q) sub_cap + a) ldg + n], q < P;
+  // L_g = *cnt_g (device) or L_g_host (cnt_g null).  sub null: always P = 1.
+  const float* sub = nullptr;
+  int64_t sub_cap = 0;
+  const int* cnt_g = nullptr;
+  int L_g_host = 0;
 };
 // The point the contraction was evaluated at, rows in ACTIVE order (stride NP): the -3w term
 // and the alpha~ identity use it so eq. (5) is evaluated consistently.
@@ -133,13 +140,20 @@ int tc_np(int N);
 // Slot range of one step launch: [s_base, s_base + s_count).  The whole step is one launch over
 // all S slots; while a pipelined host upload is in flight the first step is launched piece by
 // piece (each launch after its piece's copy event), which gives bitwise the same slot partials.
+// Split-slot output of the tensor-core step (see SlotPartials): enable = 0 forces P = 1.
+struct SplitOut {
+  float* sub;
+  int64_t sub_cap;
+  const int* cnt_g;   // global active count (device; null: the host L_act)
+  int enable;
+};
 struct Upload {
   int s_base;
   int s_count;
 };
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
                    const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
-                   const int* cnt, bool lo_capable, const Upload& up);
+                   const int* cnt, bool lo_capable, const Upload& up, const SplitOut& so);
 // fp16 plane columns [m_lo, m_hi) (m_hi < 0: ldx); multiples of 8.
 int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP,
                          int64_t ldx, __half* Xh, int64_t m_lo = 0, int64_t m_hi = -1);

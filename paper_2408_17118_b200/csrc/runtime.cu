@@ -106,6 +106,9 @@ struct oica_ctx {
   int64_t L = 0, Ll = 0, id_base = 0;
   DevBuf<double> W64, alpha_old, Gp, s4p, Gsum, s4sum;
   DevBuf<float> Gp32;   // TC slot partials
+  DevBuf<float> Gsub;   // TC split-slot parts (few active rows, common.cuh split_parts)
+  int64_t sub_cap = 0;
+  DevBuf<int> Lg;       // global active count (lock-step L-shard: all-reduced every iteration)
   DevBuf<float> W32;
   DevBuf<__half> Whi, Wlo;
   DevBuf<int> act0, act1, iters, Lact_dev, hist;
@@ -141,7 +144,11 @@ struct oica_ctx {
   int world() const { return cfg.world; }
   bool tc() const { return precision == OICA_PREC_TC || precision == OICA_PREC_TC_SPLIT; }
   bool split() const { return precision == OICA_PREC_TC_SPLIT; }
-  SlotPartials partials() const { return tc() ? SlotPartials{Gp32.p, true} : SlotPartials{Gp.p, false}; }
+  // slot partials of the last step; cnt_g / L_g: the global active count that chose its split
+  // parts (device pointer, or the host value when null)
+  SlotPartials partials(const int* cnt_g, int L_g) const {
+    return tc() ? SlotPartials{Gp32.p, true, Gsub.p, sub_cap, cnt_g, L_g} : SlotPartials{Gp.p, false};
+  }
   EvalPoint eval_point() const {
     return tc() ? EvalPoint{Whi.p, Wlo.p, nullptr, vNP} : EvalPoint{nullptr, nullptr, W32.p, vNP};
   }
@@ -280,10 +287,14 @@ void ensure_candidate_buffers(oica_ctx* c) {
   c->act0.ensure(Ll);
   c->act1.ensure(Ll);
   c->Lact_dev.ensure(2);
+  c->Lg.ensure(1);
   c->fine.ensure(Ll);
   c->dprev.ensure(Ll);
   if (c->tc()) {
     c->Gp32.ensure((size_t)c->S * Ll * NP);
+    // split parts exist only while round_up(tiles, 2) S <= kSplitTarget / 2 (split_parts)
+    c->sub_cap = std::min<int64_t>(round_up((int64_t)Ll, 128), 128 * std::max(1, kSplitTarget / 2 / c->S));
+    c->Gsub.ensure((size_t)c->S * kSplitMax * c->sub_cap * NP);
     c->Whi.ensure(Ll * NP);
     c->Wlo.ensure(Ll * NP);
   } else {
@@ -301,7 +312,8 @@ void ensure_candidate_buffers(oica_ctx* c) {
   c->csize.ensure(kMaxClusters);
   c->counts.ensure(4);
   c->ups_max.ensure(1);
-  c->nblk_alpha = (int)std::max<int64_t>(1, std::min<int64_t>(4 * c->num_sms, ceil_div(c->M, 4096)));
+  // exact-alpha blocks: enough in flight to stream X at HBM rate (>= ~512 samples per block)
+  c->nblk_alpha = (int)std::max<int64_t>(1, std::min<int64_t>(8 * c->num_sms, ceil_div(c->M, 512)));
   c->part.ensure((size_t)kMaxClusters * c->nblk_alpha);
   c->s4c.ensure(kMaxClusters);
   c->wsum.ensure(kMaxClusters * N);
@@ -334,7 +346,8 @@ void build_operand(oica_ctx* c, const int* act, int cap) {
 // One fused contraction over the active rows (positions 0..L_act-1; rows >= n_coarse are fine)
 // into the slots.  With cnt (device [L_act, n_coarse]) the host values are upper bounds that
 // only size the grid (iterations enqueued without a host round trip).
-void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, bool lo_capable, bool timed) {
+void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* cnt_g, bool lo_capable, bool timed) {
+  const SplitOut so{c->Gsub.p, c->sub_cap, cnt_g, 1};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
     e0 = c->event();
@@ -352,13 +365,13 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, bool lo_capa
       const int s0 = p * spp, s1 = std::min(c->S, s0 + spp);
       if (s1 > s0)
         n += launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
-                            c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{s0, s1 - s0});
+                            c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{s0, s1 - s0}, so);
     }
     sync_x(c);
   } else if (c->tc()) {
     sync_x(c);
     n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
-                       c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, c->S});
+                       c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, c->S}, so);
   } else {
     sync_x(c);
     n = launch_step_simt(c->st, c->vX, c->vld, c->M, c->vN, c->vNP, c->W32.p, L_act, c->slot_len, c->S, kFlush,
@@ -627,7 +640,7 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
       int n = 0;
       if (s_cnt > 0 && tc)
         n = launch_step_tc(st, c->vXh, c->ldx, c->M, NP, tb.Whi.p, tb.Wlo.p, nc_ub, L_ub, slot_len, S_all, tb.Gp32.p, T,
-                           cnt, B > 1 && !c->split(), Upload{s0, s_cnt});
+                           cnt, B > 1 && !c->split(), Upload{s0, s_cnt}, SplitOut{nullptr, 0, nullptr, 0});
       else if (s_cnt > 0)
         n = launch_step_simt(st, c->vX + m0, c->vld, M_r, vN, NP, tb.W32.p, L_ub, slot_len, s_cnt, kFlush, tb.Gp.p,
                              tb.s4p.p, T, cnt);
@@ -765,27 +778,36 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     int L_ub = L_act, nc_ub = n_coarse;
     // OICA_SHARD_HYBRID: the loop runs on the GLOBAL active count (ranks stay in step; a rank
     // without active rows idles) until it falls to hybrid_rows(), then the tail takes over
+    // L-shard with a communicator (and hybrid) runs in lock step on the GLOBAL active count: the
+    // split-slot parts of the step (common.cuh split_parts) depend on it, so every rank needs it
+    // each iteration (one 4-byte all-reduce on the stream); a rank without active rows idles
     const bool hyb = c->hybrid();
+    const bool lockstep = c->collective() && !c->mshard();
     std::vector<int> counts;
     int G_ub = L_ub;
-    auto tail_now = [&]() {
+    auto refresh = [&]() {   // all ranks' counts (host); true: hand the rest to the hybrid tail
       counts = gather_counts(c);
       G_ub = std::accumulate(counts.begin(), counts.end(), 0);
-      return G_ub > 0 && G_ub <= hybrid_rows(c) && t < K;
+      return hyb && G_ub > 0 && G_ub <= hybrid_rows(c) && t < K;
     };
-    if (hyb) OICA_CUDA(cudaMemsetAsync(c->hist.p, 0, sizeof(int) * 2 * ((size_t)K + 1), st));
-    bool to_tail = hyb && tail_now();
-    while (!to_tail && (hyb ? G_ub : L_ub) > 0 && t < K) {
-      const int B = std::min(K - t, ((hyb ? G_ub : L_ub) <= kBatchRows * (hyb ? c->world() : 1) && !c->mshard())
-                                        ? kBatch : 1);
+    if (lockstep) OICA_CUDA(cudaMemsetAsync(c->hist.p, 0, sizeof(int) * 2 * ((size_t)K + 1), st));
+    bool to_tail = lockstep && refresh();
+    while (!to_tail && (lockstep ? G_ub : L_ub) > 0 && t < K) {
+      const int B = std::min(K - t, ((lockstep ? G_ub : L_ub) <= kBatchRows * (lockstep ? c->world() : 1) &&
+                                     !c->mshard()) ? kBatch : 1);
       for (int b = 0; b < B; ++b) {
         ++t;
-        if (L_ub == 0) continue;   // hybrid: this rank idles while others iterate
         const int* cnt = c->Lact_dev.p;
+        const int* cnt_g = cnt;
+        if (lockstep) {
+          OICA_NCCL(Nccl::get().AllReduce(c->Lact_dev.p, c->Lg.p, 1, ncclInt32, ncclSum, c->comm, st));
+          cnt_g = c->Lg.p;
+        }
+        if (L_ub == 0) continue;   // lock step: this rank idles while others iterate
         c->cur_t = t;
-        run_step(c, L_ub, nc_ub, cnt, B > 1 && c->tc() && !c->split(), true);
+        run_step(c, L_ub, nc_ub, cnt, cnt_g, B > 1 && c->tc() && !c->split(), true);
         const bool tc = c->tc();
-        SlotPartials G = c->partials();
+        SlotPartials G = c->partials(cnt_g, L_ub);
         const double* s4 = tc ? nullptr : c->s4p.p;   // TC: alpha~ from the identity w_e . G (K3)
         int S = c->S;
         int64_t cap = c->Ll;
@@ -811,7 +833,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
       OICA_CUDA(cudaStreamSynchronize(st));
       L_ub = ((volatile int*)c->Lact_host)[0];
       nc_ub = ((volatile int*)c->Lact_host)[1];
-      if (hyb) to_tail = tail_now();
+      if (lockstep) to_tail = refresh();
     }
     const int t_bulk = t;
     int64_t tail_active = 0;
@@ -1217,10 +1239,10 @@ oica_status oica_fixed_point_step_mixed(oica_ctx* c, const double* W_dev, int64_
       OICA_CUDA(cudaMemsetAsync(c->fine.p, c->split() ? 1 : 0, L, c->st));   // one precision for all rows
     c->count(launch_compact(c->st, nullptr, c->keep.p, nullptr, (int)L, c->act0.p, c->Lact_dev.p, nullptr));
     build_operand(c, c->act0.p, (int)L);
-    run_step(c, (int)L, n_coarse, nullptr, false, true);
+    run_step(c, (int)L, n_coarse, nullptr, nullptr, false, true);
     account_iteration(c, (int)L, n_coarse);
     bool tc = c->tc();
-    c->count(launch_slot_reduce(c->st, c->partials(), tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L,
+    c->count(launch_slot_reduce(c->st, c->partials(nullptr, (int)L), tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L,
                                 (int)c->N, G_dev, (int)c->N, s4_dev));
     if (tc) c->count(launch_s4_from_g(c->st, c->eval_point(), c->W64.p, G_dev, (int)c->N, (int)L, (int)c->N, s4_dev));
     check_launch();
