@@ -12,28 +12,45 @@ constexpr int kMaxV = 8;  // 256 / 32 coordinates per lane
 
 // v <- v - E v with E = Wacc^T Wacc: all coefficients w_k . v are
 // taken from the incoming v (one projection, as written in the paper).
-__device__ __forceinline__ void project_warp(double (&v)[kMaxV], const double* __restrict__ Wacc, int k,
+template <int V>
+__device__ __forceinline__ void project_warp(double (&v)[V], const double* __restrict__ Wacc, int k,
                                              int N, int lane) {
-  double h[kMaxV];
+  double h[V];
 #pragma unroll
-  for (int u = 0; u < kMaxV; ++u) h[u] = 0.0;
-  for (int r = 0; r < k; ++r) {
-    const double* wr = Wacc + (int64_t)r * N;
-    double c = 0.0;
+  for (int u = 0; u < V; ++u) h[u] = 0.0;
+  // rows in blocks of 8: their 8 loads and 8 warp reductions are independent (latency-bound
+  // otherwise when few rows run); same operations in the same order per row
+  for (int r0 = 0; r0 < k; r0 += 8) {
+    const int nb = min(8, k - r0);
+    double c[8];
 #pragma unroll
-    for (int u = 0; u < kMaxV; ++u) {
-      int n = lane + 32 * u;
-      if (n < N) c += wr[n] * v[u];
+    for (int b = 0; b < 8; ++b) {
+      c[b] = 0.0;
+      if (b < nb) {
+        const double* wr = Wacc + (int64_t)(r0 + b) * N;
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          int n = lane + 32 * u;
+          if (n < N) c[b] += __ldg(wr + n) * v[u];
+        }
+      }
     }
-    c = warp_sum(c);
 #pragma unroll
-    for (int u = 0; u < kMaxV; ++u) {
-      int n = lane + 32 * u;
-      if (n < N) h[u] += c * wr[n];
+    for (int b = 0; b < 8; ++b) c[b] = warp_sum(c[b]);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      if (b < nb) {
+        const double* wr = Wacc + (int64_t)(r0 + b) * N;
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          int n = lane + 32 * u;
+          if (n < N) h[u] += c[b] * __ldg(wr + n);
+        }
+      }
     }
   }
 #pragma unroll
-  for (int u = 0; u < kMaxV; ++u) v[u] -= h[u];
+  for (int u = 0; u < V; ++u) v[u] -= h[u];
 }
 
 __global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_local, int N,
@@ -51,7 +68,7 @@ __global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_loc
     v[u] = 0.0;
     if (n < N) v[u] = candidate_normal(seed, i, l, n);   // A7
   }
-  project_warp(v, Wacc, k, N, lane);
+  project_warp<kMaxV>(v, Wacc, k, N, lane);
   double ss = 0.0;
 #pragma unroll
   for (int u = 0; u < kMaxV; ++u) ss += v[u] * v[u];
@@ -70,24 +87,51 @@ __global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_loc
   }
 }
 
-__device__ __forceinline__ double slot_sum(SlotPartials Gp, int S, int64_t cap, int ldg, int a, int n) {
-  double acc = 0.0;   // fixed slot order
-  if (Gp.f32 && Gp.sub) {   // split-slot parts (common.cuh split_parts): slot-major, part-minor
-    const int P = split_parts(Gp.cnt_g ? Gp.cnt_g[0] : Gp.L_g_host, S);
-    if (P > 1) {
-      for (int s = 0; s < S; ++s)
-        for (int q = 0; q < P; ++q) acc += (double)Gp.sub[(((int64_t)s * kSplitMax + q) * Gp.sub_cap + a) * ldg + n];
-      return acc;
-    }
+// sum_{j < n} v(j) in order j = 0, 1, ... (fp64), loads issued 8 at a time: with few active
+// rows the epilogue is a chain of dependent adds over S (x P) partials, latency-bound otherwise
+template <class F>
+__device__ __forceinline__ double ordered_sum(int n, F&& v) {
+  double acc = 0.0;
+  int j = 0;
+  for (; j + 8 <= n; j += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = v(j + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += t[u];
   }
-  if (Gp.f32) {
-    const float* g = (const float*)Gp.p;
-    for (int s = 0; s < S; ++s) acc += (double)g[((int64_t)s * cap + a) * ldg + n];
-  } else {
-    const double* g = (const double*)Gp.p;
-    for (int s = 0; s < S; ++s) acc += g[((int64_t)s * cap + a) * ldg + n];
-  }
+  for (; j < n; ++j) acc += v(j);
   return acc;
+}
+
+// Partial sum of slot s for element (a, n): the slot's fp32 value, or with split parts (P > 1,
+// common.cuh split_parts) the fp64 sum of its P parts in part order.
+__device__ __forceinline__ double slot_part(const SlotPartials& Gp, int P, int s, int64_t cap, int ldg, int a, int n) {
+  if (P > 1) {
+    const float* g = Gp.sub + (((int64_t)s * kSplitMax) * Gp.sub_cap + a) * ldg + n;
+    const int64_t qs = Gp.sub_cap * ldg;
+    float t[kSplitMax];
+#pragma unroll
+    for (int q = 0; q < kSplitMax; ++q) t[q] = q < P ? __ldg(g + q * qs) : 0.f;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kSplitMax; ++q)
+      if (q < P) acc += (double)t[q];
+    return acc;
+  }
+  if (Gp.f32) return (double)__ldg((const float*)Gp.p + ((int64_t)s * cap + a) * ldg + n);
+  return __ldg((const double*)Gp.p + ((int64_t)s * cap + a) * ldg + n);
+}
+
+__device__ __forceinline__ int parts_of(const SlotPartials& Gp, int S) {
+  return (Gp.f32 && Gp.sub) ? split_parts(Gp.cnt_g ? Gp.cnt_g[0] : Gp.L_g_host, S) : 1;
+}
+
+// sum over slots (fixed slot order) of the slot partial sums: the definition every consumer of
+// the slot partials shares (epilogue, k_slot_reduce), so a row's G is the same whichever runs it
+__device__ __forceinline__ double slot_sum(SlotPartials Gp, int S, int64_t cap, int ldg, int a, int n) {
+  const int P = parts_of(Gp, S);
+  return ordered_sum(S, [&](int s) { return slot_part(Gp, P, s, cap, ldg, a, n); });
 }
 
 // coordinate n of the point the contraction used for active row a (master value w64 if none)
@@ -103,6 +147,7 @@ __device__ __forceinline__ double eval_coord(EvalPoint ev, int a, int n, double 
 // w_e is the operand the contraction was evaluated at (the whole of eq. (5) at
 // one point, so the map keeps its vanishing tangent Jacobian at the fixed points); w_old is
 // the fp64 master row.
+template <int V>
 __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int S, int64_t cap, int ldg,
                            EvalPoint ev, const int* __restrict__ act, int L_act, const double* __restrict__ Wacc,
                            int k, int N, double M, double tol, int t, double* __restrict__ W64,
@@ -113,10 +158,10 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
   if (cnt) L_act = min(L_act, cnt[0]);   // device count when the grid is an upper bound
   if (a >= L_act) return;
   int l = act[a];
-  double g[kMaxV], wo[kMaxV];
+  double g[V], wo[V];
   double s4g = 0.0;
 #pragma unroll
-  for (int u = 0; u < kMaxV; ++u) {
+  for (int u = 0; u < V; ++u) {
     int n = lane + 32 * u;
     double acc = 0.0, w = 0.0, we = 0.0;
     if (n < N) {
@@ -131,19 +176,19 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
   double s4 = 0.0;
   if (s4p) {
     if (lane == 0)
-      for (int s = 0; s < S; ++s) s4 += s4p[(int64_t)s * cap + a];
+      s4 = ordered_sum(S, [&](int s) { return __ldg(s4p + (int64_t)s * cap + a); });
   } else {
     s4 = warp_sum(s4g);   // identity w . sum_m y^3 x = sum_m y^4 (tensor-core path: approximate alpha)
   }
-  project_warp(g, Wacc, k, N, lane);
+  project_warp<V>(g, Wacc, k, N, lane);
   double ss = 0.0;
 #pragma unroll
-  for (int u = 0; u < kMaxV; ++u) ss += g[u] * g[u];
+  for (int u = 0; u < V; ++u) ss += g[u] * g[u];
   double nrm = sqrt(warp_sum(ss));
   bool deg = nrm < kDegenerateNorm;
   double dot = 0.0;
 #pragma unroll
-  for (int u = 0; u < kMaxV; ++u) {
+  for (int u = 0; u < V; ++u) {
     g[u] = deg ? 0.0 : g[u] / nrm;
     dot += g[u] * wo[u];
   }
@@ -151,7 +196,7 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
   double sg = dot < 0.0 ? -1.0 : 1.0;
   double dd = 0.0;
 #pragma unroll
-  for (int u = 0; u < kMaxV; ++u) {
+  for (int u = 0; u < V; ++u) {
     double e = g[u] - sg * wo[u];
     dd += e * e;
   }
@@ -159,7 +204,7 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
   bool conv = !deg && dd <= tol;                          // PAPER.md:249-250 (A2)
   if (!deg) {
 #pragma unroll
-    for (int u = 0; u < kMaxV; ++u) {
+    for (int u = 0; u < V; ++u) {
       int n = lane + 32 * u;
       if (n < N) W64[(int64_t)l * N + n] = g[u];
     }
@@ -250,17 +295,39 @@ __global__ void k_operand_f16x2(const int* __restrict__ act, const int* __restri
   if (Wlo) Wlo[idx] = lo;
 }
 
-__global__ void k_slot_reduce(SlotPartials Gp, const double* __restrict__ s4p, int S, int64_t cap, int ldg, int L,
-                              int N, double* __restrict__ G_out, int ldo, double* __restrict__ s4_out) {
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int a = (int)(idx / (N + 1)), n = (int)(idx % (N + 1));
-  if (a >= L) return;
+// G_out[a][n] = slot_sum(...) and s4_out[a] (fixed slot order), one block per (row, 32
+// coordinates): 8 slot lanes load and part-sum the slots in parallel into shared memory, then
+// one thread per coordinate adds them in slot order (few active rows: the serial chain over
+// S x P partials of one thread was latency-bound)
+constexpr int kRedSlots = 128;
+__global__ void __launch_bounds__(256) k_slot_reduce(SlotPartials Gp, const double* __restrict__ s4p, int S,
+                                                     int64_t cap, int ldg, int L, int N, double* __restrict__ G_out,
+                                                     int ldo, double* __restrict__ s4_out) {
+  __shared__ double T[kRedSlots][33];
+  const int a = blockIdx.x;
+  const int nl = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int n = blockIdx.y * 32 + nl;
+  const bool g_col = n < N, s4_col = n == N && s4p && s4_out;
+  const int P = parts_of(Gp, S);
   double acc = 0.0;
-  if (n < N) {
-    G_out[(int64_t)a * ldo + n] = slot_sum(Gp, S, cap, ldg, a, n);
-  } else if (s4p && s4_out) {
-    for (int s = 0; s < S; ++s) acc += s4p[(int64_t)s * cap + a];
-    s4_out[a] = acc;
+  for (int s0 = 0; s0 < S; s0 += kRedSlots) {
+    const int ns = min(kRedSlots, S - s0);
+    for (int j = sl; j < ns; j += 8) {
+      double v = 0.0;
+      if (g_col)
+        v = slot_part(Gp, P, s0 + j, cap, ldg, a, n);
+      else if (s4_col)
+        v = __ldg(s4p + (int64_t)(s0 + j) * cap + a);
+      T[j][nl] = v;
+    }
+    __syncthreads();
+    if (sl == 0)
+      for (int j = 0; j < ns; ++j) acc += T[j][nl];
+    __syncthreads();
+  }
+  if (sl == 0) {
+    if (g_col) G_out[(int64_t)a * ldo + n] = acc;
+    if (s4_col) s4_out[a] = acc;
   }
 }
 
@@ -293,8 +360,10 @@ int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, 
                     const int* cnt) {
   if (L_act <= 0) return 0;
   int64_t threads = (int64_t)L_act * 32;
-  k_epilogue<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, ev, act, L_act, Wacc, k, N, M,
-                                                               tol, t, W64, alpha_old, iters, state, keep, pr, cnt);
+  // coordinates per lane: only as many as N needs (bitwise the same as the 8-wide loop)
+  auto kern = N <= 32 ? k_epilogue<1> : N <= 64 ? k_epilogue<2> : N <= 128 ? k_epilogue<4> : k_epilogue<kMaxV>;
+  kern<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, ev, act, L_act, Wacc, k, N, M, tol, t,
+                                                         W64, alpha_old, iters, state, keep, pr, cnt);
   return 1;
 }
 
@@ -323,8 +392,8 @@ int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact, int c
 int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, int L,
                        int N, double* G_out, int ldo, double* s4_out) {
   if (L <= 0) return 0;
-  int64_t tot = (int64_t)L * (N + 1);
-  k_slot_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, L, N, G_out, ldo, s4_out);
+  k_slot_reduce<<<dim3((unsigned)L, (unsigned)ceil_div(N + 1, 32)), 256, 0, st>>>(Gp, s4p, S, cap, ldg, L, N, G_out,
+                                                                                  ldo, s4_out);
   return 1;
 }
 

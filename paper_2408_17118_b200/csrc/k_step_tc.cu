@@ -507,8 +507,13 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       if (ok) {
 #pragma unroll
         for (int k = 0; k < 32; ++k)
-          if (NP % 32 == 0 || c + k < NP)   // streaming store: keep the X planes resident in L2
-            __stcs(out + c + k, __uint_as_float(v[k]) * 4096.0f);
+          if (NP % 32 == 0 || c + k < NP) {   // streaming store (keep the X planes in L2), except
+            const float g = __uint_as_float(v[k]) * 4096.0f;   // the few rows of split parts,
+            if (P > 1)                                          // which the epilogue reads next
+              out[c + k] = g;
+            else
+              __stcs(out + c + k, g);
+          }
       }
     }
     if (row < L_act && nchunk == 0 && h == 0)

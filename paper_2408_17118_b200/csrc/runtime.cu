@@ -109,6 +109,7 @@ struct oica_ctx {
   DevBuf<float> Gsub;   // TC split-slot parts (few active rows, common.cuh split_parts)
   int64_t sub_cap = 0;
   DevBuf<int> Lg;       // global active count (lock-step L-shard: all-reduced every iteration)
+  DevBuf<double> Gred, s4red;   // slot-reduced G, s4 of <= kBatchRows rows
   DevBuf<float> W32;
   DevBuf<__half> Whi, Wlo;
   DevBuf<int> act0, act1, iters, Lact_dev, hist;
@@ -288,6 +289,8 @@ void ensure_candidate_buffers(oica_ctx* c) {
   c->act1.ensure(Ll);
   c->Lact_dev.ensure(2);
   c->Lg.ensure(1);
+  c->Gred.ensure((size_t)kBatchRows * NP);
+  c->s4red.ensure(kBatchRows);
   c->fine.ensure(Ll);
   c->dprev.ensure(Ll);
   if (c->tc()) {
@@ -418,9 +421,31 @@ struct PhaseTrace {
             std::to_string(std::chrono::duration<double, std::micro>(t1 - t0).count()).substr(0, 7) + "us";
     t0 = t1;
   }
+  // host time enqueueing iteration batches vs waiting for them (iterate phase)
+  double enq_us = 0.0, wait_us = 0.0;
+  int batches = 0;
+  std::chrono::steady_clock::time_point tb;
+  void batch_begin() {
+    if (on) tb = std::chrono::steady_clock::now();
+  }
+  void batch_enqueued() {
+    if (!on) return;
+    auto t1 = std::chrono::steady_clock::now();
+    enq_us += std::chrono::duration<double, std::micro>(t1 - tb).count();
+    tb = t1;
+  }
+  void batch_done() {
+    if (!on) return;
+    wait_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tb).count();
+    ++batches;
+  }
   void flush(int i) {
-    if (on) fprintf(stderr, "[oica] component %d:%s\n", i, line.c_str());
+    if (on)
+      fprintf(stderr, "[oica] component %d:%s (iterate: %d batches, enqueue %.0fus, wait %.0fus)\n", i, line.c_str(),
+              batches, enq_us, wait_us);
     line.clear();
+    enq_us = wait_us = 0.0;
+    batches = 0;
   }
 };
 
@@ -795,6 +820,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     while (!to_tail && (lockstep ? G_ub : L_ub) > 0 && t < K) {
       const int B = std::min(K - t, ((lockstep ? G_ub : L_ub) <= kBatchRows * (lockstep ? c->world() : 1) &&
                                      !c->mshard()) ? kBatch : 1);
+      trace.batch_begin();
       for (int b = 0; b < B; ++b) {
         ++t;
         const int* cnt = c->Lact_dev.p;
@@ -820,6 +846,14 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
           s4 = tc ? nullptr : c->s4sum.p;
           S = 1;
           cap = c->Ll;
+        } else if (L_ub <= kBatchRows) {
+          // few rows: the S (x P) partial sums of an element are a serial chain; reduce them with
+          // one thread per (row, coordinate) first (same function, same order: bitwise the same)
+          c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, c->vNP, L_ub, vN, c->Gred.p, c->vNP, c->s4red.p));
+          G = SlotPartials{c->Gred.p, false};
+          s4 = tc ? nullptr : c->s4red.p;
+          S = 1;
+          cap = kBatchRows;
         }
         c->count(launch_epilogue(st, G, s4, S, cap, c->vNP, c->eval_point(), act, L_ub, c->Wacc.p, kk, vN,
                                  (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p, c->keep.p,
@@ -830,7 +864,9 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         if (t < K) build_operand(c, act, L_ub);
         check_launch();
       }
+      trace.batch_enqueued();
       OICA_CUDA(cudaStreamSynchronize(st));
+      trace.batch_done();
       L_ub = ((volatile int*)c->Lact_host)[0];
       nc_ub = ((volatile int*)c->Lact_host)[1];
       if (lockstep) to_tail = refresh();
