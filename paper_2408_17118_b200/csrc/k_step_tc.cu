@@ -268,7 +268,10 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const int c_lo = (int)((int64_t)nch_slot * part / P), c_hi = (int)((int64_t)nch_slot * (part + 1) / P);
   const int64_t m_begin = m_slot + (int64_t)c_lo * MT;
   const int nchunk = c_hi - c_lo;
-  const bool lo_pass = SPLIT && tile >= tile_lo0;   // CTA-uniform
+  // idle: the empty partner tile of a cluster (rows >= L_act) only streams its share of the
+  // multicast chunks; it issues no MMA (its commits still release the shared stages)
+  const bool idle = row0 >= L_act;
+  const bool lo_pass = SPLIT && tile >= tile_lo0 && !idle;   // CTA-uniform
 
   constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
   static_assert(CL == 1 || (NP / CL) % 8 == 0, "multicast slices must be whole 8-row swizzle atoms");
@@ -345,7 +348,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const int st = j % C::STAGES, b = j % C::R;
       mbar_wait(&full[st], (j / C::STAGES) & 1);
       tc_fence_after();
-      if (MODE == 5 || MODE == 6) {   // experiment: GEMM2 only / no MMA
+      if (MODE == 5 || MODE == 6 || idle) {   // idle tile; experiments: GEMM2 only / no MMA
         if (elect_one()) tc_commit(&yfull[b]);
         __syncwarp();
         return;
@@ -374,7 +377,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const int st = j % C::STAGES, b = j % C::R;
       mbar_wait(&y3ready[b], (j / C::R) & 1);
       tc_fence_after();
-      if (MODE == 4 || MODE == 6) {   // experiment: GEMM1 only / no MMA
+      if (MODE == 4 || MODE == 6 || idle) {   // idle tile; experiments: GEMM1 only / no MMA
         if (elect_one()) {
           if (CL > 1) tc_commit_mc(&empty[st], kMask); else tc_commit(&empty[st]);
         }
@@ -449,7 +452,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const uint32_t t_y = tmem + lane_off + C::C_Y0 + b * MT;
       mbar_wait(&yfull[b], (j / C::R) & 1);
       tc_fence_after();
-      if (MODE >= 3) {   // experiment: no TMEM traffic (MMA pipeline upper bound)
+      if (MODE >= 3 || idle) {   // idle tile; experiment: no TMEM traffic (MMA pipeline upper bound)
         tc_fence_before();
         mbar_arrive(&y3ready[b]);
         continue;
@@ -500,7 +503,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     float* out = P > 1 ? Gsub + (((int64_t)s * kSplitMax + part) * sub_cap + row) * NP : Gp + ((int64_t)s * cap + row) * NP;
     bool ok = row < L_act && nchunk > 0;
 #pragma unroll 1
-    for (int c = 32 * h; c < NP; c += 32 * NH) {
+    for (int c = 32 * h; c < NP && !idle; c += 32 * NH) {
       uint32_t v[32];
       tmem_ld32(tmem + lane_off + C::C_G + c, v);
       tmem_wait_ld();
@@ -604,7 +607,9 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
   // stream through L2 (~6 TB/s) otherwise paces or co-limits the kernel (cfg-4 shape +20%, cfg-3
   // shape +6%; neutral at NP = 64, which is latency-bound); OICA_TC_CL=1|2 overrides.
   static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
-  const int cl = cl_env ? cl_env : (NP > 64 ? 2 : 1);
+  // one row tile (the tail of a component): no cluster partner, whose CTA would only stream its
+  // half of the chunks in step with the active one (same arithmetic either way)
+  const int cl = cl_env ? cl_env : (NP > 64 && L_act > 128 ? 2 : 1);
   // narrow tiles: 2 Y slots of 128 samples (default) or, OICA_TC_RING=4, 4 slots of 64 samples
   // (measured slower: 7.7 vs 7.0 ms per cfg-3 step, profiles/r01/tc_experiments)
   static int rg = [] { const char* e = getenv("OICA_TC_RING"); return e && atoi(e) == 4 ? 0 : 1; }();

@@ -55,6 +55,7 @@ constexpr double kPromoteRatio = 0.3;       // ... (d > this * d_prev: stagnatin
 constexpr int kPromoteT = 40;               // ... or t >= this
 constexpr int kBatchRows = 2048;            // below this many active rows, iterations are enqueued ...
 constexpr int kBatch = 8;                   // ... this many at a time without a host round trip
+constexpr double kBatchMaxWork = 1e8;       // ... when M x NP is below this (cfg 2: 1.6e7, cfg 3: 1.3e8)
 constexpr int kHybridRowsPerRank = 128;     // OICA_SHARD_HYBRID: tail once global L_act <= this x world
 constexpr int kTailMaxSlots = 1024;
 
@@ -818,8 +819,11 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     if (lockstep) OICA_CUDA(cudaMemsetAsync(c->hist.p, 0, sizeof(int) * 2 * ((size_t)K + 1), st));
     bool to_tail = lockstep && refresh();
     while (!to_tail && (lockstep ? G_ub : L_ub) > 0 && t < K) {
+      // batches only where an iteration is short next to a host round trip (one row tile over
+      // M samples: ~M NP 512 flop); elsewhere the exact count sizes every launch (grid, clusters)
+      const bool short_iter = (double)c->M * (double)c->vNP < kBatchMaxWork;
       const int B = std::min(K - t, ((lockstep ? G_ub : L_ub) <= kBatchRows * (lockstep ? c->world() : 1) &&
-                                     !c->mshard()) ? kBatch : 1);
+                                     !c->mshard() && short_iter) ? kBatch : 1);
       trace.batch_begin();
       for (int b = 0; b < B; ++b) {
         ++t;
