@@ -264,6 +264,10 @@ oica_status oica_complement_basis(const double* W, int32_t k, int32_t N, double*
  * same for any GPU count, tiling or active-set size) and is a multiple of 384 samples; S_local
  * = ceil(M_local / slot_len) slots cover this rank's samples. */
 oica_status oica_slot_plan(int64_t M_global, int64_t M_local, int64_t* slot_len, int32_t* S_local);
+/* Host-only: split-slot parts of the tensor-core step (DESIGN.md §5 "few active rows") when
+ * L_global runs are active over S slots: P in [1, 8] CTAs share each slot's chunks.  A function
+ * of (L_global, S) only; P > 1 only while round_up(ceil(L_global/128), 2) * S <= 148. */
+oica_status oica_split_parts(int32_t L_global, int32_t S, int32_t* P);
 oica_status oica_deflate_basis(double* G, int32_t d, int32_t N, const double* b, double* G_out);
 
 oica_status oica_merge_records(const oica_cluster_record* records, const double* w, int32_t n,

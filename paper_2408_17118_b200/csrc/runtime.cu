@@ -1373,6 +1373,12 @@ oica_status oica_slot_plan(int64_t M_global, int64_t M_local, int64_t* slot_len,
   return OICA_OK;
 }
 
+oica_status oica_split_parts(int32_t L_global, int32_t S, int32_t* P) {
+  if (!P || L_global < 0 || S < 1) return OICA_ERR_INVALID_ARGUMENT;
+  *P = split_parts(L_global, S);
+  return OICA_OK;
+}
+
 oica_status oica_complement_basis(const double* W, int32_t k, int32_t N, double* G) {
   if (!G || N < 1 || N > 4096 || k < 0 || k >= N || (k > 0 && !W)) return OICA_ERR_INVALID_ARGUMENT;
   std::vector<double> g;

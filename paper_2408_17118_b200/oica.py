@@ -100,6 +100,7 @@ SIGNATURES = {
                                      _P(C.c_int64), _P(C.c_uint8)]),
     "oica_complement_basis": (C.c_int, [_P(C.c_double), C.c_int32, C.c_int32, _P(C.c_double)]),
     "oica_slot_plan": (C.c_int, [C.c_int64, C.c_int64, _P(C.c_int64), _P(C.c_int32)]),
+    "oica_split_parts": (C.c_int, [C.c_int32, C.c_int32, _P(C.c_int32)]),
     "oica_deflate_basis": (C.c_int, [_P(C.c_double), C.c_int32, C.c_int32, _P(C.c_double), _P(C.c_double)]),
 }
 
@@ -187,6 +188,13 @@ def slot_plan(M_global, M_local=None):
     ln, S = C.c_int64(), C.c_int32()
     _check(lib().oica_slot_plan(M_global, M_global if M_local is None else M_local, C.byref(ln), C.byref(S)))
     return ln.value, S.value
+
+
+def split_parts(L_global: int, S: int) -> int:
+    """Host-only (oica_split_parts): CTAs sharing each slot's chunks for L_global active runs."""
+    P = C.c_int32()
+    _check(lib().oica_split_parts(L_global, S, C.byref(P)))
+    return P.value
 
 
 def deflate_basis(G, b):

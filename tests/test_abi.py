@@ -108,6 +108,27 @@ def test_deflate_basis_host(N, d):
     assert np.abs(G2.T @ G2 - (G.T @ G - np.outer(w, w))).max() < 1e-12
 
 
+def test_split_parts_host():
+    """Split-slot parts: a function of (global active count, S); never more work units than the
+    launch grid provides (tiles x P <= 296 / S whenever P > 1), non-decreasing as runs leave,
+    and 1 once the row tiles alone fill the GPU."""
+    for S in (1, 2, 7, 30, 61, 128):
+        prev = None
+        for L in list(range(1, 600)) + [1000, 2048, 4096, 16384, 65536]:
+            P = oica.split_parts(L, S)
+            tiles2 = -(-(-(-L // 128)) // 2) * 2
+            assert 1 <= P <= 8
+            if P > 1:
+                assert tiles2 * S <= 148 and tiles2 * S * P <= 296
+            else:
+                assert tiles2 * S > 148 or 296 // (tiles2 * S) <= 1
+            if prev is not None:
+                assert P <= prev
+            prev = P
+    with pytest.raises(oica.OicaError):
+        oica.split_parts(10, 0)
+
+
 @pytest.mark.parametrize("M", [1, 2000, 5003, 20000, 150001, 250000, 1_000_000, 4_000_000, 40_000_000])
 def test_slot_plan_host(M):
     """Slots (the fixed fp32-accumulation units of every row): a function of the global M only,
