@@ -18,13 +18,15 @@ __device__ __forceinline__ void project_warp(double (&v)[V], const double* __res
   double h[V];
 #pragma unroll
   for (int u = 0; u < V; ++u) h[u] = 0.0;
-  // rows in blocks of 8: their 8 loads and 8 warp reductions are independent (latency-bound
-  // otherwise when few rows run); same operations in the same order per row
-  for (int r0 = 0; r0 < k; r0 += 8) {
-    const int nb = min(8, k - r0);
-    double c[8];
+  // rows in blocks of RB: their loads and warp reductions are independent (latency-bound
+  // otherwise when few rows run); same operations in the same order per row.  RB x V bounded
+  // (registers: 8 coordinates per lane already fill them)
+  constexpr int RB = V >= 8 ? 1 : 8 / V;
+  for (int r0 = 0; r0 < k; r0 += RB) {
+    const int nb = min(RB, k - r0);
+    double c[RB];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
+    for (int b = 0; b < RB; ++b) {
       c[b] = 0.0;
       if (b < nb) {
         const double* wr = Wacc + (int64_t)(r0 + b) * N;
@@ -36,9 +38,9 @@ __device__ __forceinline__ void project_warp(double (&v)[V], const double* __res
       }
     }
 #pragma unroll
-    for (int b = 0; b < 8; ++b) c[b] = warp_sum(c[b]);
+    for (int b = 0; b < RB; ++b) c[b] = warp_sum(c[b]);
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
+    for (int b = 0; b < RB; ++b) {
       if (b < nb) {
         const double* wr = Wacc + (int64_t)(r0 + b) * N;
 #pragma unroll
@@ -89,16 +91,16 @@ __global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_loc
 
 // sum_{j < n} v(j) in order j = 0, 1, ... (fp64), loads issued 8 at a time: with few active
 // rows the epilogue is a chain of dependent adds over S (x P) partials, latency-bound otherwise
-template <class F>
+template <int D = 8, class F>
 __device__ __forceinline__ double ordered_sum(int n, F&& v) {
   double acc = 0.0;
   int j = 0;
-  for (; j + 8 <= n; j += 8) {
-    double t[8];
+  for (; j + D <= n; j += D) {
+    double t[D];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = v(j + u);
+    for (int u = 0; u < D; ++u) t[u] = v(j + u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc += t[u];
+    for (int u = 0; u < D; ++u) acc += t[u];
   }
   for (; j < n; ++j) acc += v(j);
   return acc;
@@ -129,9 +131,19 @@ __device__ __forceinline__ int parts_of(const SlotPartials& Gp, int S) {
 
 // sum over slots (fixed slot order) of the slot partial sums: the definition every consumer of
 // the slot partials shares (epilogue, k_slot_reduce), so a row's G is the same whichever runs it
+template <int D = 8>   // loads in flight per call (callers with many coordinates per lane: fewer)
 __device__ __forceinline__ double slot_sum(SlotPartials Gp, int S, int64_t cap, int ldg, int a, int n) {
   const int P = parts_of(Gp, S);
-  return ordered_sum(S, [&](int s) { return slot_part(Gp, P, s, cap, ldg, a, n); });
+  if (P > 1) return ordered_sum<D>(S, [&](int s) { return slot_part(Gp, P, s, cap, ldg, a, n); });
+  // one partial per slot (the common case; the loop the whole-L epilogue streams at HBM rate)
+  if (Gp.f32) {
+    const float* g = (const float*)Gp.p + (int64_t)a * ldg + n;
+    const int64_t st = cap * ldg;
+    return ordered_sum<D>(S, [&](int s) { return (double)g[s * st]; });
+  }
+  const double* g = (const double*)Gp.p + (int64_t)a * ldg + n;
+  const int64_t st = cap * ldg;
+  return ordered_sum<D>(S, [&](int s) { return g[s * st]; });
 }
 
 // coordinate n of the point the contraction used for active row a (master value w64 if none)
@@ -165,7 +177,7 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
     int n = lane + 32 * u;
     double acc = 0.0, w = 0.0, we = 0.0;
     if (n < N) {
-      acc = slot_sum(Gp, S, cap, ldg, a, n);
+      acc = slot_sum<(V >= 8 ? 2 : 8 / V)>(Gp, S, cap, ldg, a, n);
       w = W64[(int64_t)l * N + n];
       we = eval_coord(ev, a, n, w);
     }
