@@ -1,12 +1,9 @@
 #!/bin/bash
-# A/B timing of two liboica builds (dev experiment): ab_libs/liboica_{base,new}.so, alternated twice
+# A/B timing of two liboica builds (dev experiment), alternated twice on one box:
+#   base = ab_libs/base_pkg (a complete older package: binding + library), new = the working tree
 set -u
 mkdir -p gpurun_out
 for r in 1 2; do
-  for v in base new; do
-    cp ab_libs/liboica_$v.so paper_2408_17118_b200/liboica.so
-    echo "== $v run $r"
-    timeout 600 python scripts/tc_variants.py 0 ${AB_SHAPES:-256 128 64} 2>&1 | grep '^{'
-  done
+  echo "== base run $r"; OICA_PKG_ROOT=$PWD/ab_libs/base_pkg timeout 600 python scripts/tc_variants.py 0 ${AB_SHAPES:-256 128 64} 2>&1 | grep '^{'
+  echo "== new run $r"; timeout 600 python scripts/tc_variants.py 0 ${AB_SHAPES:-256 128 64} 2>&1 | grep '^{'
 done
-cp ab_libs/liboica_new.so paper_2408_17118_b200/liboica.so

@@ -20,7 +20,7 @@ for CFG in cfg4_scaling cfg3_large; do
   $CMD > gpurun_out/plain_$CFG.json 2> gpurun_out/plain_$CFG.err && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:oica -c 4000 \
       --csv --log-file gpurun_out/launches_$CFG.csv $CMD > gpurun_out/ncu_list_$CFG.log 2>&1; echo list_$CFG=$?
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step_tc -s 2 -c 1 \
+  timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:k_step_tc -s 2 -c 1 \
       -o /tmp/prof_tc_${CFG}_final $CMD > gpurun_out/ncu_full_$CFG.log 2>&1; echo full_$CFG=$?
   # keep gpurun_out small (64 MiB cap): summaries only
   python scripts/ncu_summary.py full /tmp/prof_tc_${CFG}_final.ncu-rep > gpurun_out/ncu_full_${CFG}_final.json 2>&1

@@ -10,6 +10,6 @@ CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain_cfg4.json 2>/dev/null && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:oica -c 4000 \
     --csv --log-file gpurun_out/launches_cfg4_scaling.csv $CMD > /dev/null 2>&1; echo list=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step_tc -s 2 -c 1 \
+timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:k_step_tc -s 2 -c 1 \
     -o /tmp/prof_tc_cfg4_final $CMD > gpurun_out/ncu_full_cfg4.log 2>&1; echo full=$?
 python scripts/ncu_summary.py full /tmp/prof_tc_cfg4_final.ncu-rep > gpurun_out/ncu_full_cfg4_scaling_final.json 2>&1

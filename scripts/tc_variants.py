@@ -10,7 +10,7 @@ import time
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("OICA_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2408_17118_b200 import oica  # noqa: E402
 
 shapes = {256: (4_000_000, 65536), 128: (1_000_000, 16384), 64: (250_000, 4096)}
