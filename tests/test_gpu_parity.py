@@ -417,6 +417,48 @@ def test_exchange_paths_single_rank(name, precision, shard):
         assert np.array_equal(plain.W, res.W) and np.array_equal(plain.index, res.index)
 
 
+def test_hybrid_tail_from_first_iteration(tmp_path):
+    """OICA_SHARD_HYBRID with OICA_HYBRID_ROWS above L: every iteration runs in the gathered,
+    M-sharded tail (several row tiles, tail slot plan, per-iteration all-reduce over a one-rank
+    communicator); the result meets the oracle gates (subprocess: the threshold is read once)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    cfg, X32, X64 = prepared("p_tc_n128")
+    np.save(tmp_path / "x.npy", X32)
+    code = r"""
+import json, sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2408_17118_b200 import oica
+X32 = np.load(%r)
+seed, L, K, tol, N_out = %d, %d, %d, %r, %d
+with oica.Context(0, oica.PREC_AUTO, rank=0, world=1, shard_mode=oica.SHARD_HYBRID, nccl_id=oica.nccl_unique_id()) as c:
+    c.set_data(torch.from_numpy(X32).cuda())
+    c.init_candidates(seed, L)
+    r = c.extract(N_out, K, tol)
+    st = c.stats()
+json.dump({"W": np.asarray(r.W).tolist(), "index": [int(v) for v in r.index], "alpha": [float(v) for v in r.alpha],
+           "near_tie": [int(v) for v in r.near_tie], "n": int(r.n_extracted), "tail": int(st["tail_iterations"]),
+           "iterations": int(st["iterations"])}, open(%r, "w"))
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), str(tmp_path / "x.npy"), cfg.cand_seed, cfg.L,
+       cfg.K, cfg.tol, cfg.N_out, str(tmp_path / "out.json"))
+    env = dict(os.environ, OICA_HYBRID_ROWS="100000")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.load(open(tmp_path / "out.json"))
+    assert d["tail"] == d["iterations"] > 0   # every iteration ran in the tail
+    W_or, res_or, _ = oracle_run("p_tc_n128")
+    for k in range(d["n"]):
+        if res_or[k].near_tie or d["near_tie"][k]:
+            break
+        assert d["index"][k] == int(res_or[k].index)
+        assert abs(float(np.dot(d["W"][k], W_or[k]))) >= 0.9999
+        assert abs((d["alpha"][k] + 3) - (res_or[k].alpha + 3)) <= 1e-4 * abs(res_or[k].alpha + 3)
+
+
 # ---- shape edge cases: N = 1 and 2 (the feasible set is tiny), N just above a tile width (NP
 # 144 / 256 wide tiles with padding), L below one row tile, M not a multiple of anything
 @pytest.mark.parametrize("N,M,L,N_out,precision", [
