@@ -160,15 +160,13 @@ __device__ __forceinline__ double eval_coord(EvalPoint ev, int a, int n, double 
 // one point, so the map keeps its vanishing tangent Jacobian at the fixed points); w_old is
 // the fp64 master row.
 template <int V>
-__global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int S, int64_t cap, int ldg,
-                           EvalPoint ev, const int* __restrict__ act, int L_act, const double* __restrict__ Wacc,
-                           int k, int N, double M, double tol, int t, double* __restrict__ W64,
-                           double* __restrict__ alpha_old, int* __restrict__ iters, uint8_t* __restrict__ state,
-                           uint8_t* __restrict__ keep, Promotion pr, const int* __restrict__ cnt) {
-  int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  int lane = threadIdx.x & 31;
-  if (cnt) L_act = min(L_act, cnt[0]);   // device count when the grid is an upper bound
-  if (a >= L_act) return;
+__device__ __forceinline__ void epilogue_row(int a, int lane, const SlotPartials& Gp, const double* __restrict__ s4p,
+                                             int S, int64_t cap, int ldg, const EvalPoint& ev,
+                                             const int* __restrict__ act, const double* __restrict__ Wacc, int k,
+                                             int N, double M, double tol, int t, double* __restrict__ W64,
+                                             double* __restrict__ alpha_old, int* __restrict__ iters,
+                                             uint8_t* __restrict__ state, uint8_t* __restrict__ keep,
+                                             const Promotion& pr) {
   int l = act[a];
   double g[V], wo[V];
   double s4g = 0.0;
@@ -233,6 +231,20 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
   }
 }
 
+template <int V>
+__global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int S, int64_t cap, int ldg,
+                           EvalPoint ev, const int* __restrict__ act, int L_act, const double* __restrict__ Wacc,
+                           int k, int N, double M, double tol, int t, double* __restrict__ W64,
+                           double* __restrict__ alpha_old, int* __restrict__ iters, uint8_t* __restrict__ state,
+                           uint8_t* __restrict__ keep, Promotion pr, const int* __restrict__ cnt) {
+  int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int lane = threadIdx.x & 31;
+  if (cnt) L_act = min(L_act, cnt[0]);   // device count when the grid is an upper bound
+  if (a >= L_act) return;
+  epilogue_row<V>(a, lane, Gp, s4p, S, cap, ldg, ev, act, Wacc, k, N, M, tol, t, W64, alpha_old, iters, state, keep,
+                  pr);
+}
+
 // Single-block, order-preserving compaction (deterministic), stably partitioned into coarse
 // rows followed by fine rows.
 __global__ void __launch_bounds__(1024) k_compact(const int* __restrict__ act_in, const uint8_t* __restrict__ keep,
@@ -281,30 +293,98 @@ __global__ void __launch_bounds__(1024) k_compact(const int* __restrict__ act_in
   }
 }
 
+__device__ __forceinline__ void operand_f32_elem(int64_t idx, int a, int n, const int* __restrict__ act,
+                                                 const double* __restrict__ W64, int N, float* __restrict__ W32) {
+  W32[idx] = n < N ? (float)W64[(int64_t)act[a] * N + n] : 0.f;
+}
+
 __global__ void k_operand_f32(const int* __restrict__ act, const int* __restrict__ Lact, int cap,
                               const double* __restrict__ W64, int N, int NP, float* __restrict__ W32) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int a = (int)(idx / NP), n = (int)(idx % NP);
   if (a >= cap || a >= *Lact) return;
-  W32[idx] = n < N ? (float)W64[(int64_t)act[a] * N + n] : 0.f;
+  operand_f32_elem(idx, a, n, act, W64, N, W32);
 }
 
 // Split fp16 operand: w is scaled by 2^4 (|w| <= 1 -> <= 16) so most w_lo stay normal fp16;
 // hi = fp16(2^4 w), lo = fp16(2^4 w - hi).  hi + lo = 2^4 w to ~2^-22 relative (absolute error
 // <= 3e-8 / 16 per coordinate from lo subnormals); both GEMM1 passes share one accumulator.
 // Coarse rows (fine[l] == 0) get lo = 0 (their contraction is the one-pass w_h product).
-__global__ void k_operand_f16x2(const int* __restrict__ act, const int* __restrict__ Lact, int cap,
-                                const double* __restrict__ W64, int N, int NP, const uint8_t* __restrict__ fine,
-                                __half* __restrict__ Whi, __half* __restrict__ Wlo) {
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int a = (int)(idx / NP), n = (int)(idx % NP);
-  if (a >= cap || a >= *Lact) return;
+__device__ __forceinline__ void operand_f16x2_elem(int64_t idx, int a, int n, const int* __restrict__ act,
+                                                   const double* __restrict__ W64, int N,
+                                                   const uint8_t* __restrict__ fine, __half* __restrict__ Whi,
+                                                   __half* __restrict__ Wlo) {
   int l = act[a];
   double w = n < N ? W64[(int64_t)l * N + n] * 16.0 : 0.0;
   __half hi = __double2half(w);
   __half lo = (fine && !fine[l]) ? __double2half(0.0) : __double2half(w - (double)__half2float(hi));
   Whi[idx] = hi;
   if (Wlo) Wlo[idx] = lo;
+}
+
+__global__ void k_operand_f16x2(const int* __restrict__ act, const int* __restrict__ Lact, int cap,
+                                const double* __restrict__ W64, int N, int NP, const uint8_t* __restrict__ fine,
+                                __half* __restrict__ Whi, __half* __restrict__ Wlo) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int a = (int)(idx / NP), n = (int)(idx % NP);
+  if (a >= cap || a >= *Lact) return;
+  operand_f16x2_elem(idx, a, n, act, W64, N, fine, Whi, Wlo);
+}
+
+// Few active rows (<= 32): K3 epilogue (one warp per row), K4 compaction (warp ballots, the
+// same stable coarse-then-fine order as k_compact) and the next iteration's operand gather in
+// one single-block launch instead of three (each of those kernels is a few microseconds of pure
+// latency at this size).  Same per-row arithmetic as k_epilogue.
+template <int V>
+__global__ void __launch_bounds__(1024) k_iter_small(SlotPartials Gp, const double* __restrict__ s4p, int S,
+                                                     int64_t cap, int ldg, EvalPoint ev, const int* __restrict__ act,
+                                                     int L_ub, const double* __restrict__ Wacc, int k, int N,
+                                                     double M, double tol, int t, double* __restrict__ W64,
+                                                     double* __restrict__ alpha_old, int* __restrict__ iters,
+                                                     uint8_t* __restrict__ state, uint8_t* __restrict__ keep,
+                                                     Promotion pr, int* cnt, const uint8_t* __restrict__ fine,
+                                                     int* __restrict__ act_out, int* host_mapped, int* hist,
+                                                     int build, int NP, __half* __restrict__ Whi,
+                                                     __half* __restrict__ Wlo, float* __restrict__ W32) {
+  __shared__ int s_new;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L_in = min(L_ub, cnt[0]);
+  if (warp < L_in)
+    epilogue_row<V>(warp, lane, Gp, s4p, S, cap, ldg, ev, act, Wacc, k, N, M, tol, t, W64, alpha_old, iters, state,
+                    keep, pr);
+  __syncthreads();
+  if (warp == 0) {   // stable partition: kept coarse rows, then kept fine rows (k_compact order)
+    const bool in = lane < L_in && keep[lane];
+    const int id = lane < L_in ? act[lane] : 0;
+    const bool isf = in && fine && fine[id];
+    const unsigned mc = __ballot_sync(0xffffffffu, in && !isf), mf = __ballot_sync(0xffffffffu, isf);
+    const unsigned lt = (1u << lane) - 1u;
+    const int n_coarse = __popc(mc), n_new = n_coarse + __popc(mf);
+    if (in) act_out[isf ? n_coarse + __popc(mf & lt) : __popc(mc & lt)] = id;
+    if (lane == 0) {
+      cnt[0] = n_new;
+      cnt[1] = n_coarse;
+      if (host_mapped) {
+        ((volatile int*)host_mapped)[0] = n_new;
+        ((volatile int*)host_mapped)[1] = n_coarse;
+      }
+      if (hist) {
+        hist[0] = n_new;
+        hist[1] = n_coarse;
+      }
+      s_new = n_new;
+    }
+  }
+  __syncthreads();
+  if (!build) return;
+  const int tot = s_new * NP;
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    const int a = idx / NP, n = idx - a * NP;
+    if (Whi)
+      operand_f16x2_elem(idx, a, n, act_out, W64, N, fine, Whi, Wlo);
+    else
+      operand_f32_elem(idx, a, n, act_out, W64, N, W32);
+  }
 }
 
 // G_out[a][n] = slot_sum(...) and s4_out[a] (fixed slot order), one block per (row, 32
@@ -376,6 +456,18 @@ int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, 
   auto kern = N <= 32 ? k_epilogue<1> : N <= 64 ? k_epilogue<2> : N <= 128 ? k_epilogue<4> : k_epilogue<kMaxV>;
   kern<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, ev, act, L_act, Wacc, k, N, M, tol, t,
                                                          W64, alpha_old, iters, state, keep, pr, cnt);
+  return 1;
+}
+
+int launch_iter_small(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, EvalPoint ev,
+                      const int* act, int L_ub, const double* Wacc, int k, int N, double M, double tol, int t,
+                      double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep, Promotion pr,
+                      int* cnt, const uint8_t* fine, int* act_out, int* host_mapped, int* hist, bool build, int NP,
+                      __half* Whi, __half* Wlo, float* W32) {
+  if (L_ub <= 0) return 0;
+  auto kern = N <= 32 ? k_iter_small<1> : N <= 64 ? k_iter_small<2> : N <= 128 ? k_iter_small<4> : k_iter_small<kMaxV>;
+  kern<<<1, 1024, 0, st>>>(Gp, s4p, S, cap, ldg, ev, act, L_ub, Wacc, k, N, M, tol, t, W64, alpha_old, iters, state,
+                           keep, pr, cnt, fine, act_out, host_mapped, hist, build ? 1 : 0, NP, Whi, Wlo, W32);
   return 1;
 }
 

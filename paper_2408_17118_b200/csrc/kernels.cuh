@@ -75,6 +75,16 @@ int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, 
                     double tol, int t, double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep,
                     Promotion pr, const int* cnt);
 
+// <= 32 active rows: epilogue + compaction (act -> act_out, cnt = [L_act, n_coarse] updated in
+// place, host_mapped / hist as launch_compact) + the next operand rows (build: f16x2 when Whi,
+// else W32) in one single-block launch; same results as the three separate kernels.
+constexpr int kIterSmallRows = 32;
+int launch_iter_small(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, EvalPoint ev,
+                      const int* act, int L_ub, const double* Wacc, int k, int N, double M, double tol, int t,
+                      double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep, Promotion pr,
+                      int* cnt, const uint8_t* fine, int* act_out, int* host_mapped, int* hist, bool build, int NP,
+                      __half* Whi, __half* Wlo, float* W32);
+
 // Fixed-order slot sum into G_out (L x ldo) and s4_out (L).
 int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
                        int L, int N, double* G_out, int ldo, double* s4_out);

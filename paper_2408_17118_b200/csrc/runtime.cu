@@ -859,13 +859,22 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
           S = 1;
           cap = kBatchRows;
         }
-        c->count(launch_epilogue(st, G, s4, S, cap, c->vNP, c->eval_point(), act, L_ub, c->Wacc.p, kk, vN,
-                                 (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p, c->keep.p,
-                                 c->promotion(), cnt));
-        c->count(launch_compact(st, act, c->keep.p, c->fine_flags(), L_ub, act_next, c->Lact_dev.p, c->Lact_host,
-                                cnt, c->hist.p + 2 * t));
-        std::swap(act, act_next);
-        if (t < K) build_operand(c, act, L_ub);
+        if (!c->mshard() && L_ub <= kIterSmallRows) {   // epilogue + compaction + operand: one launch
+          c->count(launch_iter_small(st, G, s4, S, cap, c->vNP, c->eval_point(), act, L_ub, c->Wacc.p, kk, vN,
+                                     (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p,
+                                     c->keep.p, c->promotion(), c->Lact_dev.p, c->fine_flags(), act_next,
+                                     c->Lact_host, c->hist.p + 2 * t, t < K, c->vNP, tc ? c->Whi.p : nullptr,
+                                     tc ? c->Wlo.p : nullptr, tc ? nullptr : c->W32.p));
+          std::swap(act, act_next);
+        } else {
+          c->count(launch_epilogue(st, G, s4, S, cap, c->vNP, c->eval_point(), act, L_ub, c->Wacc.p, kk, vN,
+                                   (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p,
+                                   c->keep.p, c->promotion(), cnt));
+          c->count(launch_compact(st, act, c->keep.p, c->fine_flags(), L_ub, act_next, c->Lact_dev.p, c->Lact_host,
+                                  cnt, c->hist.p + 2 * t));
+          std::swap(act, act_next);
+          if (t < K) build_operand(c, act, L_ub);
+        }
         check_launch();
       }
       trace.batch_enqueued();
