@@ -229,7 +229,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   using C = Cfg<NP, SPLIT, RG>;
   constexpr int MT = C::MT;
   // MODE 0 = the step; timing experiments (scripts/tc_variants.py): 3 = no
-  // epilogue (MMA + data), 4 = GEMM1 only, 5 = GEMM2 only, 6 = no MMA (X streaming only)
+  // epilogue (MMA + data), 4 = GEMM1 only, 5 = GEMM2 only, 6 = no MMA (X streaming only),
+  // 7 = GEMM1 only with an fp16 accumulator
   constexpr int MODE = EPI;
   constexpr int EPI_ARRIVALS = 32 * NW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -335,7 +336,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     // ===== MMA issuer: the whole warp follows the schedule, one elected lane issues =====
     // (warp-uniform operands keep the descriptors in uniform registers: one UTCHMMA + an
     // add per MMA, no per-instruction lane waterfall)
-    constexpr uint32_t id1 = idesc_f16(MT, 1);   // GEMM1: B = X, MN-major (m contiguous)
+    // GEMM1: B = X, MN-major (m contiguous); experiment MODE 7: fp16 accumulator (D format F16)
+    constexpr uint32_t id1 = MODE == 7 ? (idesc_f16(MT, 1) & ~(1u << 4)) : idesc_f16(MT, 1);
     constexpr uint32_t id2 = idesc_f16(NP, 0);   // GEMM2: B = X, K-major (K = m)
     const uint32_t t_g = tmem + C::C_G;
     const uint64_t dx0 = sdesc(smem_u32(s_x), C::XB, 1024);   // X as MN-major B (GEMM1)
@@ -377,7 +379,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const int st = j % C::STAGES, b = j % C::R;
       mbar_wait(&y3ready[b], (j / C::R) & 1);
       tc_fence_after();
-      if (MODE == 4 || MODE == 6 || idle) {   // idle tile; experiments: GEMM1 only / no MMA
+      if (MODE == 4 || MODE == 6 || MODE == 7 || idle) {   // idle tile; experiments: GEMM1 only / no MMA
         if (elect_one()) {
           if (CL > 1) tc_commit_mc(&empty[st], kMask); else tc_commit(&empty[st]);
         }
@@ -640,6 +642,7 @@ void launch_epi(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const
     case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
     case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
     case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 7: launch_variant<NP, SPLIT, 7>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
     default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
   }
 }
