@@ -39,6 +39,8 @@ def test_bench_line_contract():
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["value"] > 0 and c["cores"] >= 1 and c["sample"]
     assert d["gpu_launches"] > 0
+    a = d["all_components"]   # BASELINE metric's "seconds to extract all N"
+    assert d["seconds_all_components"] == a["seconds"] > 0 and a["components"] == 8 and a["value"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
 
 
