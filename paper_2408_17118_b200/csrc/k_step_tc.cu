@@ -230,7 +230,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   constexpr int MT = C::MT;
   // MODE 0 = the step; timing experiments (scripts/tc_variants.py): 3 = no
   // epilogue (MMA + data), 4 = GEMM1 only, 5 = GEMM2 only, 6 = no MMA (X streaming only),
-  // 7 = GEMM1 only with an fp16 accumulator
+  // 7 = GEMM1 only with an fp16 accumulator, 8 = step with an fp16 GEMM1 accumulator read as the
+  // low half of each 32-bit TMEM cell (probe of the 16-bit accumulator layout)
   constexpr int MODE = EPI;
   constexpr int EPI_ARRIVALS = 32 * NW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -337,7 +338,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     // (warp-uniform operands keep the descriptors in uniform registers: one UTCHMMA + an
     // add per MMA, no per-instruction lane waterfall)
     // GEMM1: B = X, MN-major (m contiguous); experiment MODE 7: fp16 accumulator (D format F16)
-    constexpr uint32_t id1 = MODE == 7 ? (idesc_f16(MT, 1) & ~(1u << 4)) : idesc_f16(MT, 1);
+    constexpr uint32_t id1 = (MODE == 7 || MODE == 8) ? (idesc_f16(MT, 1) & ~(1u << 4)) : idesc_f16(MT, 1);
     constexpr uint32_t id2 = idesc_f16(NP, 0);   // GEMM2: B = X, K-major (K = m)
     const uint32_t t_g = tmem + C::C_G;
     const uint64_t dx0 = sdesc(smem_u32(s_x), C::XB, 1024);   // X as MN-major B (GEMM1)
@@ -454,7 +455,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const uint32_t t_y = tmem + lane_off + C::C_Y0 + b * MT;
       mbar_wait(&yfull[b], (j / C::R) & 1);
       tc_fence_after();
-      if (MODE >= 3 || idle) {   // idle tile; experiment: no TMEM traffic (MMA pipeline upper bound)
+      if ((MODE >= 3 && MODE != 8) || idle) {   // idle tile; experiment: no TMEM traffic (MMA pipeline upper bound)
         tc_fence_before();
         mbar_arrive(&y3ready[b]);
         continue;
@@ -487,6 +488,10 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
             for (int k = 0; k < 32; k += 2) {
               // accumulator = 2^4 y 2^-6 = y / 4 (W scaled by 2^4, X by 2^-6)  ->  acc^3 = 2^-6 y^3
+              if (MODE == 8) {   // experiment: fp16 accumulator, read as the low half of each cell
+                v[w][k] = __float_as_uint(__half2float(__ushort_as_half((unsigned short)(v[w][k] & 0xffffu))));
+                v[w][k + 1] = __float_as_uint(__half2float(__ushort_as_half((unsigned short)(v[w][k + 1] & 0xffffu))));
+              }
               const float2 cc = cube2(v[w][k], v[w][k + 1]);
               __half2 hh = __floats2half2_rn(cc.x, cc.y);
               pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
@@ -643,6 +648,7 @@ void launch_epi(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const
     case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
     case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
     case 7: launch_variant<NP, SPLIT, 7>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 8: launch_variant<NP, SPLIT, 8>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
     default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
   }
 }
