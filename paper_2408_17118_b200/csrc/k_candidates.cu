@@ -501,6 +501,21 @@ int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int 
   return 1;
 }
 
+// alpha_old[act[a]] = s4[a] / M - 3 for the runs still active at the cap (rows by position)
+__global__ void k_alpha_refresh(const int* __restrict__ act, const int* __restrict__ cnt, int L_ub,
+                                const double* __restrict__ s4, double M, double* __restrict__ alpha_old) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= min(L_ub, cnt[0])) return;
+  alpha_old[act[a]] = s4[a] / M - 3.0;   // eq. (2) at the final w
+}
+
+int launch_alpha_refresh(cudaStream_t st, const int* act, const int* cnt, int L_ub, const double* s4, double M,
+                         double* alpha_old) {
+  if (L_ub <= 0) return 0;
+  k_alpha_refresh<<<(unsigned)ceil_div(L_ub, 256), 256, 0, st>>>(act, cnt, L_ub, s4, M, alpha_old);
+  return 1;
+}
+
 int launch_s4_from_g(cudaStream_t st, EvalPoint ev, const double* W, const double* G, int ldg, int L, int N,
                      double* s4) {
   if (L <= 0) return 0;

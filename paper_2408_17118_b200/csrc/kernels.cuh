@@ -89,6 +89,10 @@ int launch_iter_small(cudaStream_t st, SlotPartials Gp, const double* s4p, int S
 int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
                        int L, int N, double* G_out, int ldo, double* s4_out);
 
+// alpha_old[act[a]] = s4[a] / M - 3 for a < min(L_ub, cnt[0]).
+int launch_alpha_refresh(cudaStream_t st, const int* act, const int* cnt, int L_ub, const double* s4, double M,
+                         double* alpha_old);
+
 // s4 = w_eval . G (identity sum_m y^3 (w.x) = sum_m y^4), rows by position.
 int launch_s4_from_g(cudaStream_t st, EvalPoint ev, const double* W, const double* G, int ldg, int L, int N,
                      double* s4);

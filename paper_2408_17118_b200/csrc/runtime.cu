@@ -111,6 +111,7 @@ struct oica_ctx {
   int64_t sub_cap = 0;
   DevBuf<int> Lg;       // global active count (lock-step L-shard: all-reduced every iteration)
   DevBuf<double> Gred, s4red;   // slot-reduced G, s4 of <= kBatchRows rows
+  DevBuf<double> Gfin, s4fin;   // final-w forward pass of the runs active at the cap
   DevBuf<float> W32;
   DevBuf<__half> Whi, Wlo;
   DevBuf<int> act0, act1, iters, Lact_dev, hist;
@@ -350,8 +351,9 @@ void build_operand(oica_ctx* c, const int* act, int cap) {
 // One fused contraction over the active rows (positions 0..L_act-1; rows >= n_coarse are fine)
 // into the slots.  With cnt (device [L_act, n_coarse]) the host values are upper bounds that
 // only size the grid (iterations enqueued without a host round trip).
-void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* cnt_g, bool lo_capable, bool timed) {
-  const SplitOut so{c->Gsub.p, c->sub_cap, cnt_g, 1};
+void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* cnt_g, bool lo_capable, bool timed,
+              bool split = true) {
+  const SplitOut so{c->Gsub.p, c->sub_cap, cnt_g, split ? 1 : 0};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
     e0 = c->event();
@@ -550,6 +552,32 @@ void use_reduced_view(oica_ctx* c, int d) {
   c->vN = d;
   c->vNP = npd;
   c->reduced = true;
+}
+
+// alpha_old of the L_fin runs still active (positions act[0..L_fin), count in Lact_dev) at their
+// final w: one step over those rows, s4 = w_e . G (TC identity) or the SIMT s4 partials.
+void refresh_unconverged_alpha(oica_ctx* c, const int* act, int L_fin, int n_coarse, int vN) {
+  cudaStream_t st = c->st;
+  const int* cnt = c->Lact_dev.p;
+  const bool tc = c->tc();
+  c->Gfin.ensure((size_t)c->Ll * c->vNP);
+  c->s4fin.ensure((size_t)c->Ll);
+  build_operand(c, act, L_fin);
+  c->cur_t = 0;
+  // no split-slot parts: they would depend on the global count, which other ranks may not join
+  // here; the plain slot sums make alpha~ of a row the same for any GPU count
+  run_step(c, L_fin, n_coarse, cnt, nullptr, false, false, false);
+  const SlotPartials G = tc ? SlotPartials{c->Gp32.p, true} : SlotPartials{c->Gp.p, false};
+  c->count(launch_slot_reduce(st, G, tc ? nullptr : c->s4p.p, c->S, c->Ll, c->vNP, L_fin, vN, c->Gfin.p, c->vNP,
+                              c->s4fin.p));
+  if (c->mshard()) {
+    auto& nc = Nccl::get();
+    OICA_NCCL(nc.AllReduce(c->Gfin.p, c->Gfin.p, (size_t)L_fin * c->vNP, ncclFloat64, ncclSum, c->comm, st));
+    if (!tc) OICA_NCCL(nc.AllReduce(c->s4fin.p, c->s4fin.p, (size_t)L_fin, ncclFloat64, ncclSum, c->comm, st));
+  }
+  if (tc) c->count(launch_s4_from_g(st, c->eval_point(), c->W64.p, c->Gfin.p, c->vNP, L_fin, vN, c->s4fin.p));
+  c->count(launch_alpha_refresh(st, act, cnt, L_fin, c->s4fin.p, (double)c->Mg, c->alpha_old.p));
+  check_launch();
 }
 
 // Active counts of every rank (hybrid mode): one all-gather of the device counter.
@@ -888,6 +916,11 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     int64_t tail_active = 0;
     std::vector<std::pair<int, int>> rows_at((size_t)K + 2, {0, 0});   // (L_act, n_coarse) entering iteration t
     if (to_tail) tail_active = run_hybrid_tail(c, act, L_ub, counts, t, K, tol, kk, vN, rows_at);
+    // Runs still active at the cap K carry alpha at their previous w (A15 holds only at a fixed
+    // point); where they can be selected (reading A4: no run converged, or
+    // OICA_INCLUDE_UNCONVERGED) rank them by alpha at their final w, as PAPER.md:257-258 does:
+    // one more forward pass over those rows (L-shard / single GPU; M-shard sums ranks).
+    if (!to_tail && L_ub > 0 && t >= K) refresh_unconverged_alpha(c, act, L_ub, nc_ub, vN);
     trace.mark("iterate");
     // per-iteration counts: entering iteration t' the active set had hist[t'-1] rows (t' >= 2)
     std::vector<int> hist(2 * (size_t)(t_bulk + 1), 0);
