@@ -283,6 +283,25 @@ def test_gaussianity_stop_and_flags():
         assert abs(raw.W[0] @ q.W[0]) >= 1 - 1e-6 and raw.cluster_size[0] == 1
 
 
+@pytest.mark.parametrize("name,K", [("p_n40", 4), ("p_tc_n128", 4)])
+def test_include_unconverged_parity(name, K):
+    """OICA_INCLUDE_UNCONVERGED with a small cap K: unconverged runs compete on alpha at their final
+    w.  Teacher-forced on the oracle's prefix (the oracle run with include_unconverged), the
+    selected objective is the oracle's to 1e-3 (unconverged end states are parity-unpinned,
+    SURVEY §8(c)); converged winners match exactly."""
+    cfg, X32, X64 = prepared(name)
+    N_out = min(cfg.N_out, 4)
+    W_or, res_or = ordering.extract(X64, cfg.L, K, cfg.tol, N_out, cfg.cand_seed, include_unconverged=True)
+    with oica.Context(0, oica.PREC_AUTO) as ctx:
+        ctx.set_data(torch.from_numpy(X32).cuda())
+        ctx.init_candidates(cfg.cand_seed, cfg.L)
+        for k in range(N_out):
+            r = ctx.extract(k + 1, K, cfg.tol, flags=oica.INCLUDE_UNCONVERGED, W_prefix=W_or[:k] if k else None)
+            a_g, a_o = r.alpha[k] + 3.0, res_or[k].alpha + 3.0
+            assert abs(a_g - a_o) <= 1e-3 * abs(a_o), (k, r.index[k], res_or[k].index, a_g, a_o)
+            assert int(r.n_converged[k]) + int(r.n_unconverged[k]) + int(r.n_degenerate[k]) == cfg.L
+
+
 def test_argument_errors():
     cfg, ctx = ctx_for("p_tiny")
     for kw in [dict(N_out=cfg.N + 1), dict(N_out=2, max_iter=0), dict(N_out=2, tol=0.0)]:
