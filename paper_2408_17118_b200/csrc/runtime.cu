@@ -720,6 +720,27 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
     L_ub = ((volatile int*)c->Lact_host)[0];
     nc_ub = ((volatile int*)c->Lact_host)[1];
   }
+  if (L_ub > 0) {   // runs capped in the tail: alpha at their final w (A15; identical on every rank)
+    const int* cnt = c->Lact_dev.p;
+    if (tc)
+      c->count(launch_operand_f16x2(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.fine.p, tb.Whi.p, tb.Wlo.p));
+    else
+      c->count(launch_operand_f32(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.W32.p));
+    if (s_cnt > 0 && tc)
+      c->count(launch_step_tc(st, c->vXh, c->ldx, c->M, NP, tb.Whi.p, tb.Wlo.p, nc_ub, L_ub, slot_len, S_all,
+                              tb.Gp32.p, T, cnt, false, Upload{s0, s_cnt}, SplitOut{nullptr, 0, nullptr, 0}));
+    else if (s_cnt > 0)
+      c->count(launch_step_simt(st, c->vX + m0, c->vld, M_r, vN, NP, tb.W32.p, L_ub, slot_len, s_cnt, kFlush, tb.Gp.p,
+                                tb.s4p.p, T, cnt));
+    SlotPartials part = tc ? SlotPartials{tb.Gp32.p + (size_t)s0 * T * NP, true} : SlotPartials{tb.Gp.p, false};
+    c->count(launch_slot_reduce(st, part, tc ? nullptr : tb.s4p.p, s_cnt, T, NP, L_ub, vN, tb.Gsum.p, NP,
+                                tb.s4sum.p));
+    OICA_NCCL(nc.AllReduce(tb.Gsum.p, tb.Gsum.p, (size_t)L_ub * NP, ncclFloat64, ncclSum, c->comm, st));
+    if (!tc) OICA_NCCL(nc.AllReduce(tb.s4sum.p, tb.s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st));
+    if (tc) c->count(launch_s4_from_g(st, ev, tb.W64.p, tb.Gsum.p, NP, L_ub, vN, tb.s4sum.p));
+    c->count(launch_alpha_refresh(st, a_cur, cnt, L_ub, tb.s4sum.p, (double)c->Mg, tb.alpha.p));
+    check_launch();
+  }
   // finished (or capped) runs back to their owners
   c->count(launch_tail_scatter(st, T, tb.ids.p, tb.W64.p, tb.alpha.p, tb.iters.p, tb.state.p, c->id_base, c->Ll, vN,
                                c->W64.p, c->alpha_old.p, c->iters.p, c->state.p));

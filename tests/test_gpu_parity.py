@@ -446,6 +446,10 @@ def test_hybrid_tail_from_first_iteration(tmp_path):
     import sys
     cfg, X32, X64 = prepared("p_tc_n128")
     np.save(tmp_path / "x.npy", X32)
+    # also: runs capped inside the tail (K = 4) compete with OICA_INCLUDE_UNCONVERGED on alpha at
+    # their final w (teacher-forced on the oracle's prefix; objective gate as for K = 1)
+    W_or4, res_or4 = ordering.extract(X64, cfg.L, 4, cfg.tol, 2, cfg.cand_seed, include_unconverged=True)
+    np.save(tmp_path / "w4.npy", W_or4)
     code = r"""
 import json, sys, numpy as np, torch
 sys.path.insert(0, %r)
@@ -457,11 +461,14 @@ with oica.Context(0, oica.PREC_AUTO, rank=0, world=1, shard_mode=oica.SHARD_HYBR
     c.init_candidates(seed, L)
     r = c.extract(N_out, K, tol)
     st = c.stats()
-json.dump({"W": np.asarray(r.W).tolist(), "index": [int(v) for v in r.index], "alpha": [float(v) for v in r.alpha],
+    W4 = np.load(%r)
+    a4 = [float(c.extract(k + 1, 4, tol, flags=oica.INCLUDE_UNCONVERGED, W_prefix=W4[:k] if k else None).alpha[k])
+          for k in range(2)]
+json.dump({"a4": a4, "W": np.asarray(r.W).tolist(), "index": [int(v) for v in r.index], "alpha": [float(v) for v in r.alpha],
            "near_tie": [int(v) for v in r.near_tie], "n": int(r.n_extracted), "tail": int(st["tail_iterations"]),
            "iterations": int(st["iterations"])}, open(%r, "w"))
 """ % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), str(tmp_path / "x.npy"), cfg.cand_seed, cfg.L,
-       cfg.K, cfg.tol, cfg.N_out, str(tmp_path / "out.json"))
+       cfg.K, cfg.tol, cfg.N_out, str(tmp_path / "w4.npy"), str(tmp_path / "out.json"))
     env = dict(os.environ, OICA_HYBRID_ROWS="100000")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
@@ -469,6 +476,8 @@ json.dump({"W": np.asarray(r.W).tolist(), "index": [int(v) for v in r.index], "a
     assert out.returncode == 0, out.stderr[-2000:]
     d = json.load(open(tmp_path / "out.json"))
     assert d["tail"] == d["iterations"] > 0   # every iteration ran in the tail
+    for k in range(2):
+        assert abs((d["a4"][k] + 3) - (res_or4[k].alpha + 3)) <= 1e-3 * abs(res_or4[k].alpha + 3), (k, d["a4"][k])
     W_or, res_or, _ = oracle_run("p_tc_n128")
     for k in range(d["n"]):
         if res_or[k].near_tie or d["near_tie"][k]:
