@@ -210,8 +210,18 @@ __global__ void __launch_bounds__(256) k_alpha_exact(const double* __restrict__ 
 __global__ void k_alpha_reduce(const double* __restrict__ part, int nblk, double* s4c) {
   int c = threadIdx.x;
   if (c >= kMaxClusters) return;
+  // fixed block order; 8 loads in flight (a serial chain of ~500 dependent loads otherwise)
+  const double* p = part + (int64_t)c * nblk;
   double v = 0.0;
-  for (int b = 0; b < nblk; ++b) v += part[(int64_t)c * nblk + b];
+  int b = 0;
+  for (; b + 8 <= nblk; b += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = p[b + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v += t[u];
+  }
+  for (; b < nblk; ++b) v += p[b];
   s4c[c] = v;
 }
 
