@@ -246,48 +246,69 @@ __global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int 
 }
 
 // Single-block, order-preserving compaction (deterministic), stably partitioned into coarse
-// rows followed by fine rows.
+// rows followed by fine rows.  Each thread takes a contiguous run of positions; per-thread counts
+// are scanned with warp shuffles and one warp over the 32 warp totals (3 barriers).
 __global__ void __launch_bounds__(1024) k_compact(const int* __restrict__ act_in, const uint8_t* __restrict__ keep,
                                                   const uint8_t* __restrict__ fine, int L_in, int* __restrict__ act_out,
                                                   int* out_dev, int* host_mapped, const int* cnt_in, int* hist) {
-  __shared__ int sc[1024], sf[1024];
-  int t = threadIdx.x;
+  __shared__ int wc[32], wf[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (cnt_in) L_in = min(L_in, cnt_in[0]);   // may alias out_dev: read before the barrier below
   __syncthreads();
-  int per = (L_in + 1023) / 1024;
-  int b = t * per, e = min(L_in, b + per);
+  const int per = (L_in + 1023) / 1024;
+  const int b = t * per, e = min(L_in, b + per);
   int cc = 0, cf = 0;
   for (int a = b; a < e; ++a) {
     if (!keep[a]) continue;
     int id = act_in ? act_in[a] : a;
     if (fine && fine[id]) ++cf; else ++cc;
   }
-  sc[t] = cc;
-  sf[t] = cf;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    int vc = t >= off ? sc[t - off] : 0, vf = t >= off ? sf[t - off] : 0;
-    __syncthreads();
-    sc[t] += vc;
-    sf[t] += vf;
-    __syncthreads();
+  // inclusive warp scans of (cc, cf)
+  int ic = cc, jf = cf;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int vc = __shfl_up_sync(0xffffffffu, ic, o), vf = __shfl_up_sync(0xffffffffu, jf, o);
+    if (lane >= o) {
+      ic += vc;
+      jf += vf;
+    }
   }
-  const int n_coarse = sc[1023];
-  int pc = sc[t] - cc, pf = n_coarse + sf[t] - cf;
+  if (lane == 31) {
+    wc[w] = ic;
+    wf[w] = jf;
+  }
+  __syncthreads();
+  if (w == 0) {   // exclusive scan of the warp totals
+    int xc = wc[lane], xf = wf[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int vc = __shfl_up_sync(0xffffffffu, xc, o), vf = __shfl_up_sync(0xffffffffu, xf, o);
+      if (lane >= o) {
+        xc += vc;
+        xf += vf;
+      }
+    }
+    wc[lane] = xc;   // inclusive totals through warp `lane`
+    wf[lane] = xf;
+  }
+  __syncthreads();
+  const int n_coarse = wc[31], n_fine = wf[31];
+  const int base_c = (w ? wc[w - 1] : 0) + ic - cc, base_f = (w ? wf[w - 1] : 0) + jf - cf;
+  int pc = base_c, pf = n_coarse + base_f;
   for (int a = b; a < e; ++a) {
     if (!keep[a]) continue;
     int id = act_in ? act_in[a] : a;
     if (fine && fine[id]) act_out[pf++] = id; else act_out[pc++] = id;
   }
-  if (t == 1023) {
-    out_dev[0] = n_coarse + sf[1023];
+  if (t == 0) {
+    out_dev[0] = n_coarse + n_fine;
     out_dev[1] = n_coarse;
     if (host_mapped) {
-      ((volatile int*)host_mapped)[0] = n_coarse + sf[1023];
+      ((volatile int*)host_mapped)[0] = n_coarse + n_fine;
       ((volatile int*)host_mapped)[1] = n_coarse;
     }
     if (hist) {
-      hist[0] = n_coarse + sf[1023];
+      hist[0] = n_coarse + n_fine;
       hist[1] = n_coarse;
     }
   }
@@ -496,8 +517,9 @@ int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact, int c
 int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, int L,
                        int N, double* G_out, int ldo, double* s4_out) {
   if (L <= 0) return 0;
-  k_slot_reduce<<<dim3((unsigned)L, (unsigned)ceil_div(N + 1, 32)), 256, 0, st>>>(Gp, s4p, S, cap, ldg, L, N, G_out,
-                                                                                  ldo, s4_out);
+  const int cols = N + (s4p && s4_out ? 1 : 0);   // coordinates (+ the s4 column when there is one)
+  k_slot_reduce<<<dim3((unsigned)L, (unsigned)ceil_div(cols, 32)), 256, 0, st>>>(Gp, s4p, S, cap, ldg, L, N, G_out,
+                                                                                ldo, s4_out);
   return 1;
 }
 
