@@ -67,7 +67,8 @@ typedef enum {
 
 /* Multi-GPU partitioning.  world == 1 ignores it. */
 typedef enum {
-  OICA_SHARD_L = 0,     /* candidates split over ranks, X replicated, one exchange/component */
+  OICA_SHARD_L = 0,     /* candidates split over ranks, X replicated, one exchange/component; */
+                        /* ranks iterate in lock step (4-byte count all-reduce per iteration) */
   OICA_SHARD_M = 1,     /* samples split over ranks, fp64 allreduce of G, s4 per iteration   */
   OICA_SHARD_HYBRID = 2 /* L-shard until the global active count falls to OICA_HYBRID_ROWS     */
                         /* (env; default 128 x world): the remaining runs are all-gathered,    */
