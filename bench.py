@@ -268,6 +268,8 @@ def run_oica(args, cfg):
     if not args.no_e2e:
         Xh = torch.empty(Xw.shape, dtype=torch.float32, pin_memory=True)
         Xh.copy_(Xw)
+        # one untimed upload: the context's upload buffer, copy stream and events are set up once
+        ctx.set_data_host_ptr(Xh.data_ptr(), cfg.N, M_local, M_local, M_global=cfg.M)
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
