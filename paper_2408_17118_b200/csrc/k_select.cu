@@ -122,6 +122,110 @@ __global__ void k_assign(const double* __restrict__ W64, const double* __restric
   }
 }
 
+// census + all argmax / assign rounds in one single-block launch for small L (the multi-kernel
+// sequence is ~17 launches of a few microseconds each there).  Same decisions as k_census,
+// k_argmax and k_assign: block reductions with the same tie rule, the same refine margin, the same
+// cluster test; q_c = min id and the sizes are order-independent (atomics).
+constexpr int kSelectSmallL = 2048;   // above: the multi-block assign is faster (cfg 2, L = 4096: 250 vs 350 us)
+__global__ void __launch_bounds__(1024) k_select_small(const double* __restrict__ W64,
+                                                       const double* __restrict__ alpha,
+                                                       const uint8_t* __restrict__ state, int L, int N,
+                                                       uint32_t flags, int* counts, int* cluster, double* ups_max,
+                                                       int* pc, int* qc, int* csize) {
+  __shared__ int cnt[4];
+  __shared__ double su[32];
+  __shared__ int sl[32];
+  __shared__ int s_p;
+  __shared__ double s_um;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const bool inc = flags & OICA_INCLUDE_UNCONVERGED;
+  const bool raw = flags & OICA_RAW_ARGMAX;
+  if (tid < 4) cnt[tid] = 0;
+  __syncthreads();
+  int nc = 0, na = 0, nd = 0;
+  for (int l = tid; l < L; l += blockDim.x) {
+    const uint8_t st = state[l];
+    nc += st == ST_CONVERGED;
+    na += st == ST_ACTIVE;
+    nd += st == ST_DEGENERATE;
+    cluster[l] = -1;
+  }
+  atomicAdd(&cnt[0], nc);
+  atomicAdd(&cnt[1], na);
+  atomicAdd(&cnt[2], nd);
+  __syncthreads();
+  const int n_conv = cnt[0];
+  int ndom = 0;
+  for (int l = tid; l < L; l += blockDim.x)
+    if (eligible(state[l], inc, n_conv) && !(alpha[l] > kAlphaFloor)) ++ndom;
+  atomicAdd(&cnt[3], ndom);
+  __syncthreads();
+  if (tid < 4) counts[tid] = cnt[tid];
+  bool done = false;
+  for (int c = 0; c < kMaxClusters; ++c) {
+    if (done) {   // an earlier round found nothing: the remaining records are empty
+      if (tid == 0) { pc[c] = -1; qc[c] = INT32_MAX; csize[c] = 0; }
+      continue;
+    }
+    double thr = -INFINITY;
+    if (c > 0) thr = s_um - fmax(kRefineMarginRel * fabs(s_um), kRefineMarginAbs);
+    double bu = -INFINITY;
+    int bl = INT32_MAX;
+    for (int l = tid; l < L; l += blockDim.x) {
+      if (!eligible(state[l], inc, n_conv) || cluster[l] >= 0) continue;
+      const double u = upsilon_of(alpha[l]);
+      if (!(u > -INFINITY) || u < thr) continue;
+      if (u > bu || (u == bu && l < bl)) { bu = u; bl = l; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u2 = __shfl_xor_sync(0xffffffffu, bu, o);
+      const int l2 = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (u2 > bu || (u2 == bu && l2 < bl)) { bu = u2; bl = l2; }
+    }
+    if (lane == 0) { su[w] = bu; sl[w] = bl; }
+    __syncthreads();
+    if (w == 0) {
+      bu = su[lane];
+      bl = sl[lane];
+      for (int o = 16; o > 0; o >>= 1) {
+        const double u2 = __shfl_xor_sync(0xffffffffu, bu, o);
+        const int l2 = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (u2 > bu || (u2 == bu && l2 < bl)) { bu = u2; bl = l2; }
+      }
+      if (lane == 0) {
+        const bool found = bu > -INFINITY && bl != INT32_MAX;
+        s_p = found ? bl : -1;
+        pc[c] = s_p;
+        qc[c] = INT32_MAX;
+        csize[c] = 0;
+        if (c == 0) {
+          s_um = found ? bu : -INFINITY;
+          *ups_max = s_um;
+        }
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p < 0) {
+      done = true;
+      continue;
+    }
+    for (int l = w; l < L; l += blockDim.x >> 5) {   // one warp per candidate row
+      if (!eligible(state[l], inc, n_conv) || cluster[l] >= 0 || !(alpha[l] > kAlphaFloor)) continue;
+      if (raw && l != p) continue;
+      double d = 0.0;
+      for (int n = lane; n < N; n += 32) d += W64[(int64_t)l * N + n] * W64[(int64_t)p * N + n];
+      d = warp_sum(d);
+      if (1.0 - fabs(d) <= kClusterDelta && lane == 0) {
+        cluster[l] = c;
+        atomicMin(&qc[c], l);
+        atomicAdd(&csize[c], 1);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // acc[c] += sum over this thread's samples of (w_c . x_m)^4 for the first CC rows, y in fp64.
 template <int CC>
 __device__ __forceinline__ void alpha_accumulate(const double (*ws)[256], const float* __restrict__ X, int64_t ld,
@@ -314,13 +418,20 @@ int launch_select_local(cudaStream_t st, const double* W64, const double* alpha_
                         int* counts, double* part, int nblk, double* s4c) {
   (void)iters;
   int launches = 0;
-  k_census<<<1, 1024, 0, st>>>(state, alpha_old, L_local, flags, counts, cluster);
-  ++launches;
-  unsigned ablocks = (unsigned)ceil_div((int64_t)L_local * 32, 256);
-  for (int c = 0; c < kMaxClusters; ++c) {
-    k_argmax<<<1, 1024, 0, st>>>(alpha_old, state, cluster, counts, L_local, id_base, flags, c, ups_max, pc, qc, csize);
-    k_assign<<<ablocks, 256, 0, st>>>(W64, alpha_old, state, cluster, counts, L_local, N, flags, c, pc, qc, csize);
-    launches += 2;
+  if (L_local <= kSelectSmallL) {
+    k_select_small<<<1, 1024, 0, st>>>(W64, alpha_old, state, L_local, N, flags, counts, cluster, ups_max, pc, qc,
+                                       csize);
+    ++launches;
+  } else {
+    k_census<<<1, 1024, 0, st>>>(state, alpha_old, L_local, flags, counts, cluster);
+    ++launches;
+    unsigned ablocks = (unsigned)ceil_div((int64_t)L_local * 32, 256);
+    for (int c = 0; c < kMaxClusters; ++c) {
+      k_argmax<<<1, 1024, 0, st>>>(alpha_old, state, cluster, counts, L_local, id_base, flags, c, ups_max, pc, qc,
+                                   csize);
+      k_assign<<<ablocks, 256, 0, st>>>(W64, alpha_old, state, cluster, counts, L_local, N, flags, c, pc, qc, csize);
+      launches += 2;
+    }
   }
   k_alpha_exact<<<nblk, 256, 0, st>>>(W64, X, ld, M_local, N, pc, qc, flags, part, nblk);
   k_alpha_reduce<<<1, 32, 0, st>>>(part, nblk, s4c);
