@@ -612,7 +612,7 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
                     const Upload& up, const SplitOut& so) {
   // Cluster multicast of the X chunks: on by default for NP > 64, where the X
   // stream through L2 (~6 TB/s) otherwise paces or co-limits the kernel (cfg-4 shape +20%, cfg-3
-  // shape +6%; neutral at NP = 64, which is latency-bound); OICA_TC_CL=1|2 overrides.
+  // shape +6%; neutral at NP = 64, which is latency-bound); OICA_TC_CL=1|2 (|4 at NP = 256) overrides.
   static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
   // one row tile (the tail of a component): no cluster partner, whose CTA would only stream its
   // half of the chunks in step with the active one (same arithmetic either way)
@@ -628,6 +628,12 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
     return;
   }
   const bool r1 = NP <= 128 && rg == 1;
+  if constexpr (NP == 256) {   // experiment (OICA_TC_CL=4): 4-CTA multicast clusters
+    if (cl == 4) {
+      launch_cl<NP, SPLIT, EPI, 4, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
+      return;
+    }
+  }
   if (cl == 2 && r1)
     launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
   else if (cl == 2)
