@@ -616,7 +616,7 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
   static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
   // one row tile (the tail of a component): no cluster partner, whose CTA would only stream its
   // half of the chunks in step with the active one (same arithmetic either way)
-  const int cl = cl_env ? cl_env : (NP > 64 && L_act > 128 ? 2 : 1);
+  const int cl = up.cl ? up.cl : cl_env ? cl_env : (NP > 64 && L_act > 128 ? 2 : 1);
   // narrow tiles: 2 Y slots of 128 samples (default) or, OICA_TC_RING=4, 4 slots of 64 samples
   // (measured slower: 7.7 vs 7.0 ms per cfg-3 step, profiles/r01/tc_experiments)
   static int rg = [] { const char* e = getenv("OICA_TC_RING"); return e && atoi(e) == 4 ? 0 : 1; }();

@@ -164,6 +164,7 @@ struct SplitOut {
 struct Upload {
   int s_base;
   int s_count;
+  int cl = 0;   // cluster size override (0: the default for NP)
 };
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
                    const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,

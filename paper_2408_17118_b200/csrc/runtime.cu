@@ -75,6 +75,8 @@ struct oica_ctx {
   // pipelined host upload (oica_set_data_host): copy + fp16 conversion on a second stream, piece
   // by piece; the tensor-core step of the first iteration waits per piece (DESIGN.md §7 e2e)
   cudaStream_t cst = nullptr;
+  cudaStream_t st2 = nullptr;   // second launch of the mixed-cluster step (run_step)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaEvent_t x_ready_ev = nullptr, st_ev = nullptr;
   std::vector<cudaEvent_t> piece_ev;   // piece p of the upload is on the device (and converted)
   int pieces = 0;
@@ -348,6 +350,14 @@ void build_operand(oica_ctx* c, const int* act, int cap) {
     c->count(launch_operand_f32(c->st, act, c->Lact_dev.p, cap, c->W64.p, c->vN, c->vNP, c->W32.p));
 }
 
+// Mixed 4-/2-CTA cluster launches (run_step), an experiment (OICA_TC_MIXED=1; measured slower
+// than 2-CTA clusters alone, profiles/r01/tc_experiments): NP = 256, >= 64 row tiles.
+bool mixed_clusters(const oica_ctx* c, int L_act) {
+  static const bool on = [] { const char* e = getenv("OICA_TC_MIXED"); return e && atoi(e) == 1; }();
+  static const bool cl_env = getenv("OICA_TC_CL") != nullptr;
+  return on && !cl_env && c->vNP == 256 && c->S >= 10 && L_act >= 64 * 128;
+}
+
 // One fused contraction over the active rows (positions 0..L_act-1; rows >= n_coarse are fine)
 // into the slots.  With cnt (device [L_act, n_coarse]) the host values are upper bounds that
 // only size the grid (iterations enqueued without a host round trip).
@@ -374,6 +384,28 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* c
                             c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{s0, s1 - s0}, so);
     }
     sync_x(c);
+  } else if (c->tc() && mixed_clusters(c, L_act)) {
+    // experiment: 4-CTA multicast clusters (a quarter of the L2 -> SM stream, less power, a higher
+    // clock) fit on only 132 of the 148 SMs (cudaOccupancyMaxActiveClusters: 33 clusters); a
+    // concurrent 2-CTA launch on a second stream takes the slots meant for the other 16 SMs.
+    // Same arithmetic per slot.
+    sync_x(c);
+    static const int sms_b = [] { const char* e = getenv("OICA_TC_MIXED_SMS"); return e ? atoi(e) : 16; }();
+    const int S_b = std::max(1, (int)((int64_t)c->S * sms_b / 148));
+    const int S_a = c->S - S_b;
+    if (!c->st2) {
+      OICA_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+      OICA_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+      OICA_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+    }
+    OICA_CUDA(cudaEventRecord(c->fork_ev, c->st));
+    OICA_CUDA(cudaStreamWaitEvent(c->st2, c->fork_ev, 0));
+    n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len, c->S,
+                       c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, S_a, 4}, so);
+    n += launch_step_tc(c->st2, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len, c->S,
+                        c->Gp32.p, c->Ll, cnt, lo_capable, Upload{S_a, S_b, 2}, so);
+    OICA_CUDA(cudaEventRecord(c->join_ev, c->st2));
+    OICA_CUDA(cudaStreamWaitEvent(c->st, c->join_ev, 0));
   } else if (c->tc()) {
     sync_x(c);
     n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
@@ -1185,6 +1217,12 @@ oica_status oica_destroy(oica_ctx* c) {
   if (c->x_ready_ev) cudaEventDestroy(c->x_ready_ev);
   for (auto e : c->piece_ev) cudaEventDestroy(e);
   if (c->st_ev) cudaEventDestroy(c->st_ev);
+  if (c->st2) {
+    cudaStreamSynchronize(c->st2);
+    cudaStreamDestroy(c->st2);
+  }
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
   return OICA_OK;
