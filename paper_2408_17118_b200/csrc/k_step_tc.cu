@@ -557,6 +557,19 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// current driver context (nullptr if unavailable): the launch attributes are per context
+void cuda_current_context(CUcontext* out) {
+  typedef CUresult (*GetCurFn)(CUcontext*);
+  static GetCurFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return (cudaGetDriverEntryPoint("cuCtxGetCurrent", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) ? (GetCurFn)p : (GetCurFn)nullptr;
+  }();
+  *out = nullptr;
+  if (fn) fn(out);
+}
+
 // 2D fp16 tensor [rows][cols] (row stride ld elements), box [box_rows][64], 128B swizzle
 CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
   CUtensorMap m;
@@ -577,11 +590,20 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
                const Upload& up, const SplitOut& so) {
   using C = Cfg<NP, SPLIT, RG>;
   auto kern = k_step_tc<NP, SPLIT, EPI, CL, RG>;
-  static bool attr = false;
-  if (!attr) {
+  // once per CUDA context the launch runs in (the step may also run in green contexts, runtime.cu)
+  static CUcontext attr_ctx[4] = {};
+  CUcontext cur = nullptr;
+  cuda_current_context(&cur);
+  bool known = false;
+  for (CUcontext k : attr_ctx) known = known || (k == cur && cur != nullptr);
+  if (!known) {
     OICA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     if (CL > 1) OICA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
+    for (CUcontext& k : attr_ctx)
+      if (!k) {
+        k = cur;
+        break;
+      }
   }
   CUtensorMap tx = make_map(Xh, NP, ldx, ldx, NP / CL);
   CUtensorMap tw = tx;

@@ -1,5 +1,6 @@
 // Host runtime and C-ABI of liboica.so: context, memory planner, per-component driver loop,
 // NCCL exchange, whitening eigensolver.  Kernels live in k_*.cu (launch wrappers in kernels.cuh).
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -61,6 +62,61 @@ constexpr int kTailMaxSlots = 1024;
 
 }  // namespace
 
+// Driver entry points for green contexts (SM partitions), resolved at run time.
+struct GreenApi {
+  CUresult (*DeviceGet)(CUdevice*, int) = nullptr;
+  CUresult (*DeviceGetDevResource)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*SmResourceSplitByCount)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned,
+                                     unsigned) = nullptr;
+  CUresult (*ResourceGenerateDesc)(CUdevResourceDesc*, CUdevResource*, unsigned) = nullptr;
+  CUresult (*GreenCtxCreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned) = nullptr;
+  CUresult (*GreenCtxStreamCreate)(CUstream*, CUgreenCtx, unsigned, int) = nullptr;
+  CUresult (*CtxFromGreenCtx)(CUcontext*, CUgreenCtx) = nullptr;
+  CUresult (*CtxGetCurrent)(CUcontext*) = nullptr;
+  CUresult (*CtxSetCurrent)(CUcontext) = nullptr;
+  CUresult (*GreenCtxDestroy)(CUgreenCtx) = nullptr;
+  CUresult (*StreamDestroy)(CUstream) = nullptr;
+  bool ok = false;
+  static GreenApi& get() {
+    static GreenApi a = [] {
+      GreenApi g;
+      auto sym = [](const char* n) -> void* {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        return (cudaGetDriverEntryPoint(n, &p, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess) ? p : nullptr;
+      };
+      g.DeviceGet = (decltype(g.DeviceGet))sym("cuDeviceGet");
+      g.DeviceGetDevResource = (decltype(g.DeviceGetDevResource))sym("cuDeviceGetDevResource");
+      g.SmResourceSplitByCount = (decltype(g.SmResourceSplitByCount))sym("cuDevSmResourceSplitByCount");
+      g.ResourceGenerateDesc = (decltype(g.ResourceGenerateDesc))sym("cuDevResourceGenerateDesc");
+      g.GreenCtxCreate = (decltype(g.GreenCtxCreate))sym("cuGreenCtxCreate");
+      g.GreenCtxStreamCreate = (decltype(g.GreenCtxStreamCreate))sym("cuGreenCtxStreamCreate");
+      g.CtxFromGreenCtx = (decltype(g.CtxFromGreenCtx))sym("cuCtxFromGreenCtx");
+      g.CtxGetCurrent = (decltype(g.CtxGetCurrent))sym("cuCtxGetCurrent");
+      g.CtxSetCurrent = (decltype(g.CtxSetCurrent))sym("cuCtxSetCurrent");
+      g.GreenCtxDestroy = (decltype(g.GreenCtxDestroy))sym("cuGreenCtxDestroy");
+      g.StreamDestroy = (decltype(g.StreamDestroy))sym("cuStreamDestroy");
+      g.ok = g.DeviceGet && g.DeviceGetDevResource && g.SmResourceSplitByCount && g.ResourceGenerateDesc &&
+             g.GreenCtxCreate && g.GreenCtxStreamCreate && g.CtxFromGreenCtx && g.CtxGetCurrent && g.CtxSetCurrent &&
+             g.GreenCtxDestroy && g.StreamDestroy;
+      return g;
+    }();
+    return a;
+  }
+};
+
+// Green-context split of the SMs for the NP = 256 step: partition A (128 SMs)
+// runs 4-CTA multicast clusters, partition B (the other 20) 2-CTA clusters, concurrently.
+struct GreenSplit {
+  bool tried = false, ok = false;
+  CUgreenCtx gA = nullptr, gB = nullptr;
+  CUcontext cA = nullptr, cB = nullptr;
+  CUstream sA = nullptr, sB = nullptr;
+  cudaEvent_t fork = nullptr, jA = nullptr, jB = nullptr;
+  unsigned smA = 0, smB = 0;
+};
+
 struct oica_ctx {
   oica_config cfg{};
   cudaStream_t st = nullptr;
@@ -76,6 +132,7 @@ struct oica_ctx {
   // by piece; the tensor-core step of the first iteration waits per piece (DESIGN.md §7 e2e)
   cudaStream_t cst = nullptr;
   cudaStream_t st2 = nullptr;   // second launch of the mixed-cluster step (run_step)
+  GreenSplit green;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaEvent_t x_ready_ev = nullptr, st_ev = nullptr;
   std::vector<cudaEvent_t> piece_ev;   // piece p of the upload is on the device (and converted)
@@ -350,6 +407,56 @@ void build_operand(oica_ctx* c, const int* act, int cap) {
     c->count(launch_operand_f32(c->st, act, c->Lact_dev.p, cap, c->W64.p, c->vN, c->vNP, c->W32.p));
 }
 
+// Lazily builds the green-context split; false (and never retried) if unavailable.
+bool green_ready(oica_ctx* c) {
+  GreenSplit& g = c->green;
+  if (g.tried) return g.ok;
+  g.tried = true;
+  GreenApi& api = GreenApi::get();
+  if (!api.ok) {
+    if (getenv("OICA_TRACE")) fprintf(stderr, "[oica] green split unavailable: driver entry points\n");
+    return false;
+  }
+  CUdevice dev;
+  CUdevResource sm, grp[1], rem;
+  unsigned nb = 1;
+  static const int smA_env = [] { const char* e = getenv("OICA_GREEN_SMS"); return e ? atoi(e) : 128; }();
+  auto fail_trace = [](const char* what) {
+    if (getenv("OICA_TRACE")) fprintf(stderr, "[oica] green split unavailable: %s\n", what);
+    return false;
+  };
+  if (api.DeviceGet(&dev, c->cfg.device) != CUDA_SUCCESS ||
+      api.DeviceGetDevResource(dev, &sm, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+      api.SmResourceSplitByCount(grp, &nb, &sm, &rem, 0, (unsigned)smA_env) != CUDA_SUCCESS || nb != 1 ||
+      rem.sm.smCount < 2)
+    return fail_trace("SM split");
+  CUdevResourceDesc dA, dB;
+  if (api.ResourceGenerateDesc(&dA, &grp[0], 1) != CUDA_SUCCESS || api.ResourceGenerateDesc(&dB, &rem, 1) != CUDA_SUCCESS ||
+      api.GreenCtxCreate(&g.gA, dA, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      api.GreenCtxCreate(&g.gB, dB, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      api.GreenCtxStreamCreate(&g.sA, g.gA, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+      api.GreenCtxStreamCreate(&g.sB, g.gB, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+      api.CtxFromGreenCtx(&g.cA, g.gA) != CUDA_SUCCESS || api.CtxFromGreenCtx(&g.cB, g.gB) != CUDA_SUCCESS)
+    return fail_trace("green context");
+  OICA_CUDA(cudaEventCreateWithFlags(&g.fork, cudaEventDisableTiming));
+  OICA_CUDA(cudaEventCreateWithFlags(&g.jA, cudaEventDisableTiming));
+  OICA_CUDA(cudaEventCreateWithFlags(&g.jB, cudaEventDisableTiming));
+  g.smA = grp[0].sm.smCount;
+  g.smB = rem.sm.smCount;
+  g.ok = true;
+  if (getenv("OICA_TRACE")) fprintf(stderr, "[oica] green split: %u + %u SMs\n", g.smA, g.smB);
+  return true;
+}
+
+// The green split (an experiment, OICA_TC_GREEN=1): full-size NP = 256 steps.  Measured equal to
+// 2-CTA clusters on all 148 SMs (same clock: the 4-CTA clusters' higher clock came from the 16 SMs
+// they leave idle, not from the smaller L2 stream; profiles/r01/tc_experiments).
+bool green_step(oica_ctx* c, int L_act) {
+  static const bool on = [] { const char* e = getenv("OICA_TC_GREEN"); return e && atoi(e) == 1; }();
+  static const bool cl_env = getenv("OICA_TC_CL") != nullptr;
+  return on && !cl_env && c->vNP == 256 && c->S >= 10 && L_act >= 64 * 128 && green_ready(c);
+}
+
 // Mixed 4-/2-CTA cluster launches (run_step), an experiment (OICA_TC_MIXED=1; measured slower
 // than 2-CTA clusters alone, profiles/r01/tc_experiments): NP = 256, >= 64 row tiles.
 bool mixed_clusters(const oica_ctx* c, int L_act) {
@@ -384,6 +491,31 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* c
                             c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{s0, s1 - s0}, so);
     }
     sync_x(c);
+  } else if (c->tc() && green_step(c, L_act)) {
+    // 4-CTA multicast clusters on a 128-SM partition (a quarter of the L2 -> SM stream: less power,
+    // a higher clock; 4-CTA clusters alone fit on only 132 SMs) and 2-CTA clusters on the other
+    // 20 SMs, concurrently, slots split in proportion.  Same arithmetic per slot.
+    sync_x(c);
+    GreenSplit& g = c->green;
+    GreenApi& api = GreenApi::get();
+    const int S_a = std::min(c->S - 1, std::max(1, (int)std::lround((double)c->S * g.smA / (g.smA + g.smB))));
+    const int S_b = c->S - S_a;
+    OICA_CUDA(cudaEventRecord(g.fork, c->st));
+    OICA_CUDA(cudaStreamWaitEvent((cudaStream_t)g.sA, g.fork, 0));
+    OICA_CUDA(cudaStreamWaitEvent((cudaStream_t)g.sB, g.fork, 0));
+    CUcontext prev = nullptr;
+    api.CtxGetCurrent(&prev);
+    api.CtxSetCurrent(g.cA);
+    n = launch_step_tc((cudaStream_t)g.sA, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act,
+                       c->slot_len, c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, S_a, 4}, so);
+    api.CtxSetCurrent(g.cB);
+    n += launch_step_tc((cudaStream_t)g.sB, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act,
+                        c->slot_len, c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{S_a, S_b, 2}, so);
+    api.CtxSetCurrent(prev);
+    OICA_CUDA(cudaEventRecord(g.jA, (cudaStream_t)g.sA));
+    OICA_CUDA(cudaEventRecord(g.jB, (cudaStream_t)g.sB));
+    OICA_CUDA(cudaStreamWaitEvent(c->st, g.jA, 0));
+    OICA_CUDA(cudaStreamWaitEvent(c->st, g.jB, 0));
   } else if (c->tc() && mixed_clusters(c, L_act)) {
     // experiment: 4-CTA multicast clusters (a quarter of the L2 -> SM stream, less power, a higher
     // clock) fit on only 132 of the 148 SMs (cudaOccupancyMaxActiveClusters: 33 clusters); a
@@ -1222,6 +1354,16 @@ oica_status oica_destroy(oica_ctx* c) {
     cudaStreamDestroy(c->st2);
   }
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->green.ok) {
+    GreenApi& api = GreenApi::get();
+    cudaEventDestroy(c->green.fork);
+    cudaEventDestroy(c->green.jA);
+    cudaEventDestroy(c->green.jB);
+    api.StreamDestroy(c->green.sA);
+    api.StreamDestroy(c->green.sB);
+    api.GreenCtxDestroy(c->green.gA);
+    api.GreenCtxDestroy(c->green.gB);
+  }
   if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
