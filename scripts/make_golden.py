@@ -6,7 +6,7 @@
 Calls only oracle/ and datagen/ (no CUDA path): the stored expected values are the oracle's.
 Inputs: datagen's seeded raw signals on the CPU, whitened by the oracle in fp64 and cast to
 fp32 (the GPU tests rebuild exactly these fp32 values and check the stored SHA-256).
-  tier A: cfg 0 (3 data/candidate seeds), cfg 1 and cfg 2 at full L, all N_out components
+  tier A: cfgs 0 and 1 (3 data/candidate seeds each), cfg 2 at full L, all N_out components
   tier B: cfgs 3 and 4 at full N, M with L' = 256 (candidate ids 0..255: an exact sub-problem),
           the first 8 (cfg 3) / 4 (cfg 4) components
 """
@@ -29,6 +29,8 @@ JOBS = {
     "cfg0_s1": ("cfg0_tiny", 1, None, None),
     "cfg0_s2": ("cfg0_tiny", 2, None, None),
     "cfg1": ("cfg1_artificial", 0, None, None),
+    "cfg1_s1": ("cfg1_artificial", 1, None, None),
+    "cfg1_s2": ("cfg1_artificial", 2, None, None),
     "cfg2": ("cfg2_eeg_shaped", 0, None, None),
     "cfg3_L256": ("cfg3_large", 0, 256, 8),
     "cfg4_L256": ("cfg4_scaling", 0, 256, 4),
