@@ -415,9 +415,11 @@ __global__ void __launch_bounds__(1024) k_iter_small(SlotPartials Gp, const doub
 constexpr int kRedSlots = 128;
 __global__ void __launch_bounds__(256) k_slot_reduce(SlotPartials Gp, const double* __restrict__ s4p, int S,
                                                      int64_t cap, int ldg, int L, int N, double* __restrict__ G_out,
-                                                     int ldo, double* __restrict__ s4_out) {
+                                                     int ldo, double* __restrict__ s4_out, const int* __restrict__ cnt) {
   __shared__ double T[kRedSlots][33];
   const int a = blockIdx.x;
+  // rows beyond the device count hold no partials (and split-part buffers have only sub_cap rows)
+  if (cnt && a >= cnt[0]) return;   // block-uniform
   const int nl = threadIdx.x & 31, sl = threadIdx.x >> 5;
   const int n = blockIdx.y * 32 + nl;
   const bool g_col = n < N, s4_col = n == N && s4p && s4_out;
@@ -515,11 +517,11 @@ int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact, int c
 }
 
 int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, int L,
-                       int N, double* G_out, int ldo, double* s4_out) {
+                       int N, double* G_out, int ldo, double* s4_out, const int* cnt) {
   if (L <= 0) return 0;
   const int cols = N + (s4p && s4_out ? 1 : 0);   // coordinates (+ the s4 column when there is one)
   k_slot_reduce<<<dim3((unsigned)L, (unsigned)ceil_div(cols, 32)), 256, 0, st>>>(Gp, s4p, S, cap, ldg, L, N, G_out,
-                                                                                ldo, s4_out);
+                                                                                ldo, s4_out, cnt);
   return 1;
 }
 

@@ -87,7 +87,7 @@ int launch_iter_small(cudaStream_t st, SlotPartials Gp, const double* s4p, int S
 
 // Fixed-order slot sum into G_out (L x ldo) and s4_out (L).
 int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
-                       int L, int N, double* G_out, int ldo, double* s4_out);
+                       int L, int N, double* G_out, int ldo, double* s4_out, const int* cnt = nullptr);
 
 // alpha_old[act[a]] = s4[a] / M - 3 for a < min(L_ub, cnt[0]).
 int launch_alpha_refresh(cudaStream_t st, const int* act, const int* cnt, int L_ub, const double* s4, double M,

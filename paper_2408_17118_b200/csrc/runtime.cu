@@ -733,7 +733,7 @@ void refresh_unconverged_alpha(oica_ctx* c, const int* act, int L_fin, int n_coa
   run_step(c, L_fin, n_coarse, cnt, nullptr, false, false, false);
   const SlotPartials G = tc ? SlotPartials{c->Gp32.p, true} : SlotPartials{c->Gp.p, false};
   c->count(launch_slot_reduce(st, G, tc ? nullptr : c->s4p.p, c->S, c->Ll, c->vNP, L_fin, vN, c->Gfin.p, c->vNP,
-                              c->s4fin.p));
+                              c->s4fin.p, cnt));
   if (c->mshard()) {
     auto& nc = Nccl::get();
     OICA_NCCL(nc.AllReduce(c->Gfin.p, c->Gfin.p, (size_t)L_fin * c->vNP, ncclFloat64, ncclSum, c->comm, st));
@@ -1055,7 +1055,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         int S = c->S;
         int64_t cap = c->Ll;
         if (c->mshard()) {  // one fp64 allreduce of (G, s4) per iteration; B == 1 here
-          c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, c->vNP, L_ub, vN, c->Gsum.p, c->vNP, c->s4sum.p));
+          c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, c->vNP, L_ub, vN, c->Gsum.p, c->vNP, c->s4sum.p, cnt));
           auto& nc = Nccl::get();
           OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_ub * c->vNP, ncclFloat64, ncclSum, c->comm, st));
           if (!tc) OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st));
@@ -1066,7 +1066,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         } else if (L_ub <= kBatchRows) {
           // few rows: the S (x P) partial sums of an element are a serial chain; reduce them with
           // one thread per (row, coordinate) first (same function, same order: bitwise the same)
-          c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, c->vNP, L_ub, vN, c->Gred.p, c->vNP, c->s4red.p));
+          c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, c->vNP, L_ub, vN, c->Gred.p, c->vNP, c->s4red.p, cnt));
           G = SlotPartials{c->Gred.p, false};
           s4 = tc ? nullptr : c->s4red.p;
           S = 1;
