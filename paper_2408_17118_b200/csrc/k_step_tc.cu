@@ -1,11 +1,13 @@
 // K2a: fused GEMM-cube-GEMM on tcgen05 tensor cores (sm_100a), Y never leaves the SM.
 //
-// For one work unit = (128-row tile of active candidates, split-M slot s) the CTA computes
+// For one work unit = (128-row tile of active candidates, split-M slot s [, part of P when few
+// rows remain: the slot's chunks divided among P CTAs, each with its own fp32 partial, P from
+// the global active count only — common.cuh split_parts]) the CTA computes
 //   Y   = W X_chunk                 GEMM1  (eq. (4))   -> TMEM, fp32
 //   Y3  = y o y o y                  epilogue warps, fp16 A operand written back into TMEM
 //   G  += Y3 X_chunk^T               GEMM2  (eq. (5))   -> TMEM, fp32 accumulator
 // streaming X through shared memory in TMA-loaded chunks, and finally stores G (x 2^12) as the
-// unit's fp64 slot partial Gp[s][row][n].  No atomics: each unit owns its slot region, so the
+// unit's fp32 slot partial Gp[s][row][n] (Gsub for parts).  No atomics: each unit owns its region, so the
 // result of a row is independent of the tile it shares (bitwise-deterministic).
 //
 // Arithmetic (DESIGN.md §5 "precision"): X is rounded once to fp16 (11-bit significand, same
@@ -33,7 +35,8 @@
 // Warp roles: 0 = TMA producer + TMEM allocator, 1 = MMA issuer (one elected lane), 2..5 =
 // epilogue (warp w reaches TMEM lanes 32*(w%4)..+31 = rows of the tile).
 //
-// Cluster multicast (CL = 2, default for NP = 256): the two CTAs of a cluster are two row tiles
+// Cluster multicast (CL = 2, default for NP > 64 unless one row tile remains; an empty partner
+// tile only streams its share and issues no MMA): the two CTAs of a cluster are two row tiles
 // of the same slot, so they stream the same X chunks; each loads half the rows of every chunk
 // and multicasts it to both (one L2 read feeds two SMs), and a stage is refilled only after
 // both CTAs' MMAs released it (the `empty` barrier counts CL commits, multicast by every CTA).

@@ -8,7 +8,7 @@ Inputs: datagen's seeded raw signals on the CPU, whitened by the oracle in fp64 
 fp32 (the GPU tests rebuild exactly these fp32 values and check the stored SHA-256).
   tier A: cfgs 0 and 1 (3 data/candidate seeds each), cfg 2 at full L, all N_out components
   tier B: cfgs 3 and 4 at full N, M with L' = 256 (candidate ids 0..255: an exact sub-problem),
-          the first 8 (cfg 3) / 4 (cfg 4) components
+          all 64 components (cfg 3) / the first 16 (cfg 4)
 """
 from __future__ import annotations
 
@@ -32,8 +32,8 @@ JOBS = {
     "cfg1_s1": ("cfg1_artificial", 1, None, None),
     "cfg1_s2": ("cfg1_artificial", 2, None, None),
     "cfg2": ("cfg2_eeg_shaped", 0, None, None),
-    "cfg3_L256": ("cfg3_large", 0, 256, 8),
-    "cfg4_L256": ("cfg4_scaling", 0, 256, 4),
+    "cfg3_L256": ("cfg3_large", 0, 256, None),   # all 64 components (105 s per 8 on 8 cores)
+    "cfg4_L256": ("cfg4_scaling", 0, 256, 16),   # 16 of 32 components (~90 s each)
 }
 
 
