@@ -156,6 +156,11 @@ PARITY = {
     "p_tc_n256": Config("p_tc_n256", 256, 150_000, 160, 200, 1e-10, 2,
                         (("gg_uniform", 256, 0.5, 1.9),),
                         data_seed=3006, cand_seed=4006),
+    # fp16 range of the tensor-core path: one sparse spike source Bernoulli(1e-4) N(0, 25) (an
+    # EEG-artifact-like source, kappa ~ 3e4) reaches |y| = 242 after whitening at this seed
+    "p_spike": Config("p_spike", 16, 250_000, 256, 200, 1e-10, 3,
+                      (("spikes", 1, 1e-4, 25.0), ("laplace", 7), ("gg_uniform", 8, 0.6, 1.6)),
+                      data_seed=3107, cand_seed=4007),
 }
 
 

@@ -50,7 +50,9 @@ typedef enum {
   OICA_ERR_UNSUPPORTED_DEVICE = 7,    /* device is not compute capability 10.0 (sm_100a)      */
   OICA_ERR_OUT_OF_MEMORY = 8,
   OICA_ERR_CUDA = 9,
-  OICA_ERR_NCCL = 10
+  OICA_ERR_NCCL = 10,
+  OICA_ERR_NONFINITE = 11             /* a candidate update was not finite (non-finite data);  */
+                                      /* the extraction stops instead of dropping the row      */
 } oica_status;
 
 /* Arithmetic of the fixed-point contraction (the two products of PAPER.md:243-245). */
@@ -135,13 +137,18 @@ typedef struct {
                              /* padding and second passes included (row tiles x NP)         */
   int64_t fine_rows;         /* sum over step launches of rows run with the two-pass GEMM1   */
   int64_t tail_iterations;   /* iterations run in the hybrid tail (OICA_SHARD_HYBRID)        */
+  double exchange_ms;        /* CUDA-event time of the NCCL exchanges on the context stream  */
+  int64_t exchange_calls;    /* NCCL collectives issued (0 without a communicator)          */
 } oica_stats;
 
 /* ---- lifetime ---------------------------------------------------------------------- */
 
 /* Create a context on cfg->device.  Fails with OICA_ERR_UNSUPPORTED_DEVICE unless the device
  * is compute capability 10.0.  world > 1 initialises an NCCL communicator from
- * cfg->nccl_unique_id (collective over all ranks). */
+ * cfg->nccl_unique_id (collective over all ranks).  With a communicator every host wait of the
+ * library polls NCCL's asynchronous error state and gives up after OICA_NCCL_TIMEOUT_S seconds
+ * (environment, default 900): the communicator is aborted, the call returns OICA_ERR_NCCL and
+ * the context is usable only for oica_destroy (a dead or absent peer never hangs the caller). */
 oica_status oica_create(const oica_config* cfg, oica_ctx** out);
 oica_status oica_destroy(oica_ctx* ctx);
 const char* oica_status_string(oica_status s);
@@ -167,10 +174,26 @@ oica_status oica_whiten(oica_ctx* ctx, const float* X_dev, int64_t N, int64_t M,
  * 1 <= N <= 256, M_global > N.  Prepares the context-owned operand planes. */
 oica_status oica_set_data(oica_ctx* ctx, const float* Xw_dev, int64_t N, int64_t M_local,
                           int64_t ld, int64_t M_global);
-/* Same with a HOST fp32 source: the library copies it into an owned device buffer
- * (the end-to-end entry point; the copy is part of the call). */
+/* Same with a HOST fp32 source: the library copies it into an owned device buffer (the
+ * end-to-end entry point).  The copy is ENQUEUED, not finished, when the call returns: it runs
+ * on a second stream in pieces of whole slots and the first step of the next extraction starts
+ * on each piece as it lands.  A pageable source may be reused as soon as the
+ * call returns (the CUDA runtime stages it); a PINNED (page-locked) source must stay valid and
+ * unchanged until the next oica_extract_components / oica_synchronize / oica_set_data* call on
+ * this context returns. */
 oica_status oica_set_data_host(oica_ctx* ctx, const float* Xw_host, int64_t N, int64_t M_local,
                                int64_t ld, int64_t M_global);
+
+/* C3: distribute whitened data from rank `root` to every rank (collective; every
+ * rank passes the same N, M_global, root).  X_root: root's device fp32 N x M_global (stride
+ * ld_root), ignored on the other ranks (may be NULL there).  X_out: this rank's device buffer,
+ * N x M_local with stride ld_out >= M_local, where M_local = M_global for OICA_SHARD_L / HYBRID
+ * (X replicated: one ncclBroadcast, or one per row when a stride is not M_global; on root X_out
+ * may equal X_root) and the samples [rank M/world, (rank+1) M/world) for OICA_SHARD_M (root sends
+ * every rank its columns, row by row, with ncclSend/ncclRecv).  Without a communicator it is a
+ * device copy.  Synchronous.  The result is what oica_set_data then borrows. */
+oica_status oica_distribute_data(oica_ctx* ctx, const float* X_root, int64_t N, int64_t M_global, int64_t ld_root,
+                                 float* X_out, int64_t ld_out, int32_t root);
 
 /* Fix the candidate generator (seed) and the global candidate count L (PAPER.md:126, :136,
  * :237; readings A7/A8).  Candidates are drawn afresh for every component from the

@@ -1,9 +1,14 @@
 """Build liboica.so in-tree with nvcc for sm_100a (B200).
 
-    python -m paper_2408_17118_b200.build [--force] [-j N]
+    python -m paper_2408_17118_b200.build [--force] [-j N] [--experiments]
 
 Every .cu under csrc/ is compiled with -gencode arch=compute_100a,code=sm_100a (the 'a'
 target is required for tcgen05) and linked into paper_2408_17118_b200/liboica.so.
+`--experiments` builds a separate liboica_exp.so with -DOICA_EXPERIMENTS: the timing variants
+of DESIGN.md §7 (modes that skip work, cluster / ring / slot / promotion overrides read from
+OICA_* environment variables).  The product library never contains them; the experiment
+library is loaded only when OICA_LIB points at it (scripts/tc_variants.py), and bench.py
+refuses to run with OICA_LIB set.
 """
 from __future__ import annotations
 
@@ -20,6 +25,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build", "oica")
 LIB = os.path.join(HERE, "liboica.so")
+LIB_EXP = os.path.join(HERE, "liboica_exp.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -45,21 +51,24 @@ def _stale(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, jobs: int = 8, verbose: bool = False, experiments: bool = False) -> str:
+    bdir = BUILD + ("_exp" if experiments else "")
+    out = LIB_EXP if experiments else LIB
+    extra = ["-DOICA_EXPERIMENTS"] if experiments else []
+    os.makedirs(bdir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     cc = nvcc()
     objs = []
     todo = []
     for s in srcs:
-        o = os.path.join(BUILD, os.path.basename(s) + ".o")
+        o = os.path.join(bdir, os.path.basename(s) + ".o")
         objs.append(o)
         if force or _stale(o, _deps(s)):
             todo.append((s, o))
 
     def comp(so):
         s, o = so
-        cmd = [cc, *ARCH, *FLAGS, "-c", s, "-o", o]
+        cmd = [cc, *ARCH, *FLAGS, *extra, "-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {os.path.basename(s)}:\n{r.stderr}")
@@ -69,12 +78,12 @@ def build(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
         for s, err in ex.map(comp, todo):
             if verbose and err.strip():
                 print(f"[{os.path.basename(s)}]\n{err}", file=sys.stderr)
-    if todo or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [cc, *ARCH, "-shared", "-o", LIB, *objs, "-ldl"]
+    if todo or not os.path.exists(out) or any(os.path.getmtime(o) > os.path.getmtime(out) for o in objs):
+        cmd = [cc, *ARCH, "-shared", "-o", out, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
@@ -82,5 +91,6 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", type=int, default=8)
     ap.add_argument("-v", action="store_true")
+    ap.add_argument("--experiments", action="store_true", help="build liboica_exp.so with -DOICA_EXPERIMENTS")
     a = ap.parse_args()
-    print(build(a.force, a.j, a.v))
+    print(build(a.force, a.j, a.v, a.experiments))

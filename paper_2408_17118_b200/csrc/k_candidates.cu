@@ -195,7 +195,10 @@ __device__ __forceinline__ void epilogue_row(int a, int lane, const SlotPartials
 #pragma unroll
   for (int u = 0; u < V; ++u) ss += g[u] * g[u];
   double nrm = sqrt(warp_sum(ss));
-  bool deg = nrm < kDegenerateNorm;
+  // a non-finite update (fp16 range failure, non-finite data) retires the row and is reported
+  // (Promotion::nonfinite): it must neither keep iterating to the cap nor enter the argmax
+  const bool bad = !isfinite(nrm);
+  bool deg = bad || nrm < kDegenerateNorm;
   double dot = 0.0;
 #pragma unroll
   for (int u = 0; u < V; ++u) {
@@ -220,6 +223,7 @@ __device__ __forceinline__ void epilogue_row(int a, int lane, const SlotPartials
     }
   }
   if (lane == 0) {
+    if (bad && pr.nonfinite) atomicAdd(pr.nonfinite, 1);
     iters[l] = t;
     alpha_old[l] = s4 / M - 3.0;                          // eq. (2) at w_old (A15)
     state[l] = deg ? ST_DEGENERATE : (conv ? ST_CONVERGED : ST_ACTIVE);

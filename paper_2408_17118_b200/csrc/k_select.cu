@@ -22,8 +22,12 @@ __device__ __forceinline__ bool eligible(uint8_t st, bool include_unconv, int n_
 }
 
 // counts: [0] converged, [1] unconverged (active), [2] degenerate, [3] domain-excluded eligible
+// nconv_g (device, may be null): the converged count over ALL ranks (L-shard): reading A4's
+// "no run converged" fallback must be decided globally, or a rank whose runs all missed the cap
+// would submit unconverged records that a single GPU would have excluded (GPU-count invariance)
 __global__ void __launch_bounds__(1024) k_census(const uint8_t* __restrict__ state, const double* __restrict__ alpha,
-                                                 int L, uint32_t flags, int* counts, int* cluster) {
+                                                 int L, uint32_t flags, int* counts, int* cluster,
+                                                 const int* __restrict__ nconv_g) {
   __shared__ int c[4];
   if (threadIdx.x < 4) c[threadIdx.x] = 0;
   __syncthreads();
@@ -40,9 +44,10 @@ __global__ void __launch_bounds__(1024) k_census(const uint8_t* __restrict__ sta
   atomicAdd(&c[2], nd);
   __syncthreads();
   bool inc = flags & OICA_INCLUDE_UNCONVERGED;
+  const int n_conv = nconv_g ? *nconv_g : c[0];
   int ndom = 0;
   for (int l = threadIdx.x; l < L; l += blockDim.x)
-    if (eligible(state[l], inc, c[0]) && !(alpha[l] > kAlphaFloor)) ++ndom;
+    if (eligible(state[l], inc, n_conv) && !(alpha[l] > kAlphaFloor)) ++ndom;
   atomicAdd(&c[3], ndom);
   __syncthreads();
   if (threadIdx.x < 4) counts[threadIdx.x] = c[threadIdx.x];
@@ -51,11 +56,11 @@ __global__ void __launch_bounds__(1024) k_census(const uint8_t* __restrict__ sta
 __global__ void __launch_bounds__(1024) k_argmax(const double* __restrict__ alpha, const uint8_t* __restrict__ state,
                                                  const int* __restrict__ cluster, const int* __restrict__ counts, int L,
                                                  int64_t id_base, uint32_t flags, int c, double* ups_max, int* pc,
-                                                 int* qc, int* csize) {
+                                                 int* qc, int* csize, const int* __restrict__ nconv_g) {
   __shared__ double su[32];
   __shared__ int sl[32];
   bool inc = flags & OICA_INCLUDE_UNCONVERGED;
-  int n_conv = counts[0];
+  int n_conv = nconv_g ? *nconv_g : counts[0];
   double thr = -INFINITY;
   if (c > 0) {
     double um = *ups_max;
@@ -104,13 +109,14 @@ __global__ void __launch_bounds__(1024) k_argmax(const double* __restrict__ alph
 
 __global__ void k_assign(const double* __restrict__ W64, const double* __restrict__ alpha,
                          const uint8_t* __restrict__ state, int* __restrict__ cluster, const int* __restrict__ counts,
-                         int L, int N, uint32_t flags, int c, const int* __restrict__ pc, int* qc, int* csize) {
+                         int L, int N, uint32_t flags, int c, const int* __restrict__ pc, int* qc, int* csize,
+                         const int* __restrict__ nconv_g) {
   int l = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   int lane = threadIdx.x & 31;
   int p = pc[c];
   if (p < 0 || l >= L) return;
   bool inc = flags & OICA_INCLUDE_UNCONVERGED;
-  if (!eligible(state[l], inc, counts[0]) || cluster[l] >= 0 || !(alpha[l] > kAlphaFloor)) return;
+  if (!eligible(state[l], inc, nconv_g ? *nconv_g : counts[0]) || cluster[l] >= 0 || !(alpha[l] > kAlphaFloor)) return;
   if ((flags & OICA_RAW_ARGMAX) && l != p) return;   // raw argmax: singleton records
   double d = 0.0;
   for (int n = lane; n < N; n += 32) d += W64[(int64_t)l * N + n] * W64[(int64_t)p * N + n];
@@ -131,7 +137,7 @@ __global__ void __launch_bounds__(1024) k_select_small(const double* __restrict_
                                                        const double* __restrict__ alpha,
                                                        const uint8_t* __restrict__ state, int L, int N,
                                                        uint32_t flags, int* counts, int* cluster, double* ups_max,
-                                                       int* pc, int* qc, int* csize) {
+                                                       int* pc, int* qc, int* csize, const int* __restrict__ nconv_g) {
   __shared__ int cnt[4];
   __shared__ double su[32];
   __shared__ int sl[32];
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(1024) k_select_small(const double* __restrict_
   atomicAdd(&cnt[1], na);
   atomicAdd(&cnt[2], nd);
   __syncthreads();
-  const int n_conv = cnt[0];
+  const int n_conv = nconv_g ? *nconv_g : cnt[0];
   int ndom = 0;
   for (int l = tid; l < L; l += blockDim.x)
     if (eligible(state[l], inc, n_conv) && !(alpha[l] > kAlphaFloor)) ++ndom;
@@ -332,7 +338,8 @@ __global__ void k_alpha_reduce(const double* __restrict__ part, int nblk, double
 __global__ void k_finish(const double* __restrict__ W64, const int* __restrict__ iters, const int* __restrict__ counts,
                          const int* __restrict__ pc, const int* __restrict__ qc, const int* __restrict__ csize,
                          const double* __restrict__ s4c, int64_t id_base, int N, double M, uint32_t flags,
-                         int64_t sum_active, int n_iter, RankSummary* sum, double* wsum) {
+                         int64_t sum_active, int n_iter, const int* __restrict__ nonfinite, RankSummary* sum,
+                         double* wsum) {
   bool raw = flags & OICA_RAW_ARGMAX;
   for (int idx = threadIdx.x; idx < kMaxClusters * N; idx += blockDim.x) {
     int c = idx / N, n = idx % N;
@@ -361,6 +368,7 @@ __global__ void k_finish(const double* __restrict__ W64, const int* __restrict__
     sum->n_domain = counts[3];
     sum->sum_active = sum_active;
     sum->n_iter = n_iter;
+    sum->n_nonfinite = nonfinite ? *nonfinite : 0;
   }
 }
 
@@ -379,6 +387,7 @@ __global__ void k_merge_accept(const RankSummary* __restrict__ all, const double
     r.n_deg += all[rk].n_deg;
     r.n_domain += all[rk].n_domain;
     r.sum_active += all[rk].sum_active;
+    r.n_nonfinite += all[rk].n_nonfinite;
     r.n_iter = max(r.n_iter, all[rk].n_iter);
   }
   MergeOut m = merge_records(recs, wall, n, N, group, flags & OICA_RAW_ARGMAX, kClusterDelta, kNearTieRel);
@@ -410,26 +419,45 @@ __global__ void k_merge_accept(const RankSummary* __restrict__ all, const double
   *out = r;
 }
 
+// out[0] = number of converged candidates on this rank (summed over ranks by the caller)
+__global__ void __launch_bounds__(1024) k_count_converged(const uint8_t* __restrict__ state, int L, int* out) {
+  __shared__ int c;
+  if (threadIdx.x == 0) c = 0;
+  __syncthreads();
+  int n = 0;
+  for (int l = threadIdx.x; l < L; l += blockDim.x) n += state[l] == ST_CONVERGED;
+  n = __reduce_add_sync(0xffffffffu, n);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&c, n);
+  __syncthreads();
+  if (threadIdx.x == 0) *out = c;
+}
+
 }  // namespace
+
+int launch_count_converged(cudaStream_t st, const uint8_t* state, int L, int* out) {
+  k_count_converged<<<1, 1024, 0, st>>>(state, L, out);
+  return 1;
+}
 
 int launch_select_local(cudaStream_t st, const double* W64, const double* alpha_old, const uint8_t* state,
                         const int* iters, int L_local, int64_t id_base, int N, uint32_t flags, const float* X,
                         int64_t ld, int64_t M_local, int* cluster, int* pc, int* qc, int* csize, double* ups_max,
-                        int* counts, double* part, int nblk, double* s4c) {
+                        int* counts, double* part, int nblk, double* s4c, const int* nconv_g) {
   (void)iters;
   int launches = 0;
   if (L_local <= kSelectSmallL) {
     k_select_small<<<1, 1024, 0, st>>>(W64, alpha_old, state, L_local, N, flags, counts, cluster, ups_max, pc, qc,
-                                       csize);
+                                       csize, nconv_g);
     ++launches;
   } else {
-    k_census<<<1, 1024, 0, st>>>(state, alpha_old, L_local, flags, counts, cluster);
+    k_census<<<1, 1024, 0, st>>>(state, alpha_old, L_local, flags, counts, cluster, nconv_g);
     ++launches;
     unsigned ablocks = (unsigned)ceil_div((int64_t)L_local * 32, 256);
     for (int c = 0; c < kMaxClusters; ++c) {
       k_argmax<<<1, 1024, 0, st>>>(alpha_old, state, cluster, counts, L_local, id_base, flags, c, ups_max, pc, qc,
-                                   csize);
-      k_assign<<<ablocks, 256, 0, st>>>(W64, alpha_old, state, cluster, counts, L_local, N, flags, c, pc, qc, csize);
+                                   csize, nconv_g);
+      k_assign<<<ablocks, 256, 0, st>>>(W64, alpha_old, state, cluster, counts, L_local, N, flags, c, pc, qc, csize,
+                                        nconv_g);
       launches += 2;
     }
   }
@@ -440,9 +468,10 @@ int launch_select_local(cudaStream_t st, const double* W64, const double* alpha_
 
 int launch_select_finish(cudaStream_t st, const double* W64, const int* iters, const int* counts, const int* pc,
                          const int* qc, const int* csize, const double* s4c, int64_t id_base, int N, double M_global,
-                         uint32_t flags, int64_t sum_active, int n_iter, RankSummary* summary, double* wsum) {
+                         uint32_t flags, int64_t sum_active, int n_iter, const int* nonfinite, RankSummary* summary,
+                         double* wsum) {
   k_finish<<<1, 256, 0, st>>>(W64, iters, counts, pc, qc, csize, s4c, id_base, N, M_global, flags, sum_active, n_iter,
-                              summary, wsum);
+                              nonfinite, summary, wsum);
   return 1;
 }
 

@@ -45,10 +45,12 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -227,7 +229,8 @@ __global__ void __launch_bounds__(192, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
           const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_ub, int64_t M, int64_t slot_len,
           float* __restrict__ Gp, int64_t cap, int n_coarse_h, int S_, const int* __restrict__ cnt, int s_base,
-          int S_total, float* __restrict__ Gsub, int64_t sub_cap, const int* __restrict__ cnt_g, int split) {
+          int S_total, float* __restrict__ Gsub, int64_t sub_cap, const int* __restrict__ cnt_g, int split,
+          const int8_t* __restrict__ xshift) {
   constexpr int NW = 4;   // epilogue warps
   using C = Cfg<NP, SPLIT, RG>;
   constexpr int MT = C::MT;
@@ -424,6 +427,19 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     // NW/4 warps of one lane quadrant split the columns in 32-column groups) =====
     constexpr int NH = NW / 4;
     const int q = warp & 3, h = (warp - 2) >> 2;
+    // fp16 range of the GEMM2 operand (DESIGN.md §5 "range"): |y| <= ||x_m|| for a unit row, and
+    // xshift[b] = dsh is the least shift with max ||x_m|| <= 2^(7+dsh) over the 384-sample block
+    // b, so y^3 2^-6 2^(-3 dsh) < 2^15 never overflows fp16 (65504).  The CTA takes the largest
+    // shift over its sample range; 0 (every shipped workload) is the unscaled arithmetic.
+    int dsh = 0;
+    if (xshift && nchunk > 0) {
+      const int64_t b0 = m_begin / kShiftBlock, b1 = ceil_div(min(M, m_begin + (int64_t)nchunk * MT), kShiftBlock);
+      int v = 0;
+      for (int64_t b = b0 + lane; b < b1; b += 32) v = max(v, (int)__ldg(xshift + b));
+      dsh = __reduce_max_sync(0xffffffffu, v);
+    }
+    const float csc = __int_as_float((127 - 3 * dsh) << 23);   // 2^(-3 dsh), exact scaling
+    const float gsc = __int_as_float((127 + 12 + 3 * dsh) << 23);   // 2^(12 + 3 dsh): flush unscale
     const int r = q * 32 + lane;
     const int row = row0 + r;
     const bool coarse_row = row < n_coarse;   // (fine tiles only: rows before the coarse/fine boundary)
@@ -470,44 +486,54 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
         for (int w = 0; w < GB; ++w) tmem_ld32(t_y + 32 * (h + NH * (g0 + w)), v[w]);
         tmem_wait_ld();
+        // SC: the range shift is active (CTA-uniform branch outside the element loop: the common
+        // dsh == 0 case runs exactly the unscaled instruction sequence)
+        auto cube_groups = [&](auto SC) {
+          constexpr bool scaled = decltype(SC)::value;
 #pragma unroll
-        for (int w = 0; w < GB; ++w) {
-          const int u = g0 + w;
-          uint32_t pk[16];
-          if (SPLIT && lo_pass) {   // fine tile: also the fp16 residual y^3 2^-6 - hi (GEMM2 second pass)
-            uint32_t pl[16];   // (zero for a coarse row sharing the tile: its result must not depend on its tile)
+          for (int w = 0; w < GB; ++w) {
+            const int u = g0 + w;
+            uint32_t pk[16];
+            if (SPLIT && lo_pass) {   // fine tile: also the fp16 residual y^3 2^-6 - hi (GEMM2 second pass)
+              uint32_t pl[16];   // (zero for a coarse row sharing the tile: its result must not depend on its tile)
 #pragma unroll
-            for (int k = 0; k < 32; k += 2) {
-              const float2 cc = cube2(v[w][k], v[w][k + 1]);
-              const float c0 = cc.x, c1 = cc.y;
-              __half2 hh = __floats2half2_rn(c0, c1);
-              pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
-              float2 hf = __half22float2(hh);
-              __half2 hl = __floats2half2_rn(c0 - hf.x, c1 - hf.y);
-              pl[k / 2] = coarse_row ? 0u : *reinterpret_cast<uint32_t*>(&hl);
-            }
-            tmem_st16(t_y + 32 * (h + NH * u) + 16, pl);
-          } else {
-#pragma unroll
-            for (int k = 0; k < 32; k += 2) {
-              // accumulator = 2^4 y 2^-6 = y / 4 (W scaled by 2^4, X by 2^-6)  ->  acc^3 = 2^-6 y^3
-              if (MODE == 8) {   // experiment: fp16 accumulator, read as the low half of each cell
-                v[w][k] = __float_as_uint(__half2float(__ushort_as_half((unsigned short)(v[w][k] & 0xffffu))));
-                v[w][k + 1] = __float_as_uint(__half2float(__ushort_as_half((unsigned short)(v[w][k + 1] & 0xffffu))));
+              for (int k = 0; k < 32; k += 2) {
+                const float2 cc = cube2(v[w][k], v[w][k + 1]);
+                const float c0 = scaled ? cc.x * csc : cc.x, c1 = scaled ? cc.y * csc : cc.y;
+                __half2 hh = __floats2half2_rn(c0, c1);
+                pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
+                float2 hf = __half22float2(hh);
+                __half2 hl = __floats2half2_rn(c0 - hf.x, c1 - hf.y);
+                pl[k / 2] = coarse_row ? 0u : *reinterpret_cast<uint32_t*>(&hl);
               }
-              const float2 cc = cube2(v[w][k], v[w][k + 1]);
-              __half2 hh = __floats2half2_rn(cc.x, cc.y);
-              pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
+              tmem_st16(t_y + 32 * (h + NH * u) + 16, pl);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 32; k += 2) {
+                // accumulator = 2^4 y 2^-6 = y / 4 (W scaled by 2^4, X by 2^-6)  ->  acc^3 = 2^-6 y^3
+                if (MODE == 8) {   // experiment: fp16 accumulator, read as the low half of each cell
+                  v[w][k] = __float_as_uint(__half2float(__ushort_as_half((unsigned short)(v[w][k] & 0xffffu))));
+                  v[w][k + 1] = __float_as_uint(__half2float(__ushort_as_half((unsigned short)(v[w][k + 1] & 0xffffu))));
+                }
+                const float2 cc = cube2(v[w][k], v[w][k + 1]);
+                __half2 hh = scaled ? __floats2half2_rn(cc.x * csc, cc.y * csc) : __floats2half2_rn(cc.x, cc.y);
+                pk[k / 2] = *reinterpret_cast<uint32_t*>(&hh);
+              }
             }
+            tmem_st16(t_y + 32 * (h + NH * u), pk);   // Y^3 (fp16 pairs): A operand of GEMM2
           }
-          tmem_st16(t_y + 32 * (h + NH * u), pk);   // Y^3 (fp16 pairs): A operand of GEMM2
-        }
+        };
+        if (dsh == 0)
+          cube_groups(std::false_type{});
+        else
+          cube_groups(std::true_type{});
       }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&y3ready[b]);
     }
-    // G (fp32, scaled 2^-12: y^3 by 2^-6, X by 2^-6) -> fp32 slot partial (x 2^12: exact)
+    // G (fp32, scaled 2^-12 2^(-3 dsh): y^3 by 2^-6 2^(-3 dsh), X by 2^-6) -> fp32 slot partial
+    // (x 2^(12 + 3 dsh): exact)
     mbar_wait(gdone, 0);
     tc_fence_after();
     float* out = P > 1 ? Gsub + (((int64_t)s * kSplitMax + part) * sub_cap + row) * NP : Gp + ((int64_t)s * cap + row) * NP;
@@ -521,7 +547,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
         for (int k = 0; k < 32; ++k)
           if (NP % 32 == 0 || c + k < NP) {   // streaming store (keep the X planes in L2), except
-            const float g = __uint_as_float(v[k]) * 4096.0f;   // the few rows of split parts,
+            const float g = __uint_as_float(v[k]) * gsc;       // the few rows of split parts,
             if (P > 1)                                          // which the epilogue reads next
               out[c + k] = g;
             else
@@ -590,7 +616,7 @@ CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld,
 template <int NP, bool SPLIT, int EPI, int CL, int RG>
 void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
-               const Upload& up, const SplitOut& so) {
+               const Upload& up, const SplitOut& so, const int8_t* xshift) {
   using C = Cfg<NP, SPLIT, RG>;
   auto kern = k_step_tc<NP, SPLIT, EPI, CL, RG>;
   // once per CUDA context the launch runs in (the step may also run in green contexts, runtime.cu)
@@ -628,82 +654,92 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   lc.numAttrs = 1;
   lc.gridDim = dim3((unsigned)(n_tiles * up.s_count));
   OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_coarse, up.s_count, cnt,
-                               up.s_base, S, so.sub, so.sub_cap, so.cnt_g, so.enable));
+                               up.s_base, S, so.sub, so.sub_cap, so.cnt_g, so.enable, xshift));
 }
 
+// Release build: the measured-best layout per NP --
+//   NP <= 64        2 Y slots of 192 samples, no cluster (latency-bound chunk hand-offs);
+//   64 < NP <= 128  2 Y slots of 128 samples, 2-CTA multicast clusters;
+//   NP > 128        wide layout (2 Y slots of 64 samples), 2-CTA multicast clusters;
+// one remaining row tile (the tail of a component) launches without a cluster partner, whose
+// CTA would only stream its half of the chunks in step with the active one (same arithmetic).
+// -DOICA_EXPERIMENTS adds the timing variants of profiles/r01/tc_experiments (OICA_TC_EPI
+// modes 3-8 that skip work, OICA_TC_CL = 1|2|4 and OICA_TC_RING overrides); they are compiled
+// out of the product library so no environment variable can change what the timed step does.
 template <int NP, bool SPLIT, int EPI>
 void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
                     int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
-                    const Upload& up, const SplitOut& so) {
-  // Cluster multicast of the X chunks: on by default for NP > 64, where the X
-  // stream through L2 (~6 TB/s) otherwise paces or co-limits the kernel (cfg-4 shape +20%, cfg-3
-  // shape +6%; neutral at NP = 64, which is latency-bound); OICA_TC_CL=1|2 (|4 at NP = 256) overrides.
-  static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
-  // one row tile (the tail of a component): no cluster partner, whose CTA would only stream its
-  // half of the chunks in step with the active one (same arithmetic either way)
-  const int cl = up.cl ? up.cl : cl_env ? cl_env : (NP > 64 && L_act > 128 ? 2 : 1);
-  // narrow tiles: 2 Y slots of 128 samples (default) or, OICA_TC_RING=4, 4 slots of 64 samples
-  // (measured slower: 7.7 vs 7.0 ms per cfg-3 step, profiles/r01/tc_experiments)
-  static int rg = [] { const char* e = getenv("OICA_TC_RING"); return e && atoi(e) == 4 ? 0 : 1; }();
-  static bool r192 = [] { const char* e = getenv("OICA_TC_RING"); return !(e && atoi(e) == 2); }();
+                    const Upload& up, const SplitOut& so, const int8_t* xshift) {
   constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
-  if (NP <= 64 && r192 && cl == 1) {   // small NP: 2 Y slots of 192 samples (OICA_TC_RING=2: 2 x 128)
-    launch_cl<NP, SPLIT, EPI, 1, (NP <= 64 ? 3 : 1)>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse,
-                                                    cnt, up, so);
-    return;
-  }
-  const bool r1 = NP <= 128 && rg == 1;
-  if constexpr (NP == 256) {   // experiment (OICA_TC_CL=4): 4-CTA multicast clusters
+  constexpr int RGN = NP <= 64 ? 3 : NP <= 128 ? 1 : 0;   // release Y-ring layout for this NP
+#ifdef OICA_EXPERIMENTS
+  static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
+  static int ring = [] { const char* e = getenv("OICA_TC_RING"); return e ? atoi(e) : 0; }();
+  const int cl = up.cl ? up.cl : cl_env ? cl_env : (NP > 64 && L_act > 128 ? 2 : 1);
+  if constexpr (NP == 256) {   // 4-CTA multicast clusters
     if (cl == 4) {
-      launch_cl<NP, SPLIT, EPI, 4, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
+      launch_cl<NP, SPLIT, EPI, 4, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
       return;
     }
   }
-  if (cl == 2 && r1)
-    launch_cl<NP, SPLIT, EPI, CL2, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
-  else if (cl == 2)
-    launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
-  else if (r1)
-    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
+  if (NP <= 128 && ring == 4) {   // narrow 4 x 64-sample Y ring (measured slower)
+    if (cl == 2)
+      launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+    else
+      launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+    return;
+  }
+  if (NP <= 64 && ring == 2) {   // small NP with 2 x 128-sample slots
+    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+    return;
+  }
+#else
+  const int cl = up.cl ? up.cl : (NP > 64 && L_act > 128 ? 2 : 1);
+#endif
+  if (NP > 64 && cl == 2)
+    launch_cl<NP, SPLIT, EPI, CL2, RGN>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
   else
-    launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
+    launch_cl<NP, SPLIT, EPI, 1, RGN>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
 }
 
 template <int NP, bool SPLIT>
 void launch_epi(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so) {
+                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so, const int8_t* xshift) {
+#ifdef OICA_EXPERIMENTS
   static int epi = [] { const char* e = getenv("OICA_TC_EPI"); return e ? atoi(e) : 0; }();
   switch (epi) {
-    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 7: launch_variant<NP, SPLIT, 7>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 8: launch_variant<NP, SPLIT, 8>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    default: launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 7: launch_variant<NP, SPLIT, 7>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 8: launch_variant<NP, SPLIT, 8>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    default: break;
   }
+#endif
+  launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift);
 }
 
 template <bool SPLIT>
 void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi, const __half* Wlo,
-               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so) {
+               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so, const int8_t* xshift) {
   switch (NP) {
-    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 64: launch_epi<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 144: launch_variant<144, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 160: launch_variant<160, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 176: launch_variant<176, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 192: launch_variant<192, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 208: launch_variant<208, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 224: launch_variant<224, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 240: launch_variant<240, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
-    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so); break;
+    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 64: launch_epi<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 144: launch_variant<144, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 160: launch_variant<160, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 176: launch_variant<176, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 192: launch_variant<192, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 208: launch_variant<208, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 224: launch_variant<224, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 240: launch_variant<240, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
   }
 }
@@ -728,22 +764,60 @@ __global__ void k_x_prepare_f16(const float* __restrict__ X, int64_t ld, int N, 
   *reinterpret_cast<uint4*>(Xh + (int64_t)n * ldx + m0) = *reinterpret_cast<uint4*>(h);
 }
 
+// xshift[b] for the 384-sample blocks b in [m_lo / 384, ceil(m_hi / 384)): the least dsh >= 0 with
+// 1.01 max_m ||x_m|| <= 2^(7 + dsh) over the block's samples (DESIGN.md §5 "range"; capped at
+// kMaxShift).  One CTA per block, one thread per sample.
+__global__ void __launch_bounds__(kShiftBlock) k_block_shift(const float* __restrict__ X, int64_t ld, int N,
+                                                             int64_t M, int64_t m_lo, int8_t* __restrict__ xshift) {
+  __shared__ float red[kShiftBlock / 32];
+  const int64_t b = m_lo / kShiftBlock + blockIdx.x;
+  const int64_t m = b * kShiftBlock + threadIdx.x;
+  float ss = 0.f;
+  if (m < M)
+    for (int n = 0; n < N; ++n) {
+      const float x = __ldg(X + (int64_t)n * ld + m);
+      ss = fmaf(x, x, ss);
+    }
+  // max over the block (ss >= 0: the float bit patterns order like the values)
+  unsigned u = __reduce_max_sync(0xffffffffu, __float_as_uint(ss));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = __uint_as_float(u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mx = 0.f;
+    for (int w = 0; w < kShiftBlock / 32; ++w) mx = fmaxf(mx, red[w]);
+    const float B = 1.01f * sqrtf(mx);
+    int d = 0;
+    while (d < kMaxShift && B > ldexpf(1.0f, 7 + d)) ++d;
+    xshift[b] = (int8_t)d;
+  }
+}
 
 }  // namespace
+
+int launch_block_shift(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int64_t m_lo, int64_t m_hi,
+                       int8_t* xshift) {
+  m_hi = std::min<int64_t>(m_hi, M);
+  if (m_hi <= m_lo) return 0;
+  const int64_t nb = ceil_div(m_hi, kShiftBlock) - m_lo / kShiftBlock;
+  k_block_shift<<<(unsigned)nb, kShiftBlock, 0, st>>>(X, ld, N, M, m_lo, xshift);
+  return 1;
+}
 
 bool tc_supported(int N) { return N >= 1 && N <= 256; }
 int tc_np(int N) { return (int)round_up(N < 16 ? 16 : N, 16); }
 
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
                    const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
-                   const int* cnt, bool lo_capable, const Upload& up, const SplitOut& so) {
+                   const int* cnt, bool lo_capable, const Upload& up, const SplitOut& so, const int8_t* xshift) {
   if (L_act <= 0) return 0;
-  static bool force_lo = getenv("OICA_TC_FORCE_LO") != nullptr;   // experiment: LO-capable layout always
+#ifdef OICA_EXPERIMENTS
+  static bool force_lo = getenv("OICA_TC_FORCE_LO") != nullptr;   // LO-capable layout always
   lo_capable = lo_capable || force_lo;
+#endif
   if (lo_capable || n_coarse < L_act)   // fine rows (possibly): LO-capable layout, 2nd pass from tile n_coarse/128
-    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so);
+    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
   else
-    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0, cnt, up, so);
+    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0, cnt, up, so, xshift);
   return 1;
 }
 

@@ -63,12 +63,16 @@ struct EvalPoint {
 // ---- K3: fp64 epilogue: slot sum, /M - 3w, projection, normalise, convergence
 // Precision promotion (TC): an unconverged row becomes fine when its step
 // distance d <= d_promote stagnates (d > ratio d_prev) or t >= t_force.  fine may be null.
+// nonfinite (device counter, may be null): rows whose update g was not finite (an fp16 range
+// failure or non-finite data) are counted there and retired as degenerate, never silently kept
+// iterating; the runtime fails the extraction with OICA_ERR_NONFINITE when the count is > 0.
 struct Promotion {
   uint8_t* fine;
   double* dprev;
   double d_promote;
   double ratio;   // stagnation: d > ratio * d_prev
   int t_force;
+  int* nonfinite = nullptr;
 };
 int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
                     EvalPoint ev, const int* act, int L_act, const double* Wacc, int k, int N, double M,
@@ -113,12 +117,12 @@ int launch_tail_scatter(cudaStream_t st, int T, const int64_t* ids, const double
 struct SelectWork;  // defined in k_select.cu
 struct ComponentRecord {
   double w_alpha, w_upsilon;
-  int64_t q, cluster_size, n_conv, n_unconv, n_deg, sum_active;
+  int64_t q, cluster_size, n_conv, n_unconv, n_deg, sum_active, n_nonfinite;
   int32_t iters, n_iter, status, gaussian, near_tie, n_domain;
 };
 struct RankSummary {
   oica_cluster_record rec[kMaxClusters];
-  int64_t n_conv, n_unconv, n_deg, sum_active;
+  int64_t n_conv, n_unconv, n_deg, sum_active, n_nonfinite;
   int32_t n_iter, n_domain;
 };
 
@@ -127,11 +131,15 @@ struct RankSummary {
 int launch_select_local(cudaStream_t st, const double* W64, const double* alpha_old, const uint8_t* state,
                         const int* iters, int L_local, int64_t id_base, int N, uint32_t flags,
                         const float* X, int64_t ld, int64_t M_local, int* cluster, int* pc, int* qc,
-                        int* csize, double* ups_max, int* counts, double* part, int nblk, double* s4c);
+                        int* csize, double* ups_max, int* counts, double* part, int nblk, double* s4c,
+                        const int* nconv_g = nullptr);
+// *out = converged candidates on this rank (L-shard: all-reduced into nconv_g of select_local)
+int launch_count_converged(cudaStream_t st, const uint8_t* state, int L, int* out);
+// nonfinite (device, may be null): this rank's count of rows retired by a non-finite update.
 int launch_select_finish(cudaStream_t st, const double* W64, const int* iters, const int* counts,
                          const int* pc, const int* qc, const int* csize, const double* s4c,
                          int64_t id_base, int N, double M_global, uint32_t flags, int64_t sum_active,
-                         int n_iter, RankSummary* summary, double* wsum);
+                         int n_iter, const int* nonfinite, RankSummary* summary, double* wsum);
 // Merge all ranks' summaries (world x RankSummary, world x kMaxClusters x N), append the winner to
 // Wacc row k, write the record.
 int launch_merge_accept(cudaStream_t st, const RankSummary* all, const double* wall, int world, int N,
@@ -166,9 +174,19 @@ struct Upload {
   int s_count;
   int cl = 0;   // cluster size override (0: the default for NP)
 };
+// xshift (device, one int8 per 384-sample block of the local samples, launch_block_shift): the
+// fp16 range shift of the GEMM2 operand; null: no shift.
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
                    const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
-                   const int* cnt, bool lo_capable, const Upload& up, const SplitOut& so);
+                   const int* cnt, bool lo_capable, const Upload& up, const SplitOut& so, const int8_t* xshift);
+// fp16 range of the tensor-core step (DESIGN.md §5 "range"): for every 384-sample block b of the
+// samples [m_lo, m_hi) (m_lo a multiple of 384), xshift[b] = the least dsh in [0, kMaxShift] with
+// 1.01 max ||x_m||_2 <= 2^(7 + dsh).  The y^3 operand is scaled by 2^(-3 dsh) before its fp16
+// rounding and G unscaled at the flush, so y^3 2^-6 2^(-3 dsh) < 2^15 < 65504 for |y| <= ||x_m||.
+constexpr int kShiftBlock = 384;
+constexpr int kMaxShift = 30;
+int launch_block_shift(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int64_t m_lo, int64_t m_hi,
+                       int8_t* xshift);
 // fp16 plane columns [m_lo, m_hi) (m_hi < 0: ldx); multiples of 8.
 int launch_x_prepare_f16(cudaStream_t st, const float* X, int64_t ld, int N, int64_t M, int NP,
                          int64_t ldx, __half* Xh, int64_t m_lo = 0, int64_t m_hi = -1);

@@ -20,6 +20,12 @@ struct Nccl {
                             cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
 
   static Nccl& get() {
     static Nccl n;
@@ -46,6 +52,12 @@ struct Nccl {
     AllReduce = (decltype(AllReduce))sym("ncclAllReduce");
     Broadcast = (decltype(Broadcast))sym("ncclBroadcast");
     GetErrorString = (decltype(GetErrorString))sym("ncclGetErrorString");
+    CommGetAsyncError = (decltype(CommGetAsyncError))sym("ncclCommGetAsyncError");
+    CommAbort = (decltype(CommAbort))sym("ncclCommAbort");
+    Send = (decltype(Send))sym("ncclSend");
+    Recv = (decltype(Recv))sym("ncclRecv");
+    GroupStart = (decltype(GroupStart))sym("ncclGroupStart");
+    GroupEnd = (decltype(GroupEnd))sym("ncclGroupEnd");
   }
 };
 

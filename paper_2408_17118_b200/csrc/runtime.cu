@@ -11,6 +11,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/oica.h"
@@ -62,6 +63,7 @@ constexpr int kTailMaxSlots = 1024;
 
 }  // namespace
 
+#ifdef OICA_EXPERIMENTS
 // Driver entry points for green contexts (SM partitions), resolved at run time.
 struct GreenApi {
   CUresult (*DeviceGet)(CUdevice*, int) = nullptr;
@@ -117,6 +119,8 @@ struct GreenSplit {
   unsigned smA = 0, smB = 0;
 };
 
+#endif
+
 struct oica_ctx {
   oica_config cfg{};
   cudaStream_t st = nullptr;
@@ -131,9 +135,11 @@ struct oica_ctx {
   // pipelined host upload (oica_set_data_host): copy + fp16 conversion on a second stream, piece
   // by piece; the tensor-core step of the first iteration waits per piece (DESIGN.md §7 e2e)
   cudaStream_t cst = nullptr;
+#ifdef OICA_EXPERIMENTS
   cudaStream_t st2 = nullptr;   // second launch of the mixed-cluster step (run_step)
   GreenSplit green;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+#endif
   cudaEvent_t x_ready_ev = nullptr, st_ev = nullptr;
   std::vector<cudaEvent_t> piece_ev;   // piece p of the upload is on the device (and converted)
   int pieces = 0;
@@ -143,6 +149,9 @@ struct oica_ctx {
   int precision = OICA_PREC_FP32;
   DevBuf<__half> Xh;   // TC operand plane
   int64_t ldx = 0;
+  DevBuf<int8_t> xshift;   // fp16 range shift per 384-sample block (launch_block_shift)
+  DevBuf<int> nonfinite;   // rows retired by a non-finite update in the current component
+  DevBuf<int> nconv;       // converged count summed over ranks (L-shard selection, reading A4)
   // the data the current component iterates on (DESIGN.md §5 "reduced X"): the full whitened X,
   // or X~ = G X in the d = N-k dimensional complement of the accepted rows (OICA_REDUCE_X)
   const float* vX = nullptr;
@@ -203,6 +212,60 @@ struct oica_ctx {
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
 
+  // NCCL failure handling: with a communicator every host wait polls the stream and
+  // NCCL's asynchronous error state, and gives up after nccl_timeout_s (OICA_NCCL_TIMEOUT_S,
+  // default 900 s): a peer that died or never joined cannot hang the caller.  The communicator is
+  // then aborted and the context is usable only for oica_destroy (`broken`).
+  bool broken = false;
+  double nccl_timeout_s = 900.0;
+  void abort_comm(const std::string& why) {
+    if (comm) Nccl::get().CommAbort(comm);
+    comm = nullptr;
+    broken = true;
+    throw Error(OICA_ERR_NCCL, why);
+  }
+  void wait() {
+    if (!comm) {
+      OICA_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+    auto& nc = Nccl::get();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t spin = 0;; ++spin) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) return;
+      if (q != cudaErrorNotReady) OICA_CUDA(q);
+      if ((spin & 255) == 0) {
+        ncclResult_t ae = ncclSuccess;
+        nc.CommGetAsyncError(comm, &ae);
+        if (ae != ncclSuccess && ae != ncclInProgress)
+          abort_comm(std::string("NCCL asynchronous error: ") + nc.GetErrorString(ae));
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > nccl_timeout_s)
+          abort_comm("collective wait exceeded " + std::to_string((int)nccl_timeout_s) +
+                     " s (OICA_NCCL_TIMEOUT_S): a peer rank stopped or never called");
+      }
+      if (spin > 64) std::this_thread::yield();
+    }
+  }
+  // CUDA-event time of the NCCL exchanges inside extract (oica_stats.exchange_ms)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> xev;
+  size_t xev_used = 0;
+  template <class F>
+  void exchange(F&& f) {
+    if (xev_used == xev.size()) {
+      cudaEvent_t a, b;
+      OICA_CUDA(cudaEventCreate(&a));
+      OICA_CUDA(cudaEventCreate(&b));
+      xev.emplace_back(a, b);
+    }
+    auto& e = xev[xev_used++];
+    OICA_CUDA(cudaEventRecord(e.first, st));
+    f();
+    OICA_CUDA(cudaEventRecord(e.second, st));
+    ++stats.exchange_calls;
+  }
+
   int world() const { return cfg.world; }
   bool tc() const { return precision == OICA_PREC_TC || precision == OICA_PREC_TC_SPLIT; }
   bool split() const { return precision == OICA_PREC_TC_SPLIT; }
@@ -215,10 +278,17 @@ struct oica_ctx {
     return tc() ? EvalPoint{Whi.p, Wlo.p, nullptr, vNP} : EvalPoint{nullptr, nullptr, W32.p, vNP};
   }
   Promotion promotion() const {
+#ifdef OICA_EXPERIMENTS
     static const double pd = getenv("OICA_PROMOTE_D") ? atof(getenv("OICA_PROMOTE_D")) : kPromoteD;
     static const double pr = getenv("OICA_PROMOTE_RATIO") ? atof(getenv("OICA_PROMOTE_RATIO")) : kPromoteRatio;
     static const int pt = getenv("OICA_PROMOTE_T") ? atoi(getenv("OICA_PROMOTE_T")) : kPromoteT;
-    return tc() ? Promotion{fine.p, dprev.p, pd, pr, pt} : Promotion{nullptr, nullptr, 0.0, 0.0, 0};
+#else
+    constexpr double pd = kPromoteD, pr = kPromoteRatio;
+    constexpr int pt = kPromoteT;
+#endif
+    Promotion p = tc() ? Promotion{fine.p, dprev.p, pd, pr, pt} : Promotion{nullptr, nullptr, 0.0, 0.0, 0};
+    p.nonfinite = nonfinite.p;
+    return p;
   }
   const uint8_t* fine_flags() const { return tc() ? fine.p : nullptr; }
   // a communicator exists for world > 1, or at world == 1 when a unique id is passed (the
@@ -243,7 +313,13 @@ struct oica_ctx {
   std::vector<oica_iteration_record> iter_log;
   void mark_pair() { ev_t.push_back(cur_t); }
   void harvest_events() {
-    OICA_CUDA(cudaStreamSynchronize(st));
+    wait();
+    for (size_t k = 0; k < xev_used; ++k) {
+      float ms = 0.f;
+      OICA_CUDA(cudaEventElapsedTime(&ms, xev[k].first, xev[k].second));
+      stats.exchange_ms += ms;
+    }
+    xev_used = 0;
     pairs.clear();
     for (size_t k = 0; k + 1 < ev_used; k += 2) {
       float ms = 0.f;
@@ -268,6 +344,7 @@ oica_status guard(oica_ctx* ctx, F&& f) {
   try {
     if (ctx) {
       ctx->err.clear();
+      OICA_REQUIRE(!ctx->broken, OICA_ERR_NCCL, "context unusable after an NCCL failure: destroy it");
       OICA_CUDA(cudaSetDevice(ctx->cfg.device));
     }
     f();
@@ -329,8 +406,12 @@ void plan_slots_for(int64_t M_global, int64_t M_local, int64_t* slot_len, int* S
   // one CTA per (row tile, slot): long slots amortise each CTA's set-up (TMEM allocation, W
   // load, pipeline fill, G flush: ~13% of the step at 8192-sample slots and N = 128), while up
   // to 30 slots (of >= 128 samples) keep enough CTAs per row tile for small L and small M
+#ifdef OICA_EXPERIMENTS
   static int64_t target = [] { const char* e = getenv("OICA_SLOT_TARGET"); return e ? atoll(e) : kSlotTarget; }();
   static int64_t min_slots = [] { const char* e = getenv("OICA_MIN_SLOTS"); return e ? atoll(e) : (int64_t)kMinSlots; }();
+#else
+  constexpr int64_t target = kSlotTarget, min_slots = kMinSlots;
+#endif
   int64_t S = std::max<int64_t>(std::min<int64_t>(min_slots, M_global / kSlotMin), M_global / target);
   S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, S));
   *slot_len = round_up(ceil_div(M_global, S), kSlotAlign);
@@ -341,6 +422,8 @@ void plan_slots(oica_ctx* c) { plan_slots_for(c->Mg, c->M, &c->slot_len, &c->S);
 
 void ensure_candidate_buffers(oica_ctx* c) {
   size_t Ll = (size_t)c->Ll, N = (size_t)c->N, NP = (size_t)c->NP;
+  c->nonfinite.ensure(1);
+  c->nconv.ensure(1);
   c->W64.ensure(Ll * N);
   c->alpha_old.ensure(Ll);
   c->iters.ensure(Ll);
@@ -407,6 +490,7 @@ void build_operand(oica_ctx* c, const int* act, int cap) {
     c->count(launch_operand_f32(c->st, act, c->Lact_dev.p, cap, c->W64.p, c->vN, c->vNP, c->W32.p));
 }
 
+#ifdef OICA_EXPERIMENTS
 // Lazily builds the green-context split; false (and never retried) if unavailable.
 bool green_ready(oica_ctx* c) {
   GreenSplit& g = c->green;
@@ -465,6 +549,8 @@ bool mixed_clusters(const oica_ctx* c, int L_act) {
   return on && !cl_env && c->vNP == 256 && c->S >= 10 && L_act >= 64 * 128;
 }
 
+#endif
+
 // One fused contraction over the active rows (positions 0..L_act-1; rows >= n_coarse are fine)
 // into the slots.  With cnt (device [L_act, n_coarse]) the host values are upper bounds that
 // only size the grid (iterations enqueued without a host round trip).
@@ -488,9 +574,10 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* c
       const int s0 = p * spp, s1 = std::min(c->S, s0 + spp);
       if (s1 > s0)
         n += launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
-                            c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{s0, s1 - s0}, so);
+                            c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{s0, s1 - s0}, so, c->xshift.p);
     }
     sync_x(c);
+#ifdef OICA_EXPERIMENTS
   } else if (c->tc() && green_step(c, L_act)) {
     // 4-CTA multicast clusters on a 128-SM partition (a quarter of the L2 -> SM stream: less power,
     // a higher clock; 4-CTA clusters alone fit on only 132 SMs) and 2-CTA clusters on the other
@@ -503,15 +590,18 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* c
     OICA_CUDA(cudaEventRecord(g.fork, c->st));
     OICA_CUDA(cudaStreamWaitEvent((cudaStream_t)g.sA, g.fork, 0));
     OICA_CUDA(cudaStreamWaitEvent((cudaStream_t)g.sB, g.fork, 0));
-    CUcontext prev = nullptr;
-    api.CtxGetCurrent(&prev);
+    struct CtxRestore {   // the calling thread leaves in its own context even if a launch throws
+      GreenApi& api;
+      CUcontext prev = nullptr;
+      explicit CtxRestore(GreenApi& a) : api(a) { api.CtxGetCurrent(&prev); }
+      ~CtxRestore() { api.CtxSetCurrent(prev); }
+    } restore(api);
     api.CtxSetCurrent(g.cA);
     n = launch_step_tc((cudaStream_t)g.sA, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act,
-                       c->slot_len, c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, S_a, 4}, so);
+                       c->slot_len, c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, S_a, 4}, so, c->xshift.p);
     api.CtxSetCurrent(g.cB);
     n += launch_step_tc((cudaStream_t)g.sB, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act,
-                        c->slot_len, c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{S_a, S_b, 2}, so);
-    api.CtxSetCurrent(prev);
+                        c->slot_len, c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{S_a, S_b, 2}, so, c->xshift.p);
     OICA_CUDA(cudaEventRecord(g.jA, (cudaStream_t)g.sA));
     OICA_CUDA(cudaEventRecord(g.jB, (cudaStream_t)g.sB));
     OICA_CUDA(cudaStreamWaitEvent(c->st, g.jA, 0));
@@ -533,15 +623,16 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* c
     OICA_CUDA(cudaEventRecord(c->fork_ev, c->st));
     OICA_CUDA(cudaStreamWaitEvent(c->st2, c->fork_ev, 0));
     n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len, c->S,
-                       c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, S_a, 4}, so);
+                       c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, S_a, 4}, so, c->xshift.p);
     n += launch_step_tc(c->st2, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len, c->S,
-                        c->Gp32.p, c->Ll, cnt, lo_capable, Upload{S_a, S_b, 2}, so);
+                        c->Gp32.p, c->Ll, cnt, lo_capable, Upload{S_a, S_b, 2}, so, c->xshift.p);
     OICA_CUDA(cudaEventRecord(c->join_ev, c->st2));
     OICA_CUDA(cudaStreamWaitEvent(c->st, c->join_ev, 0));
+#endif
   } else if (c->tc()) {
     sync_x(c);
     n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
-                       c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, c->S}, so);
+                       c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, c->S}, so, c->xshift.p);
   } else {
     sync_x(c);
     n = launch_step_simt(c->st, c->vX, c->vld, c->M, c->vN, c->vNP, c->W32.p, L_act, c->slot_len, c->S, kFlush,
@@ -709,7 +800,7 @@ void use_reduced_view(oica_ctx* c, int d) {
   c->count(launch_reduce_apply(c->st, c->Gf.p, d, N, c->X, c->ld, c->M, c->Xr.p, c->M, c->tc() ? c->Xrh.p : nullptr,
                                npd, c->ldx));
   check_launch();
-  OICA_CUDA(cudaStreamSynchronize(c->st));   // gf is a host temporary
+  c->wait();   // gf is a host temporary
   c->vX = c->Xr.p;
   c->vld = c->M;
   c->vXh = c->tc() ? c->Xrh.p : nullptr;
@@ -736,8 +827,8 @@ void refresh_unconverged_alpha(oica_ctx* c, const int* act, int L_fin, int n_coa
                               c->s4fin.p, cnt));
   if (c->mshard()) {
     auto& nc = Nccl::get();
-    OICA_NCCL(nc.AllReduce(c->Gfin.p, c->Gfin.p, (size_t)L_fin * c->vNP, ncclFloat64, ncclSum, c->comm, st));
-    if (!tc) OICA_NCCL(nc.AllReduce(c->s4fin.p, c->s4fin.p, (size_t)L_fin, ncclFloat64, ncclSum, c->comm, st));
+    c->exchange([&] { OICA_NCCL(nc.AllReduce(c->Gfin.p, c->Gfin.p, (size_t)L_fin * c->vNP, ncclFloat64, ncclSum, c->comm, st)); });
+    if (!tc) c->exchange([&] { OICA_NCCL(nc.AllReduce(c->s4fin.p, c->s4fin.p, (size_t)L_fin, ncclFloat64, ncclSum, c->comm, st)); });
   }
   if (tc) c->count(launch_s4_from_g(st, c->eval_point(), c->W64.p, c->Gfin.p, c->vNP, L_fin, vN, c->s4fin.p));
   c->count(launch_alpha_refresh(st, act, cnt, L_fin, c->s4fin.p, (double)c->Mg, c->alpha_old.p));
@@ -748,10 +839,10 @@ void refresh_unconverged_alpha(oica_ctx* c, const int* act, int L_fin, int n_coa
 std::vector<int> gather_counts(oica_ctx* c) {
   const int W = c->world();
   c->tail.cnt_all.ensure((size_t)W);
-  OICA_NCCL(Nccl::get().AllGather(c->Lact_dev.p, c->tail.cnt_all.p, 1, ncclInt32, c->comm, c->st));
+  c->exchange([&] { OICA_NCCL(Nccl::get().AllGather(c->Lact_dev.p, c->tail.cnt_all.p, 1, ncclInt32, c->comm, c->st)); });
   std::vector<int> v((size_t)W);
   OICA_CUDA(cudaMemcpyAsync(v.data(), c->tail.cnt_all.p, sizeof(int) * W, cudaMemcpyDeviceToHost, c->st));
-  OICA_CUDA(cudaStreamSynchronize(c->st));
+  c->wait();
   return v;
 }
 
@@ -798,7 +889,7 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
   // C4: records of this rank's active rows, all-gathered; dense in rank order
   c->count(launch_tail_pack(st, act, c->Lact_dev.p, L_local, c->W64.p, c->alpha_old.p, tc ? c->dprev.p : nullptr,
                             c->fine_flags(), c->id_base, vN, tb.pack.p));
-  OICA_NCCL(nc.AllGather(tb.pack.p, tb.pack_all.p, (size_t)Pmax * R, ncclFloat64, c->comm, st));
+  c->exchange([&] { OICA_NCCL(nc.AllGather(tb.pack.p, tb.pack_all.p, (size_t)Pmax * R, ncclFloat64, c->comm, st)); });
   size_t off = 0;
   for (int r = 0; r < W; ++r) {
     if (counts[r] > 0)
@@ -836,7 +927,7 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
     pr.fine = tb.fine.p;
     pr.dprev = tb.dprev.p;
   }
-  OICA_CUDA(cudaStreamSynchronize(st));
+  c->wait();
   int L_ub = ((volatile int*)c->Lact_host)[0], nc_ub = ((volatile int*)c->Lact_host)[1];
   const int nc_first = nc_ub;
   int* a_cur = tb.act0.p;
@@ -858,7 +949,7 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
       int n = 0;
       if (s_cnt > 0 && tc)
         n = launch_step_tc(st, c->vXh, c->ldx, c->M, NP, tb.Whi.p, tb.Wlo.p, nc_ub, L_ub, slot_len, S_all, tb.Gp32.p, T,
-                           cnt, B > 1 && !c->split(), Upload{s0, s_cnt}, SplitOut{nullptr, 0, nullptr, 0});
+                           cnt, B > 1 && !c->split(), Upload{s0, s_cnt}, SplitOut{nullptr, 0, nullptr, 0}, c->xshift.p);
       else if (s_cnt > 0)
         n = launch_step_simt(st, c->vX + m0, c->vld, M_r, vN, NP, tb.W32.p, L_ub, slot_len, s_cnt, kFlush, tb.Gp.p,
                              tb.s4p.p, T, cnt);
@@ -870,8 +961,8 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
       SlotPartials part = tc ? SlotPartials{tb.Gp32.p + (size_t)s0 * T * NP, true} : SlotPartials{tb.Gp.p, false};
       c->count(launch_slot_reduce(st, part, tc ? nullptr : tb.s4p.p, s_cnt, T, NP, L_ub, vN, tb.Gsum.p, NP,
                                   tb.s4sum.p));
-      OICA_NCCL(nc.AllReduce(tb.Gsum.p, tb.Gsum.p, (size_t)L_ub * NP, ncclFloat64, ncclSum, c->comm, st));
-      if (!tc) OICA_NCCL(nc.AllReduce(tb.s4sum.p, tb.s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st));
+      c->exchange([&] { OICA_NCCL(nc.AllReduce(tb.Gsum.p, tb.Gsum.p, (size_t)L_ub * NP, ncclFloat64, ncclSum, c->comm, st)); });
+      if (!tc) c->exchange([&] { OICA_NCCL(nc.AllReduce(tb.s4sum.p, tb.s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st)); });
       c->count(launch_epilogue(st, SlotPartials{tb.Gsum.p, false}, tc ? nullptr : tb.s4sum.p, 1, T, NP, ev, a_cur,
                                L_ub, c->Wacc.p, kk, vN, (double)c->Mg, tol, t, tb.W64.p, tb.alpha.p, tb.iters.p,
                                tb.state.p, tb.keep.p, pr, cnt));
@@ -880,7 +971,7 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
       std::swap(a_cur, a_nxt);
       check_launch();
     }
-    OICA_CUDA(cudaStreamSynchronize(st));
+    c->wait();
     L_ub = ((volatile int*)c->Lact_host)[0];
     nc_ub = ((volatile int*)c->Lact_host)[1];
   }
@@ -892,15 +983,15 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
       c->count(launch_operand_f32(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.W32.p));
     if (s_cnt > 0 && tc)
       c->count(launch_step_tc(st, c->vXh, c->ldx, c->M, NP, tb.Whi.p, tb.Wlo.p, nc_ub, L_ub, slot_len, S_all,
-                              tb.Gp32.p, T, cnt, false, Upload{s0, s_cnt}, SplitOut{nullptr, 0, nullptr, 0}));
+                              tb.Gp32.p, T, cnt, false, Upload{s0, s_cnt}, SplitOut{nullptr, 0, nullptr, 0}, c->xshift.p));
     else if (s_cnt > 0)
       c->count(launch_step_simt(st, c->vX + m0, c->vld, M_r, vN, NP, tb.W32.p, L_ub, slot_len, s_cnt, kFlush, tb.Gp.p,
                                 tb.s4p.p, T, cnt));
     SlotPartials part = tc ? SlotPartials{tb.Gp32.p + (size_t)s0 * T * NP, true} : SlotPartials{tb.Gp.p, false};
     c->count(launch_slot_reduce(st, part, tc ? nullptr : tb.s4p.p, s_cnt, T, NP, L_ub, vN, tb.Gsum.p, NP,
                                 tb.s4sum.p));
-    OICA_NCCL(nc.AllReduce(tb.Gsum.p, tb.Gsum.p, (size_t)L_ub * NP, ncclFloat64, ncclSum, c->comm, st));
-    if (!tc) OICA_NCCL(nc.AllReduce(tb.s4sum.p, tb.s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st));
+    c->exchange([&] { OICA_NCCL(nc.AllReduce(tb.Gsum.p, tb.Gsum.p, (size_t)L_ub * NP, ncclFloat64, ncclSum, c->comm, st)); });
+    if (!tc) c->exchange([&] { OICA_NCCL(nc.AllReduce(tb.s4sum.p, tb.s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st)); });
     if (tc) c->count(launch_s4_from_g(st, ev, tb.W64.p, tb.Gsum.p, NP, L_ub, vN, tb.s4sum.p));
     c->count(launch_alpha_refresh(st, a_cur, cnt, L_ub, tb.s4sum.p, (double)c->Mg, tb.alpha.p));
     check_launch();
@@ -912,7 +1003,7 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
   // work counters: rows entering tail iteration t' (T for the first)
   std::vector<int> hist(2 * ((size_t)K + 1), 0);
   OICA_CUDA(cudaMemcpyAsync(hist.data(), tb.hist.p, sizeof(int) * hist.size(), cudaMemcpyDeviceToHost, st));
-  OICA_CUDA(cudaStreamSynchronize(st));
+  c->wait();
   int64_t sum_active = 0;
   for (int tt = t_start + 1; tt <= t; ++tt) {
     const int Lin = tt == t_start + 1 ? T : hist[2 * (tt - 1)];
@@ -957,9 +1048,9 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     int64_t v[2] = {(int64_t)(h >> 2), -(int64_t)(h >> 2)}, r[2] = {0, 0};
     c->arghash.ensure(2);
     OICA_CUDA(cudaMemcpyAsync(c->arghash.p, v, sizeof v, cudaMemcpyHostToDevice, st));
-    OICA_NCCL(Nccl::get().AllReduce(c->arghash.p, c->arghash.p, 2, ncclInt64, ncclMax, c->comm, st));
+    c->exchange([&] { OICA_NCCL(Nccl::get().AllReduce(c->arghash.p, c->arghash.p, 2, ncclInt64, ncclMax, c->comm, st)); });
     OICA_CUDA(cudaMemcpyAsync(r, c->arghash.p, sizeof r, cudaMemcpyDeviceToHost, st));
-    OICA_CUDA(cudaStreamSynchronize(st));
+    c->wait();
     OICA_REQUIRE(r[0] == v[0] && r[1] == v[1], OICA_ERR_INVALID_ARGUMENT,
                  "ranks called oica_extract_components with different arguments");
   }
@@ -1001,7 +1092,8 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
                                 c->fine.p, c->split() ? 1 : 0, c->dprev.p));
     c->count(launch_compact(st, nullptr, c->keep.p, c->fine_flags(), (int)c->Ll, c->act0.p, c->Lact_dev.p,
                             c->Lact_host));
-    OICA_CUDA(cudaStreamSynchronize(st));
+    OICA_CUDA(cudaMemsetAsync(c->nonfinite.p, 0, sizeof(int), st));
+    c->wait();
     trace.mark("init");
     int L_act = ((volatile int*)c->Lact_host)[0];
     int n_coarse = ((volatile int*)c->Lact_host)[1];
@@ -1043,7 +1135,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         const int* cnt = c->Lact_dev.p;
         const int* cnt_g = cnt;
         if (lockstep) {
-          OICA_NCCL(Nccl::get().AllReduce(c->Lact_dev.p, c->Lg.p, 1, ncclInt32, ncclSum, c->comm, st));
+          c->exchange([&] { OICA_NCCL(Nccl::get().AllReduce(c->Lact_dev.p, c->Lg.p, 1, ncclInt32, ncclSum, c->comm, st)); });
           cnt_g = c->Lg.p;
         }
         if (L_ub == 0) continue;   // lock step: this rank idles while others iterate
@@ -1057,8 +1149,8 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         if (c->mshard()) {  // one fp64 allreduce of (G, s4) per iteration; B == 1 here
           c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, c->vNP, L_ub, vN, c->Gsum.p, c->vNP, c->s4sum.p, cnt));
           auto& nc = Nccl::get();
-          OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_ub * c->vNP, ncclFloat64, ncclSum, c->comm, st));
-          if (!tc) OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st));
+          c->exchange([&] { OICA_NCCL(nc.AllReduce(c->Gsum.p, c->Gsum.p, (size_t)L_ub * c->vNP, ncclFloat64, ncclSum, c->comm, st)); });
+          if (!tc) c->exchange([&] { OICA_NCCL(nc.AllReduce(c->s4sum.p, c->s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st)); });
           G = SlotPartials{c->Gsum.p, false};
           s4 = tc ? nullptr : c->s4sum.p;
           S = 1;
@@ -1091,7 +1183,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         check_launch();
       }
       trace.batch_enqueued();
-      OICA_CUDA(cudaStreamSynchronize(st));
+      c->wait();
       trace.batch_done();
       L_ub = ((volatile int*)c->Lact_host)[0];
       nc_ub = ((volatile int*)c->Lact_host)[1];
@@ -1112,7 +1204,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     if (t_bulk > 0) {
       OICA_CUDA(cudaMemcpyAsync(hist.data(), c->hist.p, sizeof(int) * 2 * (size_t)(t_bulk + 1), cudaMemcpyDeviceToHost,
                                 st));
-      OICA_CUDA(cudaStreamSynchronize(st));
+      c->wait();
     }
     int64_t sum_active = 0;
     int t_exec = 0;
@@ -1130,20 +1222,28 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     }
     t = t_exec;
     // a7: selection and accept
+    sync_x(c);   // the exact-alpha pass reads X (a rank may reach here without running a step)
+    const int* nconv_g = nullptr;
+    if (c->collective() && !c->mshard()) {   // reading A4's "none converged" decided over all ranks
+      c->count(launch_count_converged(st, c->state.p, (int)c->Ll, c->nconv.p));
+      c->exchange([&] { OICA_NCCL(Nccl::get().AllReduce(c->nconv.p, c->nconv.p, 1, ncclInt32, ncclSum, c->comm, st)); });
+      nconv_g = c->nconv.p;
+    }
     c->count(launch_select_local(st, c->W64.p, c->alpha_old.p, c->state.p, c->iters.p, (int)c->Ll, c->id_base, vN,
                                  flags, c->vX, c->vld, c->M, c->cluster.p, c->pc.p, c->qc.p, c->csize.p, c->ups_max.p,
-                                 c->counts.p, c->part.p, c->nblk_alpha, c->s4c.p));
+                                 c->counts.p, c->part.p, c->nblk_alpha, c->s4c.p, nconv_g));
     if (c->mshard())
-      OICA_NCCL(Nccl::get().AllReduce(c->s4c.p, c->s4c.p, kMaxClusters, ncclFloat64, ncclSum, c->comm, st));
+      c->exchange([&] { OICA_NCCL(Nccl::get().AllReduce(c->s4c.p, c->s4c.p, kMaxClusters, ncclFloat64, ncclSum, c->comm, st)); });
     c->count(launch_select_finish(st, c->W64.p, c->iters.p, c->counts.p, c->pc.p, c->qc.p, c->csize.p, c->s4c.p,
-                                  c->id_base, vN, (double)c->Mg, flags, sum_active, t, c->summary.p, c->wsum.p));
+                                  c->id_base, vN, (double)c->Mg, flags, sum_active, t, c->nonfinite.p, c->summary.p,
+                                  c->wsum.p));
     const RankSummary* all = c->summary.p;
     const double* wall = c->wsum.p;
     int world = 1;
     if (c->collective() && !c->mshard()) {  // L-shard: one exchange per component (C1)
       auto& nc = Nccl::get();
-      OICA_NCCL(nc.AllGather(c->summary.p, c->summary_all.p, sizeof(RankSummary), ncclUint8, c->comm, st));
-      OICA_NCCL(nc.AllGather(c->wsum.p, c->wsum_all.p, (size_t)kMaxClusters * vN, ncclFloat64, c->comm, st));
+      c->exchange([&] { OICA_NCCL(nc.AllGather(c->summary.p, c->summary_all.p, sizeof(RankSummary), ncclUint8, c->comm, st)); });
+      c->exchange([&] { OICA_NCCL(nc.AllGather(c->wsum.p, c->wsum_all.p, (size_t)kMaxClusters * vN, ncclFloat64, c->comm, st)); });
       all = c->summary_all.p;
       wall = c->wsum_all.p;
       world = c->world();
@@ -1172,6 +1272,9 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     }
     trace.mark("select");
     c->last_valid = true;
+    if (rec_h.n_nonfinite > 0)
+      throw Error(OICA_ERR_NONFINITE, "component " + std::to_string(i) + ": " + std::to_string(rec_h.n_nonfinite) +
+                                          " candidate update(s) were not finite (non-finite data?)");
     if (rec_h.status != OICA_OK)
       throw Error((oica_status)rec_h.status,
                   rec_h.status == OICA_ERR_ALL_CANDIDATES_DEGENERATE ? "all candidates degenerate (A18)"
@@ -1192,7 +1295,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
       for (int n = 0; n < N; ++n) w_host[n] *= sg / nw;
       OICA_CUDA(cudaMemcpyAsync(c->Wacc.p + (size_t)k * N, w_host.data(), sizeof(double) * N, cudaMemcpyHostToDevice,
                                 st));
-      OICA_CUDA(cudaStreamSynchronize(st));
+      c->wait();
     } else {
       std::copy(b_host.begin(), b_host.begin() + N, w_host.begin());
     }
@@ -1254,8 +1357,10 @@ void set_data_impl(oica_ctx* c, const float* Xw, int64_t N, int64_t M_local, int
   if (tc) {
     c->ldx = round_up(M_local, 128);
     c->Xh.ensure((size_t)c->NP * c->ldx);
+    c->xshift.ensure((size_t)ceil_div(M_local, kShiftBlock));
     if (prepare) {
       c->count(launch_x_prepare_f16(c->st, Xw, ld, (int)N, M_local, (int)c->NP, c->ldx, c->Xh.p));
+      c->count(launch_block_shift(c->st, Xw, ld, (int)N, M_local, 0, M_local, c->xshift.p));
       check_launch();
     }
   }
@@ -1281,6 +1386,7 @@ const char* oica_status_string(oica_status s) {
     case OICA_ERR_OUT_OF_MEMORY: return "OICA_ERR_OUT_OF_MEMORY";
     case OICA_ERR_CUDA: return "OICA_ERR_CUDA";
     case OICA_ERR_NCCL: return "OICA_ERR_NCCL";
+    case OICA_ERR_NONFINITE: return "OICA_ERR_NONFINITE";
   }
   return "OICA_UNKNOWN_STATUS";
 }
@@ -1321,6 +1427,7 @@ oica_status oica_create(const oica_config* cfg, oica_ctx** out) {
       c->own_stream = true;
     }
     OICA_CUDA(cudaHostAlloc((void**)&c->Lact_host, 2 * sizeof(int), cudaHostAllocMapped));
+    if (const char* e = getenv("OICA_NCCL_TIMEOUT_S")) c->nccl_timeout_s = std::max(1.0, atof(e));
     if (cfg->world > 1 || cfg->nccl_unique_id) {
       ncclUniqueId id;
       std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
@@ -1349,11 +1456,13 @@ oica_status oica_destroy(oica_ctx* c) {
   if (c->x_ready_ev) cudaEventDestroy(c->x_ready_ev);
   for (auto e : c->piece_ev) cudaEventDestroy(e);
   if (c->st_ev) cudaEventDestroy(c->st_ev);
+#ifdef OICA_EXPERIMENTS
   if (c->st2) {
     cudaStreamSynchronize(c->st2);
     cudaStreamDestroy(c->st2);
   }
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->green.ok) {
     GreenApi& api = GreenApi::get();
     cudaEventDestroy(c->green.fork);
@@ -1364,7 +1473,7 @@ oica_status oica_destroy(oica_ctx* c) {
     api.GreenCtxDestroy(c->green.gA);
     api.GreenCtxDestroy(c->green.gB);
   }
-  if (c->join_ev) cudaEventDestroy(c->join_ev);
+#endif
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
   return OICA_OK;
@@ -1416,7 +1525,7 @@ oica_status oica_whiten(oica_ctx* c, const float* X, int64_t N, int64_t M, int64
     OICA_CUDA(cudaMemcpyAsync(c->wh_V.p, V.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, c->st));
     c->count(launch_apply_whitening(c->st, X, ld, n, M, c->wh_mean.p, c->wh_V.p, Xw, ld_out));
     check_launch();
-    OICA_CUDA(cudaStreamSynchronize(c->st));
+    c->wait();
     if (mean_out) std::memcpy(mean_out, mean.data(), sizeof(double) * n);
     if (V_out) std::memcpy(V_out, V.data(), sizeof(double) * n * n);
     if (eig_out) std::memcpy(eig_out, ev.data(), sizeof(double) * n);
@@ -1459,14 +1568,76 @@ oica_status oica_set_data_host(oica_ctx* c, const float* Xh, int64_t N, int64_t 
       const int64_t m0 = p * c->piece_len, m1 = std::min(M, m0 + c->piece_len);
       OICA_CUDA(cudaMemcpy2DAsync(c->Xown.p + m0, sizeof(float) * M, Xh + m0, sizeof(float) * ld, sizeof(float) * (m1 - m0),
                                   (size_t)N, cudaMemcpyHostToDevice, c->cst));
-      if (c->tc())
+      if (c->tc()) {
         c->count(launch_x_prepare_f16(c->cst, c->Xown.p, M, (int)N, M, (int)c->NP, c->ldx, c->Xh.p, m0,
                                       p == c->pieces - 1 ? c->ldx : m1));
+        c->count(launch_block_shift(c->cst, c->Xown.p, M, (int)N, M, m0, m1, c->xshift.p));   // m0: whole slots
+      }
       OICA_CUDA(cudaEventRecord(c->piece_ev[p], c->cst));
     }
     check_launch();
     OICA_CUDA(cudaEventRecord(c->x_ready_ev, c->cst));
     c->x_pending = true;
+  });
+}
+
+oica_status oica_distribute_data(oica_ctx* c, const float* X_root, int64_t N, int64_t M_global, int64_t ld_root,
+                                 float* X_out, int64_t ld_out, int32_t root) {
+  if (!c) return OICA_ERR_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    const int W = c->cfg.world, r = c->cfg.rank;
+    OICA_REQUIRE(N >= 1 && N <= 256 && M_global > N && X_out && root >= 0 && root < W, OICA_ERR_INVALID_ARGUMENT,
+                 "need 1 <= N <= 256, M_global > N, X_out, 0 <= root < world");
+    OICA_REQUIRE(r != root || (X_root && ld_root >= M_global), OICA_ERR_INVALID_ARGUMENT,
+                 "root: X_root NULL or ld_root < M_global");
+    const bool msh = c->cfg.shard_mode == OICA_SHARD_M && W > 1;
+    const int64_t lo = msh ? M_global * r / W : 0, hi = msh ? M_global * (r + 1) / W : M_global;
+    OICA_REQUIRE(ld_out >= hi - lo, OICA_ERR_INVALID_ARGUMENT, "ld_out < this rank's sample count");
+    cudaStream_t st = c->st;
+    if (!c->comm) {   // one rank: a plain device copy (nothing to distribute)
+      if (X_out != X_root)
+        OICA_CUDA(cudaMemcpy2DAsync(X_out, sizeof(float) * ld_out, X_root, sizeof(float) * ld_root,
+                                    sizeof(float) * M_global, (size_t)N, cudaMemcpyDeviceToDevice, st));
+      c->wait();
+      return;
+    }
+    auto& nc = Nccl::get();
+    if (!msh) {   // replicated X (L-shard / hybrid): broadcast from root
+      if (ld_root == M_global && ld_out == M_global) {
+        c->exchange([&] {
+          OICA_NCCL(nc.Broadcast(r == root ? X_root : X_out, X_out, (size_t)N * M_global, ncclFloat32, root, c->comm, st));
+        });
+      } else {   // strided rows: one broadcast per row, grouped
+        c->exchange([&] {
+          OICA_NCCL(nc.GroupStart());
+          for (int64_t n = 0; n < N; ++n)
+            OICA_NCCL(nc.Broadcast(r == root ? X_root + n * ld_root : X_out + n * ld_out, X_out + n * ld_out,
+                                   (size_t)M_global, ncclFloat32, root, c->comm, st));
+          OICA_NCCL(nc.GroupEnd());
+        });
+      }
+    } else {   // M-shard: rank q receives the samples [q M/W, (q+1) M/W) of every row from root
+      c->exchange([&] {
+        OICA_NCCL(nc.GroupStart());
+        if (r == root) {
+          for (int q = 0; q < W; ++q) {
+            const int64_t ql = M_global * q / W, qh = M_global * (q + 1) / W;
+            if (q == root || qh <= ql) continue;
+            for (int64_t n = 0; n < N; ++n)
+              OICA_NCCL(nc.Send(X_root + n * ld_root + ql, (size_t)(qh - ql), ncclFloat32, q, c->comm, st));
+          }
+        } else if (hi > lo) {
+          for (int64_t n = 0; n < N; ++n)
+            OICA_NCCL(nc.Recv(X_out + n * ld_out, (size_t)(hi - lo), ncclFloat32, root, c->comm, st));
+        }
+        OICA_NCCL(nc.GroupEnd());
+      });
+      if (r == root && hi > lo)
+        OICA_CUDA(cudaMemcpy2DAsync(X_out, sizeof(float) * ld_out, X_root + lo, sizeof(float) * ld_root,
+                                    sizeof(float) * (hi - lo), (size_t)N, cudaMemcpyDeviceToDevice, st));
+    }
+    c->wait();
+    c->harvest_events();
   });
 }
 
@@ -1605,7 +1776,7 @@ oica_status oica_reset_stats(oica_ctx* c) {
 
 oica_status oica_synchronize(oica_ctx* c) {
   if (!c) return OICA_ERR_INVALID_ARGUMENT;
-  return guard(c, [&] { OICA_CUDA(cudaStreamSynchronize(c->st)); });
+  return guard(c, [&] { c->wait(); });
 }
 
 oica_status oica_slot_plan(int64_t M_global, int64_t M_local, int64_t* slot_len, int32_t* S_local) {

@@ -18,11 +18,13 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboica.so")
+# OICA_LIB selects another build of the library (the -DOICA_EXPERIMENTS timing build,
+# paper_2408_17118_b200/build.py --experiments); bench.py refuses to run with it set
+LIB_PATH = os.environ.get("OICA_LIB") or os.path.join(_HERE, "liboica.so")
 
 OK = 0
 STATUS = ["OK", "INVALID_ARGUMENT", "DIMENSION_MISMATCH", "RANK_DEFICIENT", "ALL_CANDIDATES_DEGENERATE",
-          "DOMAIN", "STATE", "UNSUPPORTED_DEVICE", "OUT_OF_MEMORY", "CUDA", "NCCL"]
+          "DOMAIN", "STATE", "UNSUPPORTED_DEVICE", "OUT_OF_MEMORY", "CUDA", "NCCL", "NONFINITE"]
 
 PREC_AUTO, PREC_FP32, PREC_TC, PREC_TC_SPLIT = 0, 1, 2, 3
 SHARD_L, SHARD_M, SHARD_HYBRID = 0, 1, 2
@@ -59,7 +61,8 @@ class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("step_launches", C.c_int64), ("step_ms", C.c_double),
                 ("step_flops", C.c_double), ("iterations", C.c_int64), ("sum_active", C.c_int64),
                 ("precision", C.c_int32), ("slots", C.c_int32), ("step_issued_flops", C.c_double),
-                ("fine_rows", C.c_int64), ("tail_iterations", C.c_int64)]
+                ("fine_rows", C.c_int64), ("tail_iterations", C.c_int64), ("exchange_ms", C.c_double),
+                ("exchange_calls", C.c_int64)]
 
 
 class IterationRecord(C.Structure):
@@ -84,6 +87,8 @@ SIGNATURES = {
     "oica_set_data": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64]),
     "oica_set_data_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64]),
     "oica_init_candidates": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64]),
+    "oica_distribute_data": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                       C.c_int64, C.c_int32]),
     "oica_extract_components": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_uint32,
                                           _P(C.c_double), C.c_int32, _P(Result)]),
     "oica_fixed_point_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
@@ -295,9 +300,18 @@ class Context:
         self.N, self.M = N, M
 
     def set_data_host_ptr(self, ptr: int, N: int, M: int, ld: int, M_global: Optional[int] = None):
-        """Host fp32 buffer by address (pinned torch tensor: tensor.data_ptr())."""
+        """Host fp32 buffer by address (pinned torch tensor: tensor.data_ptr()).  The copy is only
+        enqueued: a pinned buffer must stay valid and unchanged until the next extract /
+        synchronize / set_data* call returns (include/oica.h)."""
         self._c(lib().oica_set_data_host(self.h, ptr, N, M, ld, M if M_global is None else M_global))
         self.N, self.M = N, M
+
+    def distribute_data(self, X_root, N: int, M_global: int, X_out, root: int = 0):
+        """C3: root's device fp32 N x M_global whitened data -> X_out on every rank (replicated for
+        L-shard / hybrid, this rank's column block for M-shard).  X_root may be None off root."""
+        self._c(lib().oica_distribute_data(self.h, _dptr(X_root) if X_root is not None else None, N, M_global,
+                                           X_root.stride(0) if X_root is not None else M_global, _dptr(X_out),
+                                           X_out.stride(0), root))
 
     def init_candidates(self, seed: int, L: int):
         self._c(lib().oica_init_candidates(self.h, seed & 0xFFFFFFFFFFFFFFFF, L))

@@ -9,7 +9,9 @@ in the bench's launch configuration (AUTO precision: tensor cores for M >= 16384
 Gates (north_star): identical accepted indices, |cos| >= 0.9999, objective rel. error <= 1e-4.
   * teacher-forced: component k is extracted with the oracle's accepted rows 1..k-1 as the
     prefix (an oracle value, not a GPU one), so one near-tie cannot cascade;
-  * free-running: compared until the first component the oracle or the GPU flags as a near-tie.
+  * free-running: every component must match (no stored golden has a near-tie; SURVEY §8(c)
+    lets only a near-tie the ORACLE flags excuse the index gate, and the objective is still
+    checked on such a component).
 """
 import glob
 import hashlib
@@ -67,18 +69,22 @@ def test_gpu_matches_oracle_golden(path):
         # teacher-forced, one component per call
         for k, c in enumerate(comps):
             r = ctx.extract(k + 1, cfg.K, cfg.tol, W_prefix=Wg[:k] if k else None)
-            if r.index[k] != c["index"] and (c["near_tie"] or r.near_tie[k]):
+            if r.index[k] != c["index"] and c["near_tie"]:   # oracle-flagged tie: objective still gated
+                rel = abs((r.alpha[k] + 3.0) - (c["alpha"] + 3.0)) / abs(c["alpha"] + 3.0)
+                assert rel <= 1e-4, (k, rel)
                 continue
             d, rel = _gate(k, int(r.index[k]), r.W[k], float(r.alpha[k]), c)
             worst = [max(worst[0], d), max(worst[1], rel)]
-        # free-running
+        # free-running: all components
         r = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
+        assert r.n_extracted == len(comps)
         matched = 0
         for k, c in enumerate(comps):
-            if c["near_tie"] or r.near_tie[k]:
+            if c["near_tie"] and r.index[k] != c["index"]:   # later components run on another prefix
                 break
             _gate(k, int(r.index[k]), r.W[k], float(r.alpha[k]), c)
             matched += 1
+        assert matched == len(comps) or any(c["near_tie"] for c in comps), (matched, len(comps))
         prec = ctx.stats()["precision"]
     print(os.path.basename(path), "precision", prec, "components", len(comps), "free-running matched", matched,
           "worst 1-cos", worst[0], "worst rel", worst[1])

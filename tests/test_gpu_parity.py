@@ -153,7 +153,13 @@ def test_iteration_log(name, flags):
         assert all(r["flops"] == pytest.approx(r["L_act"] * (4 * d + 3) * cfg.M) for r in recs)
 
 
-def _compare(res_gpu, res_or, W_or, X64, allow_near_tie=True):
+def _compare(res_gpu, res_or, W_or, X64, st_or=None):
+    """Free-running comparison with the oracle (SURVEY §8(c) parity protocol): identical indices,
+    |cos| >= 0.9999, objective rel. error <= 1e-4 on every component.  An index mismatch is excused
+    only where the ORACLE flags a near-tie (reading A6); that component is still checked -- its
+    objective against the oracle's and the GPU's accepted row against the oracle's own end state of
+    the GPU's candidate (st_or: the oracle's candidate states) -- and the comparison ends there,
+    since later components run on a different prefix (the teacher-forced tests cover them)."""
     idx_g = list(res_gpu.index[: res_gpu.n_extracted])
     idx_o = [r.index for r in res_or]
     report = []
@@ -164,11 +170,14 @@ def _compare(res_gpu, res_or, W_or, X64, allow_near_tie=True):
         obj_g, obj_o = res_gpu.alpha[k] + 3.0, r.alpha + 3.0
         rel = abs(obj_g - obj_o) / abs(obj_o)
         report.append((k + 1, idx_g[k], idx_o[k], cos, rel))
+        assert rel <= 1e-4, report
         if idx_g[k] != idx_o[k]:
-            assert allow_near_tie and (r.near_tie or res_gpu.near_tie[k]), report
+            assert r.near_tie, ("index mismatch without an oracle near-tie", report)
+            assert st_or is not None, ("oracle near-tie: candidate end states needed to check it", report)
+            wq = st_or[k].W[int(idx_g[k])]
+            assert abs(float(res_gpu.W[k] @ wq)) >= 0.9999, ("GPU row is not the oracle's end state of q", report)
             return report
         assert cos >= 0.9999, report
-        assert rel <= 1e-4, report
     return report
 
 
@@ -189,12 +198,13 @@ def test_extract_parity(name, precision):
     if name in LARGE_M:
         assert used in TC_MODES and (precision != oica.PREC_TC_SPLIT or used == oica.PREC_TC_SPLIT)
     assert res.n_extracted == cfg.N_out
-    rep = _compare(res, res_or, W_or, X64)
+    W_or, res_or, st_or = oracle_run(name)
+    rep = _compare(res, res_or, W_or, X64, st_or)
     assert np.abs(res.W @ res.W.T - np.eye(cfg.N_out)).max() < 1e-10
-    # the convergence census is exact up to candidates sitting at d ~ tol; at small M the tensor-core
-    # path's fp16 rounding noise (~2^-12/sqrt(M) in G) leaves more of them unconverged
-    loose = used in TC_MODES and cfg.M < 131072
-    slack = cfg.L // 2 if loose else max(2, cfg.L // 50)
+    # convergence census: every run converges in both arithmetics on these workloads (K = 200 is
+    # far above the iteration counts), so the counts agree up to runs whose step distance sits at
+    # d ~ tol in the last iterations; 2% of L (reading A28)
+    slack = max(2, cfg.L // 50)
     for k, r in enumerate(res_or):
         assert res.n_degenerate[k] == r.n_degenerate
         assert abs(int(res.n_converged[k]) - r.n_converged) <= slack, (k, res.n_converged[k], r.n_converged)
@@ -202,6 +212,39 @@ def test_extract_parity(name, precision):
         assert bool(res.gaussian_flag[k]) == r.gaussian_flag
     assert st["kernel_launches"] > 0 and st["step_launches"] > 0
     print(name, used, rep, [(int(a), b.n_converged) for a, b in zip(res.n_converged, res_or)])
+
+
+@pytest.mark.parametrize("precision", [oica.PREC_AUTO, oica.PREC_TC_SPLIT])
+def test_fp16_range_spike_source(precision):
+    """A sparse spike source Bernoulli(1e-4) N(0,25) (EEG-artifact-like, kappa ~ 3e4) reaches |y| = 242
+    after whitening: y^3 2^-6 = 2.2e5 would overflow fp16 (65504) in the tensor-core GEMM2 operand
+    without the range shift (DESIGN.md §5 "range").  It is the most non-Gaussian direction, so
+    Theorem 1 extracts it first; every component meets the oracle gates."""
+    cfg, ctx = ctx_for("p_spike", precision)
+    _, _, X64 = prepared("p_spike")
+    W_or, res_or, st_or = oracle_run("p_spike")
+    assert np.abs(W_or[0] @ X64).max() > 4 * 65504 ** (1 / 3)   # the regime that overflowed (|y| > 161)
+    with ctx:
+        res = ctx.extract(cfg.N_out, cfg.K, cfg.tol)
+        assert ctx.stats()["precision"] in TC_MODES
+    _compare(res, res_or, W_or, X64, st_or)
+    assert res.index[0] == res_or[0].index and res.alpha[0] > 1e4
+    assert all(res.n_converged[k] >= cfg.L - 2 for k in range(cfg.N_out))
+
+
+@pytest.mark.parametrize("precision", [oica.PREC_FP32, oica.PREC_TC])
+def test_nonfinite_data_fails_loudly(precision):
+    """A non-finite sample makes every update non-finite: the extraction fails with
+    OICA_ERR_NONFINITE instead of retiring the rows silently (DESIGN.md §5 "range")."""
+    cfg, X32, _ = prepared("p_n40")
+    Xb = X32.copy()
+    Xb[3, 777] = np.nan
+    with oica.Context(0, precision) as ctx:
+        ctx.set_data(torch.from_numpy(Xb).cuda())
+        ctx.init_candidates(cfg.cand_seed, 64)
+        with pytest.raises(oica.OicaError) as e:
+            ctx.extract(1, cfg.K, cfg.tol)
+    assert e.value.name == "NONFINITE"
 
 
 def test_teacher_forced_prefix():
@@ -213,8 +256,9 @@ def test_teacher_forced_prefix():
     res = ctx.extract(cfg.N_out, cfg.K, cfg.tol, W_prefix=W_or[:k])
     assert np.array_equal(res.W[:k], W_or[:k])
     for j in range(k, cfg.N_out):
-        assert res.index[j] == res_or[j].index or res_or[j].near_tie
+        assert res.index[j] == res_or[j].index and not res_or[j].near_tie
         assert abs(res.W[j] @ W_or[j]) >= 0.9999
+        assert abs((res.alpha[j] + 3.0) - (res_or[j].alpha + 3.0)) <= 1e-4 * (res_or[j].alpha + 3.0)
 
 
 def test_candidate_end_state_parity():
@@ -325,7 +369,8 @@ def test_extract_parity_reduced(name, precision):
     res = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=oica.REDUCE_X)
     assert res.n_extracted == cfg.N_out
     assert list(res.dim[: cfg.N_out]) == [cfg.N - k for k in range(cfg.N_out)]
-    rep = _compare(res, res_or, W_or, X64)
+    W_or, res_or, st_or = oracle_run(name)
+    rep = _compare(res, res_or, W_or, X64, st_or)
     assert np.abs(res.W @ res.W.T - np.eye(cfg.N_out)).max() < 1e-10
     for k, r in enumerate(res_or):
         assert bool(res.gaussian_flag[k]) == r.gaussian_flag
@@ -358,7 +403,7 @@ def test_reduced_wide_tile_widths(N, k, precision):
     assert list(res.dim[k:k + 2]) == [N - k, N - k - 1]
     for j, r in enumerate(res_or):
         for out in (res, full):
-            assert out.index[k + j] == r.index or r.near_tie, (j, out.index[k + j], r.index)
+            assert out.index[k + j] == r.index or r.near_tie, (j, out.index[k + j], r.index)   # oracle flag only
             assert abs(out.W[k + j] @ W_or[k + j]) >= 0.9999
             assert abs((out.alpha[k + j] + 3) - (r.alpha + 3)) <= 1e-4 * (r.alpha + 3)
     assert np.abs(res.W[k:] @ Wp.T).max() < 1e-10
@@ -402,7 +447,7 @@ def test_paper_experiment_parity(name, L):
                 # outcome (ii)), so q = min C may differ; the cluster (direction) is unique: the
                 # GPU's q must end, in the oracle, on the accepted optimum.
                 wq = st_or[k].W[int(out.index[k])]
-                assert 1.0 - abs(wq @ W_or[k]) <= 1e-6 or r.near_tie or out.near_tie[k], (k, out.index[k], r.index)
+                assert 1.0 - abs(wq @ W_or[k]) <= 1e-6 or r.near_tie, (k, out.index[k], r.index)
                 assert st_or[k].iters[int(out.index[k])] >= cfg.K - 3 or st_or[k].iters[r.index] >= cfg.K - 3
     print(name, L, "estimated non-Gaussian sources", res.n_extracted, "index matches",
           int(np.sum(res.index[:n] == np.array([r.index for r in res_or[:n]]))), "/", n)
@@ -426,8 +471,9 @@ def test_exchange_paths_single_rank(name, precision, shard):
     # hybrid: the last <= 128 active runs of every component go through the gather / M-sharded
     # tail / scatter path (tail slot plan: within tolerance of the L-shard result)
     assert (tail > 0) == (shard == oica.SHARD_HYBRID)
+    W_or, res_or, st_or = oracle_run(name)
     for out in (res, red):
-        _compare(out, res_or, W_or, X64)
+        _compare(out, res_or, W_or, X64, st_or)
     if shard == oica.SHARD_L:   # the exchange does not change the arithmetic: bitwise equal
         with oica.Context(0, precision) as ctx:
             ctx.set_data(torch.from_numpy(X32).cuda())
@@ -480,7 +526,8 @@ json.dump({"a4": a4, "W": np.asarray(r.W).tolist(), "index": [int(v) for v in r.
         assert abs((d["a4"][k] + 3) - (res_or4[k].alpha + 3)) <= 1e-3 * abs(res_or4[k].alpha + 3), (k, d["a4"][k])
     W_or, res_or, _ = oracle_run("p_tc_n128")
     for k in range(d["n"]):
-        if res_or[k].near_tie or d["near_tie"][k]:
+        if res_or[k].near_tie and d["index"][k] != int(res_or[k].index):   # oracle-flagged tie only
+            assert abs((d["alpha"][k] + 3) - (res_or[k].alpha + 3)) <= 1e-4 * abs(res_or[k].alpha + 3)
             break
         assert d["index"][k] == int(res_or[k].index)
         assert abs(float(np.dot(d["W"][k], W_or[k]))) >= 0.9999
@@ -500,7 +547,7 @@ def test_shape_edge_cases(N, M, L, N_out, precision):
     Xw, _, _, _ = whiten.whiten(ds.X.numpy())
     X32 = np.ascontiguousarray(Xw.astype(np.float32))
     X64 = X32.astype(np.float64)
-    W_or, res_or = ordering.extract(X64, L, cfg.K, cfg.tol, N_out, cfg.cand_seed)
+    W_or, res_or, st_or = ordering.extract(X64, L, cfg.K, cfg.tol, N_out, cfg.cand_seed, keep_candidates=True)
     with oica.Context(0, precision) as ctx:
         ctx.set_data(torch.from_numpy(X32).cuda())
         ctx.init_candidates(cfg.cand_seed, L)
@@ -508,7 +555,7 @@ def test_shape_edge_cases(N, M, L, N_out, precision):
         red = ctx.extract(N_out, cfg.K, cfg.tol, flags=oica.REDUCE_X)
     for out in (res, red):
         assert out.n_extracted == N_out
-        _compare(out, res_or, W_or, X64)
+        _compare(out, res_or, W_or, X64, st_or)
 
 
 # ---- degenerate settings of the method: one candidate (L = 1, the textbook one-unit iteration),
@@ -525,7 +572,7 @@ def test_degenerate_settings(N, M, L, N_out, K, precision):
     Xw, _, _, _ = whiten.whiten(ds.X.numpy())
     X32 = np.ascontiguousarray(Xw.astype(np.float32))
     X64 = X32.astype(np.float64)
-    W_or, res_or = ordering.extract(X64, L, K, cfg.tol, N_out, cfg.cand_seed)
+    W_or, res_or, st_or = ordering.extract(X64, L, K, cfg.tol, N_out, cfg.cand_seed, keep_candidates=True)
     with oica.Context(0, precision) as ctx:
         ctx.set_data(torch.from_numpy(X32).cuda())
         ctx.init_candidates(cfg.cand_seed, L)
@@ -533,7 +580,7 @@ def test_degenerate_settings(N, M, L, N_out, K, precision):
         assert res.n_extracted == N_out
         assert np.allclose(res.W[:N_out] @ res.W[:N_out].T, np.eye(N_out), atol=1e-9)   # deflation
         if K > 1:
-            _compare(res, res_or, W_or, X64)
+            _compare(res, res_or, W_or, X64, st_or)
             return
         # K = 1: nothing converges in one update (unless the feasible set is {+-w}), so every run
         # counts as unconverged and the selection runs over all of them (A4).  Unconverged end

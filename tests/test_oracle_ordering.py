@@ -20,7 +20,7 @@ from scipy.optimize import minimize
 
 import datagen
 from datagen import Config
-from oracle import contrast, fastica, metrics, ordering, reduced, select, whiten
+from oracle import contrast, fastica, metrics, ordering, reduced, rng, select, whiten
 
 
 def _prep(cfg, M=None, seed=None):
@@ -280,3 +280,95 @@ def test_metric_worked_examples():
     runs = [np.array([[math.cos(t), math.sin(t)]]) for t in (0, math.pi / 3, 2 * math.pi / 3)]
     assert metrics.fluctuation(runs)[0] == pytest.approx(0.5)
     assert metrics.amari_rows(np.eye(3)[:2] * [[2.0], [-1.0]]) == 0
+
+
+# ---- reading A4 pinned against the literal algorithms (Alg. 1: every FastICA
+# run returns after at most K updates and the argmax runs over ALL L runs
+# Alg. 2: the argmax runs over B_conv only).  The reference below is the per-candidate FastICA
+# function of PAPER.md:149-165 (oracle.fastica.fastica_one_unit) followed by the paper's plain
+# argmax p = argmax_l Upsilon(alpha_l) written out here (ties -> lowest l): no eligibility code,
+# no cluster rule (O1 is run with raw_argmax, the paper's p itself).
+def _literal_component(X, W_acc, i, seed, L, K, tol, over):
+    N, M = X.shape
+    E = W_acc.T @ W_acc if W_acc.shape[0] else np.zeros((N, N))
+    R = rng.candidates(seed, i, np.arange(L), N)
+    ws, alphas, its, conv = [], [], [], []
+    for l in range(L):
+        w, y, t, c = fastica.fastica_one_unit(R[l], X, E, K, tol)
+        ws.append(w)
+        alphas.append(np.sum(y ** 4) / M - 3.0)
+        its.append(t)
+        conv.append(c)
+    alphas, conv = np.array(alphas), np.array(conv)
+    ups = alphas - 2.0 * np.log(alphas / 2.0 + 1.0)                   # eq. (1)
+    pool = np.arange(L) if over == "all" else np.nonzero(conv)[0]      # Alg. 1: all runs; Alg. 2: B_conv
+    p = int(pool[np.argmax(ups[pool])])                               # PAPER.md:142 / :259
+    return p, ws[p], alphas[p], np.array(its), conv
+
+
+@pytest.mark.parametrize("K", [1, 3, 5, 9])   # K = 9: some runs converged, some not
+def test_include_unconverged_is_literal_alg1(K):
+    """OICA_INCLUDE_UNCONVERGED (O1 include_unconverged=True) is Algorithm 1's selection: argmax
+    over every run after <= K updates, converged or not."""
+    cfg = datagen.PARITY["p_ragged"].with_(L=60)
+    X, _, _ = _prep(cfg)
+    W1, r1 = ordering.extract(X, cfg.L, K, cfg.tol, 2, cfg.cand_seed, include_unconverged=True, raw_argmax=True)
+    W_acc = np.zeros((0, cfg.N))
+    for k in range(2):
+        p, w, a, its, conv = _literal_component(X, W_acc, k + 1, cfg.cand_seed, cfg.L, K, cfg.tol, "all")
+        assert r1[k].index == p
+        assert 1.0 - abs(float(r1[k].w @ w)) <= 1e-9 and abs(r1[k].alpha - a) <= 1e-9 * abs(a + 3.0)
+        assert r1[k].n_converged == int(conv.sum())
+        W_acc = np.vstack([W_acc, select.canonical_sign(w)[None, :]])
+    assert np.abs(W1 - W_acc).max() < 1e-9
+
+
+@pytest.mark.parametrize("K", [7, 9, 12])
+def test_default_excludes_unconverged_as_alg2(K):
+    """The default (reading A4) is Algorithm 2's selection: argmax over B_conv only,
+    at a cap where some runs converge and some do not."""
+    cfg = datagen.PARITY["p_ragged"].with_(L=60)
+    X, _, _ = _prep(cfg)
+    W1, r1 = ordering.extract(X, cfg.L, K, cfg.tol, 2, cfg.cand_seed, raw_argmax=True)
+    W_acc = np.zeros((0, cfg.N))
+    for k in range(2):
+        p, w, a, its, conv = _literal_component(X, W_acc, k + 1, cfg.cand_seed, cfg.L, K, cfg.tol, "conv")
+        assert 0 < conv.sum() < cfg.L, "the cap must leave some runs unconverged for this pin"
+        assert not r1[k].no_converged and r1[k].index == p
+        assert 1.0 - abs(float(r1[k].w @ w)) <= 1e-9 and abs(r1[k].alpha - a) <= 1e-9 * abs(a + 3.0)
+        W_acc = np.vstack([W_acc, select.canonical_sign(w)[None, :]])
+
+
+def test_no_converged_fallback_is_literal_alg1():
+    """K = 1: no run can converge in one update, B_conv is empty; reading A4's fallback (all runs
+    compete, flagged no_converged) is then Algorithm 1's argmax over all runs."""
+    cfg = datagen.PARITY["p_ragged"].with_(L=60)
+    X, _, _ = _prep(cfg)
+    W1, r1 = ordering.extract(X, cfg.L, 1, cfg.tol, 2, cfg.cand_seed, raw_argmax=True)
+    W_acc = np.zeros((0, cfg.N))
+    for k in range(2):
+        p, w, a, its, conv = _literal_component(X, W_acc, k + 1, cfg.cand_seed, cfg.L, 1, cfg.tol, "all")
+        assert not conv.any() and r1[k].no_converged and r1[k].n_converged == 0
+        assert r1[k].index == p and 1.0 - abs(float(r1[k].w @ w)) <= 1e-9
+        W_acc = np.vstack([W_acc, select.canonical_sign(w)[None, :]])
+
+
+def test_algorithmic_flops_counts_every_row_update():
+    """F_alg = sum_t L_act(t) (4NM + 3M): every run is active in exactly the
+    iterations that update it, so sum_t L_act(t) = sum_l t_l with t_l the per-run update counts of
+    the literal per-candidate loop; 4NM + 3M is the flop count of one update
+    (y = w X: 2NM, y^3: 2M, X y^3: 2NM, and y^4 for alpha: M)."""
+    cfg = datagen.PARITY["p_ragged"].with_(L=40)
+    X, _, _ = _prep(cfg)
+    N, M = X.shape
+    for K in (2, 200):
+        W1, r1 = ordering.extract(X, cfg.L, K, cfg.tol, 2, cfg.cand_seed, raw_argmax=True)
+        W_acc = np.zeros((0, N))
+        total = 0
+        for k in range(2):
+            p, w, a, its, conv = _literal_component(X, W_acc, k + 1, cfg.cand_seed, cfg.L, K, cfg.tol, "all")
+            assert r1[k].sum_active == int(its.sum()) and r1[k].n_iter == int(its.max())
+            total += int(its.sum())
+            W_acc = np.vstack([W_acc, r1[k].w[None, :]])
+        assert ordering.algorithmic_flops(r1, N, M) == float(total) * (4.0 * N * M + 3.0 * M)
+        assert ordering.algorithmic_flops(r1, N, M) == float(total) * (2 * N * M + 2 * M + 2 * N * M + M)
