@@ -14,6 +14,17 @@ are larger than L2, so no flush is needed between steps.
 --impl reference times the float64 CPU oracle (the reference arm for this tier) on a bounded
 sample of the same workload.  Multi-GPU: launch under torchrun; L-shard (candidates split,
 one NCCL exchange per component).  One JSON line is printed by rank 0.
+
+Data (--data): `golden` (default) regenerates on the host exactly the raw signals of the
+config's stored oracle golden (tests/golden/oracle_<cfg>.json, written by scripts/make_golden.py
+from oracle/ + datagen/), whitens them on the device (oica_whiten) and, after the run, compares
+the all-components leg's accepted indices / rows / objectives with the stored oracle results
+(`golden_match`; the file is read as data, no oracle code runs).  `device` draws the same recipe
+with the device generator (faster set-up, a different draw, no golden).  Under torchrun rank 0
+prepares the data and oica_distribute_data broadcasts it (C3).
+
+The product library only: bench.py refuses to run when OICA_LIB or an experiment variable of
+the -DOICA_EXPERIMENTS build is set.
 """
 from __future__ import annotations
 
@@ -34,6 +45,48 @@ DEFAULT_CONFIG = "cfg4_scaling"
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+# experiment knobs of the -DOICA_EXPERIMENTS build (compiled out of liboica.so); OICA_LIB selects
+# another library build.  A bench line is only ever taken on the product library with none set.
+EXPERIMENT_VARS = ("OICA_LIB", "OICA_TC_EPI", "OICA_TC_CL", "OICA_TC_RING", "OICA_TC_FORCE_LO", "OICA_TC_MIXED",
+                   "OICA_TC_MIXED_SMS", "OICA_TC_GREEN", "OICA_GREEN_SMS", "OICA_SLOT_TARGET", "OICA_MIN_SLOTS",
+                   "OICA_PROMOTE_D", "OICA_PROMOTE_RATIO", "OICA_PROMOTE_T")
+
+
+def refuse_experiments():
+    bad = [v for v in EXPERIMENT_VARS if os.environ.get(v) is not None]
+    if bad:
+        sys.stderr.write(f"bench.py: refusing to run with experiment variables set: {bad}\n")
+        sys.exit(2)
+
+
+def golden_path(cfg):
+    """The stored oracle golden whose data seed is the config's own (tier A full L, tier B L'=256)."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "oracle_*.json"))):
+        try:
+            with open(p) as f:
+                head = json.loads(f.read())
+        except Exception:
+            continue
+        if head.get("config") == cfg.name and head.get("data_seed") == cfg.data_seed and \
+                head.get("cand_seed") == cfg.cand_seed:
+            return p
+    return None
+
+
+def golden_match(path, W, index, alpha, n):
+    """Compare the all-components leg with the stored oracle results (north_star gates)."""
+    import numpy as np
+    g = json.load(open(path))
+    comps = g["components"][:n]
+    same = sum(int(index[k]) == c["index"] for k, c in enumerate(comps))
+    cos = [abs(float(np.dot(W[k], c["w"]))) for k, c in enumerate(comps)]
+    rel = [abs((alpha[k] + 3.0) - (c["alpha"] + 3.0)) / abs(c["alpha"] + 3.0) for k, c in enumerate(comps)]
+    return {"golden": os.path.relpath(path, ROOT), "golden_L": g["L"], "components": len(comps),
+            "index_match": same, "min_abs_cos": min(cos) if cos else None, "max_objective_rel_err": max(rel) if rel else None,
+            "pass": bool(same == len(comps) and comps and min(cos) >= 0.9999 and max(rel) <= 1e-4)}
 
 
 def dist_env():
@@ -114,8 +167,8 @@ def cpu_baseline(cfg, n_steps: int = 1, M_sample: int = 200_000, L_sample: int =
     """Time the float64 oracle (as it stands) on a bounded sample of the workload.
 
     The sample's raw signals come from the seeded generator (on the GPU when present, only for
-    speed); whitening and the extraction are the oracle's.  BLAS threads: half the host cores
-    (OpenBLAS with one thread per logical core hits threading pathologies on skinny products)."""
+    speed); whitening and the extraction are the oracle's.  BLAS threads: every core of the
+    process's affinity set (reported as `cores`)."""
     import numpy as np
     import torch
     from threadpoolctl import threadpool_info, threadpool_limits
@@ -128,7 +181,7 @@ def cpu_baseline(cfg, n_steps: int = 1, M_sample: int = 200_000, L_sample: int =
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     ds = datagen.make_dataset(cfg, M=M_s, keep_sources=False, device=dev)
     Xraw = ds.X.cpu().numpy()
-    threads = max(1, len(os.sched_getaffinity(0)) // 2)
+    threads = max(1, len(os.sched_getaffinity(0)))   # every host core the process may use
     with threadpool_limits(threads, user_api="blas"):
         Xw, _, _, _ = whiten.whiten(Xraw)
         X = Xw.astype(np.float32).astype(np.float64)
@@ -195,22 +248,40 @@ def run_oica(args, cfg):
     prec = {"auto": oica.PREC_AUTO, "fp32": oica.PREC_FP32, "tc": oica.PREC_TC,
             "tc_split": oica.PREC_TC_SPLIT}[args.precision]
     shard = {"l": oica.SHARD_L, "m": oica.SHARD_M, "hybrid": oica.SHARD_HYBRID}[args.shard]
+    t_ctx = time.perf_counter()
     ctx = oica.Context(local, prec, rank, world, shard, stream=stream, nccl_id=nid)
 
-    # synthetic inputs of the config's recipe, generated and whitened on the device (not timed)
+    comm_init_s = time.perf_counter() - t_ctx
+    # synthetic inputs of the config's recipe (not timed): rank 0 draws the raw signals (the
+    # golden's host draw, or the device generator), whitens them on the device with oica_whiten
+    # and distributes Xw to every rank (oica_distribute_data, C3)
     t0 = time.perf_counter()
-    ds = datagen.make_dataset(cfg, device=dev, dtype=torch.float32, keep_sources=False)
-    X = ds.X.contiguous()
-    del ds
-    Xw = torch.empty_like(X)
-    ctx.whiten(X, Xw)
-    del X
-    torch.cuda.synchronize()
+    gpath = golden_path(cfg) if args.data == "golden" else None
+    if args.data == "golden" and gpath is None:
+        raise SystemExit(f"bench.py: no stored golden for {cfg.name}; use --data device")
     M_local = cfg.M
     if shard == oica.SHARD_M and world > 1:
-        lo, hi = cfg.M * rank // world, cfg.M * (rank + 1) // world
-        Xw = Xw[:, lo:hi].contiguous()
-        M_local = hi - lo
+        M_local = cfg.M * (rank + 1) // world - cfg.M * rank // world
+    Xw_root = None
+    if rank == 0:
+        if gpath is not None:   # host draw of the golden's raw signals (fp64 generator, fp32 upload)
+            ds = datagen.make_dataset(cfg, keep_sources=False)
+            X = ds.X.to(torch.float32).contiguous().to(dev)
+        else:
+            ds = datagen.make_dataset(cfg, device=dev, dtype=torch.float32, keep_sources=False)
+            X = ds.X.contiguous()
+        del ds
+        Xw_root = torch.empty_like(X)
+        ctx.whiten(X, Xw_root)
+        del X
+        torch.cuda.synchronize()
+    if shard == oica.SHARD_M and world > 1:
+        Xw = torch.empty(cfg.N, M_local, dtype=torch.float32, device=dev)
+    else:
+        Xw = Xw_root if rank == 0 else torch.empty(cfg.N, cfg.M, dtype=torch.float32, device=dev)
+    ctx.distribute_data(Xw_root, cfg.N, cfg.M, Xw)
+    if Xw_root is not None and Xw_root.data_ptr() != Xw.data_ptr():
+        del Xw_root
     ctx.set_data(Xw, M_global=cfg.M)
     ctx.init_candidates(cfg.cand_seed, cfg.L)
     setup_s = time.perf_counter() - t0
@@ -250,7 +321,8 @@ def run_oica(args, cfg):
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    ms = e0.elapsed_time(e1)
+    ms_local = e0.elapsed_time(e1)
+    ms = ms_local
     st = ctx.stats()
     timed = recs[args.warmup:]
     M = cfg.M
@@ -314,6 +386,19 @@ def run_oica(args, cfg):
         aflops = sum(int(ra.sum_active[k]) * (4.0 * dims[k] * cfg.M + 3.0 * cfg.M) for k in range(ra.n_extracted))
         all_leg = {"seconds": ams / 1e3, "components": int(ra.n_extracted), "value": aflops / (ams / 1e3) / 1e12,
                    "unit": "TFLOP/s", "indices": [int(v) for v in ra.index[: ra.n_extracted]]}
+        if gpath is not None:
+            all_leg["golden_match"] = golden_match(gpath, ra.W, ra.index, ra.alpha, int(ra.n_extracted))
+
+    # per-rank breakdown (multi-GPU diagnosis: step kernel / NCCL exchange / tail, communicator init)
+    st_now = ctx.stats()
+    mine = {"rank": rank, "comm_init_s": comm_init_s, "setup_s": setup_s, "timed_ms": ms_local,
+            "step_ms": st["step_ms"], "exchange_ms": st["exchange_ms"], "exchange_calls": st["exchange_calls"],
+            "iterations": st["iterations"], "tail_iterations": st["tail_iterations"],
+            "kernel_launches": st["kernel_launches"], "all_leg_exchange_ms": st_now["exchange_ms"] - st["exchange_ms"]}
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
 
     if rank != 0:
         ctx.close()
@@ -369,10 +454,13 @@ def run_oica(args, cfg):
                       "parallelism": f"{args.shard}shard{world}",
                       "l2": f"inputs larger than L2 (X = {4 * cfg.N * cfg.M / 1e9:.2f} GB fp32), no flush",
                       "precision": precision, "slots": st["slots"],
-                      "reduced_x": bool(args.reduce)},
+                      "reduced_x": bool(args.reduce), "data_draw": args.data,
+                      "library": "liboica.so (release build: no experiment modes)",
+                      "seconds_all_components": sec_all,
+                      "golden_match": (all_leg or {}).get("golden_match")},
            "seconds_per_component": sec_per_comp, "seconds_all_components": sec_all, "all_components": all_leg,
            "gpu_launches": st["kernel_launches"], "roofline": roof, "e2e": e2e, "cpu_baseline": cb,
-           "clocks": clocks, "components": timed, "setup_s": setup_s}
+           "clocks": clocks, "components": timed, "setup_s": setup_s, "per_rank": per_rank}
     print(json.dumps(out), flush=True)
     ctx.close()
     if world > 1:
@@ -395,9 +483,12 @@ def main():
                     help="time all N_out components (seconds to extract all N); --steps is ignored")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-all", action="store_true", help="skip the all-components leg")
+    ap.add_argument("--data", default="golden", choices=["golden", "device"],
+                    help="golden: the stored oracle golden's host draw (checked against it); device: device draw")
     ap.add_argument("--ref-M", type=int, default=1_000_000)
     ap.add_argument("--ref-L", type=int, default=256)
     args = ap.parse_args()
+    refuse_experiments()
     import datagen
     cfg = datagen.get(args.config)
     if args.impl == "reference":

@@ -1,0 +1,41 @@
+"""Inputs of the stored oracle goldens (tests/golden/oracle_*.json), rebuilt exactly: datagen's
+seeded raw signals on the CPU, whitened by the ORACLE in fp64 and cast to fp32 -- the values the
+oracle consumed when scripts/make_golden.py wrote the golden.  Cached per process: the cfg-4 draw
+takes ~100 s on the host and several GPU test modules use it."""
+import functools
+import hashlib
+import json
+import os
+
+import numpy as np
+
+import datagen
+from oracle import whiten
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def golden(name: str) -> dict:
+    return json.load(open(os.path.join(HERE, "golden", f"oracle_{name}.json")))
+
+
+@functools.lru_cache(maxsize=2)
+def golden_input(name: str):
+    """(cfg, X32) of tests/golden/oracle_<name>.json; cfg carries the golden's L and N_out."""
+    g = golden(name)
+    cfg = datagen.get(g["config"]).with_(data_seed=g["data_seed"], cand_seed=g["cand_seed"], L=g["L"],
+                                         N_out=g["N_out"])
+    ds = datagen.make_dataset(cfg, keep_sources=False)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    del ds
+    X32 = np.ascontiguousarray(Xw.astype(np.float32))
+    del Xw
+    if hashlib.sha256(X32.tobytes()).hexdigest() != g["x32_sha256"]:
+        # BLAS summation order in data generation / whitening may differ between CPUs: accept
+        # last-bit differences (far inside every gate), nothing more
+        fp = g["x32_fingerprint"]
+        rows = X32.astype(np.float64).sum(axis=1)
+        assert np.allclose(rows, fp["row_sums"], rtol=0, atol=1e-5 * np.sqrt(cfg.M)), "input drifted"
+        samp = X32.reshape(-1)[np.asarray(fp["sample_index"])]
+        assert np.allclose(samp, fp["sample_value"], rtol=1e-5, atol=1e-6), "input drifted"
+    return cfg, X32

@@ -3,6 +3,8 @@ maps statuses, refuses non-sm_100 / absent devices, and its host-only selection 
 (reading A6) decides as the oracle's selection rule does."""
 import os
 import re
+import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -140,3 +142,11 @@ def test_slot_plan_host(M):
         ml = -(-M // world)
         ln2, S2 = oica.slot_plan(M, min(ml, M))
         assert ln2 == ln and (S2 - 1) * ln2 < min(ml, M) <= S2 * ln2
+
+
+def test_bench_refuses_experiment_variables():
+    env = dict(os.environ, OICA_TC_EPI="3")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "cfg0_tiny"], capture_output=True,
+                         text=True, timeout=300, cwd=root, env=env)
+    assert out.returncode == 2 and "OICA_TC_EPI" in out.stderr and not out.stdout.strip()

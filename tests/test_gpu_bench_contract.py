@@ -13,9 +13,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(*args):
+def _run(*args, env=None):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
-                         timeout=900, cwd=ROOT)
+                         timeout=900, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
     assert len(lines) == 1, out.stdout
@@ -42,6 +42,10 @@ def test_bench_line_contract():
     a = d["all_components"]   # BASELINE metric's "seconds to extract all N"
     assert d["seconds_all_components"] == a["seconds"] > 0 and a["components"] == 8 and a["value"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert d["config"]["seconds_all_components"] == a["seconds"] and d["config"]["data_draw"] == "golden"
+    g = a["golden_match"]   # the stored tier-A oracle golden of cfg 0 (same data seed, full L)
+    assert g["pass"] and g["index_match"] == 8 == g["components"], g
+    assert d["config"]["golden_match"] == g and len(d["per_rank"]) == 1 and d["per_rank"][0]["step_ms"] > 0
 
 
 def test_reference_arm_contract():

@@ -22,8 +22,7 @@ import numpy as np
 import pytest
 import torch
 
-import datagen
-from oracle import whiten
+from _golden_data import golden_input
 from paper_2408_17118_b200 import oica
 
 pytestmark = pytest.mark.gpu
@@ -32,19 +31,7 @@ GOLDEN = sorted(glob.glob(os.path.join(HERE, "golden", "oracle_*.json")))
 
 
 def _input(g):
-    cfg = datagen.get(g["config"]).with_(data_seed=g["data_seed"], cand_seed=g["cand_seed"], L=g["L"],
-                                         N_out=g["N_out"])
-    ds = datagen.make_dataset(cfg, keep_sources=False)
-    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
-    X32 = np.ascontiguousarray(Xw.astype(np.float32))
-    if hashlib.sha256(X32.tobytes()).hexdigest() != g["x32_sha256"]:
-        # BLAS summation order in data generation / whitening may differ between CPUs: accept
-        # last-bit differences (far inside every gate below), nothing more
-        fp = g["x32_fingerprint"]
-        rows = X32.astype(np.float64).sum(axis=1)
-        assert np.allclose(rows, fp["row_sums"], rtol=0, atol=1e-5 * np.sqrt(cfg.M)), "input drifted"
-        samp = X32.reshape(-1)[np.asarray(fp["sample_index"])]
-        assert np.allclose(samp, fp["sample_value"], rtol=1e-5, atol=1e-6), "input drifted"
+    cfg, X32 = golden_input(g["job"])
     return cfg, X32
 
 
