@@ -288,7 +288,7 @@ def run_oica(args, cfg):
 
     if args.all_components:   # time the whole extraction: components 1..N_out after a warm-up pass
         args.steps = cfg.N_out
-    xflags = oica.REDUCE_X if args.reduce else 0
+    xflags = (oica.REDUCE_X if args.reduce else 0) | (oica.EAGER if args.eager else 0)
     N_out = args.warmup + args.steps
     assert args.all_components or N_out <= cfg.N_out, "warmup + steps exceeds the config's N_out"
     Wacc = np.zeros((cfg.N_out, cfg.N))
@@ -392,7 +392,8 @@ def run_oica(args, cfg):
     # per-rank breakdown (multi-GPU diagnosis: step kernel / NCCL exchange / tail, communicator init)
     st_now = ctx.stats()
     mine = {"rank": rank, "comm_init_s": comm_init_s, "setup_s": setup_s, "timed_ms": ms_local,
-            "step_ms": st["step_ms"], "exchange_ms": st["exchange_ms"], "exchange_calls": st["exchange_calls"],
+            "step_ms": st["step_ms"], "graph_ms": st["graph_ms"], "graph_iterations": st["graph_iterations"],
+            "exchange_ms": st["exchange_ms"], "exchange_calls": st["exchange_calls"],
             "iterations": st["iterations"], "tail_iterations": st["tail_iterations"],
             "kernel_launches": st["kernel_launches"], "all_leg_exchange_ms": st_now["exchange_ms"] - st["exchange_ms"]}
     per_rank = [mine]
@@ -411,6 +412,9 @@ def run_oica(args, cfg):
     precision = {oica.PREC_TC: "tc", oica.PREC_TC_SPLIT: "tc_split"}.get(st["precision"], "fp32")
     kern_tflops = st["step_flops"] / (st["step_ms"] / 1e3) / 1e12 if st["step_ms"] > 0 else None
     issued_tflops = st["step_issued_flops"] / (st["step_ms"] / 1e3) / 1e12 if st["step_ms"] > 0 else None
+    loop_only = kern_tflops is None and st["graph_ms"] > 0   # short iterations: the device-side loop
+    if loop_only:
+        kern_tflops = st["graph_flops"] / (st["graph_ms"] / 1e3) / 1e12
     if precision.startswith("tc"):
         peak = peaks.get("bf16_tflops_sustained") or 1404.1
         passes = 3 if precision == "tc_split" else 2
@@ -431,6 +435,11 @@ def run_oica(args, cfg):
                  "traffic_launch": tr if tr else None,
                  "kernel": "fused fixed-point step (GEMM-cube-GEMM)", "launches": st["step_launches"],
                  "kernel_ms": st["step_ms"], "share_of_step": st["step_ms"] / ms if ms else None})
+    if loop_only:
+        roof.update({"kernel": "device-side iteration loop (CUDA-graph WHILE node: fused step + fused update per "
+                               "iteration; steps not timed one by one -- run with --eager for the step alone)",
+                     "launches": 2 * st["graph_iterations"], "kernel_ms": st["graph_ms"],
+                     "share_of_step": st["graph_ms"] / ms if ms else None})
     if precision.startswith("tc") and kern_tflops:
         # transparency: the sustained figure is cuBLAS bf16 under the power cap (at its own, lower
         # clock); also the burst figure and the dense peak at the clock sampled in this run
@@ -454,7 +463,7 @@ def run_oica(args, cfg):
                       "parallelism": f"{args.shard}shard{world}",
                       "l2": f"inputs larger than L2 (X = {4 * cfg.N * cfg.M / 1e9:.2f} GB fp32), no flush",
                       "precision": precision, "slots": st["slots"],
-                      "reduced_x": bool(args.reduce), "data_draw": args.data,
+                      "reduced_x": bool(args.reduce), "data_draw": args.data, "eager": bool(args.eager),
                       "library": "liboica.so (release build: no experiment modes)",
                       "seconds_all_components": sec_all,
                       "golden_match": (all_leg or {}).get("golden_match")},
@@ -482,6 +491,8 @@ def main():
     ap.add_argument("--all-components", action="store_true",
                     help="time all N_out components (seconds to extract all N); --steps is ignored")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true",
+                    help="host-launched iterations (times every step launch; default: device-side loop where short)")
     ap.add_argument("--no-all", action="store_true", help="skip the all-components leg")
     ap.add_argument("--data", default="golden", choices=["golden", "device"],
                     help="golden: the stored oracle golden's host draw (checked against it); device: device draw")

@@ -122,6 +122,12 @@ typedef struct {
  * the accepted row is w = G^T b.  Same trajectories as the default projection form in exact
  * arithmetic; 4 d M instead of 4 N M flop per row-iteration. */
 #define OICA_REDUCE_X            0x8u
+/* Host-launched iterations.  By default, on one rank, where an iteration is short next to a host
+ * round trip (M x padded N < 1e8: the device-side loop of DESIGN.md §5 "iteration"), the
+ * do-while of PAPER.md:241-256 runs on the device as one CUDA-graph WHILE loop per component
+ * (bitwise the same results); OICA_EAGER launches every iteration from the host instead, which
+ * times each step launch for oica_get_iteration_log / oica_stats.step_ms. */
+#define OICA_EAGER               0x10u
 
 /* Counters of the last extract / step call (for benchmarks; all host values). */
 typedef struct {
@@ -139,6 +145,9 @@ typedef struct {
   int64_t tail_iterations;   /* iterations run in the hybrid tail (OICA_SHARD_HYBRID)        */
   double exchange_ms;        /* CUDA-event time of the NCCL exchanges on the context stream  */
   int64_t exchange_calls;    /* NCCL collectives issued (0 without a communicator)          */
+  int64_t graph_iterations;  /* iterations run by the device-side loop (not in step_ms/step_flops) */
+  double graph_ms;           /* CUDA-event time of those loops (steps and updates together)  */
+  double graph_flops;        /* algorithmic flops of those iterations: sum L_act (4NM + 3M)  */
 } oica_stats;
 
 /* ---- lifetime ---------------------------------------------------------------------- */
@@ -241,7 +250,8 @@ oica_status oica_get_candidates(oica_ctx* ctx, double* W, double* alpha, int32_t
                                 uint8_t* state, int64_t* L_local, int64_t* id_base);
 /* Per-iteration log of the last oica_extract_components call: one record per
  * executed fixed-point iteration of every component on this rank.  step_ms is the CUDA-event
- * time of that iteration's step launch(es) on the context stream; flops its algorithmic work
+ * time of that iteration's step launch(es) on the context stream (-1 for iterations of the
+ * device-side loop, which are not timed one by one: use OICA_EAGER); flops its algorithmic work
  * L_act (4 d + 3) M_local (d = the dimension iterated on).  Copies min(cap, *n) records;
  * *n = the number available (call with cap = 0 to size). */
 typedef struct {
@@ -284,10 +294,13 @@ typedef struct {
  * complement of w = G^T b inside span(G) (rows 2..d of H G, H the reflection taking b to -+e1). */
 oica_status oica_complement_basis(const double* W, int32_t k, int32_t N, double* G);
 /* Host-only: the split-M slot plan of the step kernels (DESIGN.md §5 "HBM layout").  Slot length
- * depends on M_global only (so every row's fp32-per-slot / fp64-across-slot arithmetic is the
- * same for any GPU count, tiling or active-set size) and is a multiple of 384 samples; S_local
- * = ceil(M_local / slot_len) slots cover this rank's samples. */
-oica_status oica_slot_plan(int64_t M_global, int64_t M_local, int64_t* slot_len, int32_t* S_local);
+ * depends on M_global and the precision only (so every row's fp32-per-slot / fp64-across-slot
+ * arithmetic is the same for any GPU count, tiling or active-set size): a multiple of 384 samples
+ * for the tensor-core step; for the FP32 step below 65536 samples, up to 128 slots of >= 128
+ * samples, 64-aligned.  precision: an oica_precision (AUTO resolves as oica_set_data does).
+ * S_local = ceil(M_local / slot_len) slots cover this rank's samples. */
+oica_status oica_slot_plan(int32_t precision, int64_t M_global, int64_t M_local, int64_t* slot_len,
+                           int32_t* S_local);
 /* Host-only: split-slot parts of the tensor-core step (DESIGN.md §5 "few active rows") when
  * L_global runs are active over S slots: P in [1, 8] CTAs share each slot's chunks.  A function
  * of (L_global, S) only; P > 1 only while round_up(ceil(L_global/128), 2) * S <= 148. */

@@ -2,6 +2,8 @@
 // One warp per candidate row for the fp64 row work (N <= 256 -> <= 8 values per lane).
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace oica {
@@ -19,9 +21,9 @@ __device__ __forceinline__ void project_warp(double (&v)[V], const double* __res
 #pragma unroll
   for (int u = 0; u < V; ++u) h[u] = 0.0;
   // rows in blocks of RB: their loads and warp reductions are independent (latency-bound
-  // otherwise when few rows run); same operations in the same order per row.  RB x V bounded
-  // (registers: 8 coordinates per lane already fill them)
-  constexpr int RB = V >= 8 ? 1 : 8 / V;
+  // otherwise when few rows run); same operations in the same order per row (h accumulates the
+  // rows in row order for any RB).  RB x V bounded (registers: 8 coordinates per lane fill them)
+  constexpr int RB = V >= 8 ? 1 : V == 1 ? 16 : 8 / V;
   for (int r0 = 0; r0 < k; r0 += RB) {
     const int nb = min(RB, k - r0);
     double c[RB];
@@ -131,12 +133,21 @@ __device__ __forceinline__ int parts_of(const SlotPartials& Gp, int S) {
 
 // sum over slots (fixed slot order) of the slot partial sums: the definition every consumer of
 // the slot partials shares (epilogue, k_slot_reduce), so a row's G is the same whichever runs it
-template <int D = 8>   // loads in flight per call (callers with many coordinates per lane: fewer)
+// D: loads in flight per call (callers with many coordinates per lane: fewer).  KIND: 0 = the
+// partials' type read at run time, 1 = fp64 partials, 2 = fp32 partials (with split parts): a
+// caller that knows the type compiles one branch (kernel code size: latency of short kernels)
+template <int D = 8, int KIND = 0>
 __device__ __forceinline__ double slot_sum(SlotPartials Gp, int S, int64_t cap, int ldg, int a, int n) {
+  if (KIND == 1) {
+    const double* g = (const double*)Gp.p + (int64_t)a * ldg + n;
+    const int64_t st = cap * ldg;
+    return ordered_sum<D>(S, [&](int s) { return g[s * st]; });
+  }
   const int P = parts_of(Gp, S);
-  if (P > 1) return ordered_sum<D>(S, [&](int s) { return slot_part(Gp, P, s, cap, ldg, a, n); });
+  // split parts: each slot's value already sums up to 8 partials (loads in flight); rolled loop
+  if (P > 1) return ordered_sum<2>(S, [&](int s) { return slot_part(Gp, P, s, cap, ldg, a, n); });
   // one partial per slot (the common case; the loop the whole-L epilogue streams at HBM rate)
-  if (Gp.f32) {
+  if (KIND == 2 || Gp.f32) {
     const float* g = (const float*)Gp.p + (int64_t)a * ldg + n;
     const int64_t st = cap * ldg;
     return ordered_sum<D>(S, [&](int s) { return (double)g[s * st]; });
@@ -146,54 +157,65 @@ __device__ __forceinline__ double slot_sum(SlotPartials Gp, int S, int64_t cap, 
   return ordered_sum<D>(S, [&](int s) { return g[s * st]; });
 }
 
-// coordinate n of the point the contraction used for active row a (master value w64 if none)
-__device__ __forceinline__ double eval_coord(EvalPoint ev, int a, int n, double w64) {
-  int64_t i = (int64_t)a * ev.ld + n;
+// coordinate n of the point the contraction used for candidate l (master value w64 if none)
+__device__ __forceinline__ double eval_coord(const EvalPoint& ev, int l, int n, double w64) {
+  int64_t i = (int64_t)l * ev.ld + n;
   if (ev.hi) return ((double)__half2float(ev.hi[i]) + (ev.lo ? (double)__half2float(ev.lo[i]) : 0.0)) * 0.0625;
   if (ev.f32) return (double)ev.f32[i];
   return w64;
 }
 
-// K3: g = sum_s Gp / M - 3 w_e; g <- g - E g; w = g / ||g||;
-// d = 1 - |w . w_old| as 0.5 ||w - s w_old||^2 (A1/A2); converged iff d <= tol.
-// w_e is the operand the contraction was evaluated at (the whole of eq. (5) at
-// one point, so the map keeps its vanishing tangent Jacobian at the fixed points); w_old is
-// the fp64 master row.
+// Split fp16 operand of one coordinate: w is scaled by 2^4 (|w| <= 1 -> <= 16) so most w_lo stay
+// normal fp16; hi = fp16(2^4 w), lo = fp16(2^4 w - hi) (fine rows; 0 for coarse rows).  hi + lo =
+// 2^4 w to ~2^-22 relative (absolute error <= 3e-8 / 16 per coordinate from lo subnormals).
+__device__ __forceinline__ void operand_f16x2_coord(double w, bool fine_row, __half* hi_out, __half* lo_out) {
+  const double w16 = w * 16.0;
+  const __half hi = __double2half(w16);
+  *hi_out = hi;
+  if (lo_out) *lo_out = fine_row ? __double2half(w16 - (double)__half2float(hi)) : __double2half(0.0);
+}
+
+// K3 core for candidate l, G already summed over the slots (acc[v] = coordinate
+// lane + 32 v): g = G / M - 3 w_e; g <- g - E g; w = g / ||g||; d = 1 - |w . w_old| as
+// 0.5 ||w - s w_old||^2 (A1/A2); converged iff d <= tol.  w_e is the operand the contraction was
+// evaluated at (the whole of eq. (5) at one point, so the map keeps its vanishing
+// tangent Jacobian at the fixed points); w_old is the fp64 master row.  Writes the new master row
+// and, for a row that stays active, its next operand row; returns keep (still active).
+// w_old and w_e of candidate l, coordinates lane + 32 v (loaded ahead of the slot sums)
 template <int V>
-__device__ __forceinline__ void epilogue_row(int a, int lane, const SlotPartials& Gp, const double* __restrict__ s4p,
-                                             int S, int64_t cap, int ldg, const EvalPoint& ev,
-                                             const int* __restrict__ act, const double* __restrict__ Wacc, int k,
-                                             int N, double M, double tol, int t, double* __restrict__ W64,
-                                             double* __restrict__ alpha_old, int* __restrict__ iters,
-                                             uint8_t* __restrict__ state, uint8_t* __restrict__ keep,
-                                             const Promotion& pr) {
-  int l = act[a];
-  double g[V], wo[V];
+__device__ __forceinline__ void load_row(const UpdateArgs& u, int l, int lane, double (&wo)[V], double (&we)[V]) {
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int n = lane + 32 * v;
+    wo[v] = 0.0;
+    we[v] = 0.0;
+    if (n < u.N) {
+      wo[v] = u.W64[(int64_t)l * u.N + n];
+      we[v] = eval_coord(u.ev, l, n, wo[v]);
+    }
+  }
+}
+
+template <int V>
+__device__ __forceinline__ bool epilogue_core(int l, int lane, const double (&acc)[V], double s4_slots,
+                                              const double (&wo)[V], const double (&we)[V], const UpdateArgs& u,
+                                              int k, int t) {
+  const int N = u.N;
+  double g[V];
   double s4g = 0.0;
 #pragma unroll
-  for (int u = 0; u < V; ++u) {
-    int n = lane + 32 * u;
-    double acc = 0.0, w = 0.0, we = 0.0;
-    if (n < N) {
-      acc = slot_sum<(V >= 8 ? 2 : 8 / V)>(Gp, S, cap, ldg, a, n);
-      w = W64[(int64_t)l * N + n];
-      we = eval_coord(ev, a, n, w);
-    }
-    wo[u] = w;
-    s4g += we * acc;
-    g[u] = (n < N) ? acc / M - 3.0 * we : 0.0;           // PAPER.md:244-245 (eq. (5), A3)
+  for (int v = 0; v < V; ++v) {
+    int n = lane + 32 * v;
+    s4g += we[v] * acc[v];
+    g[v] = (n < N) ? acc[v] / u.M - 3.0 * we[v] : 0.0;     // PAPER.md:244-245 (eq. (5), A3)
   }
-  double s4 = 0.0;
-  if (s4p) {
-    if (lane == 0)
-      s4 = ordered_sum(S, [&](int s) { return __ldg(s4p + (int64_t)s * cap + a); });
-  } else {
-    s4 = warp_sum(s4g);   // identity w . sum_m y^3 x = sum_m y^4 (tensor-core path: approximate alpha)
-  }
-  project_warp<V>(g, Wacc, k, N, lane);
+  // SIMT: sum y^4 from its slot partials; TC: the identity w . sum_m y^3 x = sum_m y^4 (approximate alpha)
+  s4g = warp_sum(s4g);
+  const double s4 = u.s4p ? s4_slots : s4g;
+  project_warp<V>(g, u.Wacc, k, N, lane);
   double ss = 0.0;
 #pragma unroll
-  for (int u = 0; u < V; ++u) ss += g[u] * g[u];
+  for (int v = 0; v < V; ++v) ss += g[v] * g[v];
   double nrm = sqrt(warp_sum(ss));
   // a non-finite update (fp16 range failure, non-finite data) retires the row and is reported
   // (Promotion::nonfinite): it must neither keep iterating to the cap nor enter the argmax
@@ -201,52 +223,225 @@ __device__ __forceinline__ void epilogue_row(int a, int lane, const SlotPartials
   bool deg = bad || nrm < kDegenerateNorm;
   double dot = 0.0;
 #pragma unroll
-  for (int u = 0; u < V; ++u) {
-    g[u] = deg ? 0.0 : g[u] / nrm;
-    dot += g[u] * wo[u];
+  for (int v = 0; v < V; ++v) {
+    g[v] = deg ? 0.0 : g[v] / nrm;
+    dot += g[v] * wo[v];
   }
   dot = warp_sum(dot);
   double sg = dot < 0.0 ? -1.0 : 1.0;
   double dd = 0.0;
 #pragma unroll
-  for (int u = 0; u < V; ++u) {
-    double e = g[u] - sg * wo[u];
+  for (int v = 0; v < V; ++v) {
+    double e = g[v] - sg * wo[v];
     dd += e * e;
   }
   dd = 0.5 * warp_sum(dd);
-  bool conv = !deg && dd <= tol;                          // PAPER.md:249-250 (A2)
+  const bool conv = !deg && dd <= u.tol;                    // PAPER.md:249-250 (A2)
+  const bool keep = !deg && !conv;
+  const Promotion& pr = u.pr;
+  bool fine_row = pr.fine == nullptr;                       // (no promotion state: two-pass rows)
+  if (pr.fine) {
+    fine_row = pr.fine[l] != 0;
+    // DESIGN.md §5 precision promotion (decided identically on every lane)
+    if (keep && !fine_row && ((dd <= pr.d_promote && dd > pr.ratio * pr.dprev[l]) || t >= pr.t_force))
+      fine_row = true;
+  }
   if (!deg) {
 #pragma unroll
-    for (int u = 0; u < V; ++u) {
-      int n = lane + 32 * u;
-      if (n < N) W64[(int64_t)l * N + n] = g[u];
+    for (int v = 0; v < V; ++v) {
+      int n = lane + 32 * v;
+      if (n < N) u.W64[(int64_t)l * N + n] = g[v];
+    }
+  }
+  if (keep) {   // next operand row of l (ld coordinates, zero padded); eval reads above came first
+    const int ld = u.ev.ld;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int n = lane + 32 * v;
+      if (n < ld) {
+        const double w = n < N ? g[v] : 0.0;
+        const int64_t i = (int64_t)l * ld + n;
+        if (u.ev.hi)
+          operand_f16x2_coord(w, fine_row, u.ev.hi + i, u.ev.lo ? u.ev.lo + i : nullptr);
+        else if (u.ev.f32)
+          u.ev.f32[i] = (float)w;
+      }
     }
   }
   if (lane == 0) {
     if (bad && pr.nonfinite) atomicAdd(pr.nonfinite, 1);
-    iters[l] = t;
-    alpha_old[l] = s4 / M - 3.0;                          // eq. (2) at w_old (A15)
-    state[l] = deg ? ST_DEGENERATE : (conv ? ST_CONVERGED : ST_ACTIVE);
-    keep[a] = (deg || conv) ? 0 : 1;
-    if (pr.fine && !deg && !conv) {                       // DESIGN.md §5 precision promotion
-      if (!pr.fine[l] && ((dd <= pr.d_promote && dd > pr.ratio * pr.dprev[l]) || t >= pr.t_force)) pr.fine[l] = 1;
+    u.iters[l] = t;
+    u.alpha_old[l] = s4 / u.M - 3.0;                        // eq. (2) at w_old (A15)
+    u.state[l] = deg ? ST_DEGENERATE : (conv ? ST_CONVERGED : ST_ACTIVE);
+    if (pr.fine && keep) {
+      pr.fine[l] = fine_row ? 1 : 0;
       pr.dprev[l] = dd;
     }
   }
+  return keep;
 }
 
-template <int V>
-__global__ void k_epilogue(SlotPartials Gp, const double* __restrict__ s4p, int S, int64_t cap, int ldg,
-                           EvalPoint ev, const int* __restrict__ act, int L_act, const double* __restrict__ Wacc,
-                           int k, int N, double M, double tol, int t, double* __restrict__ W64,
-                           double* __restrict__ alpha_old, int* __restrict__ iters, uint8_t* __restrict__ state,
-                           uint8_t* __restrict__ keep, Promotion pr, const int* __restrict__ cnt) {
-  int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  int lane = threadIdx.x & 31;
-  if (cnt) L_act = min(L_act, cnt[0]);   // device count when the grid is an upper bound
-  if (a >= L_act) return;
-  epilogue_row<V>(a, lane, Gp, s4p, S, cap, ldg, ev, act, Wacc, k, N, M, tol, t, W64, alpha_old, iters, state, keep,
-                  pr);
+// Order-preserving compaction by one block (deterministic), stably partitioned into coarse rows
+// followed by fine rows; act_in null: the identity list.  Each thread takes a contiguous run of
+// positions; counts are scanned with warp shuffles and one warp over the warp totals.  Returns
+// (n_coarse + n_fine, n_coarse) in every thread.
+__device__ __forceinline__ int2 compact_block(const int* __restrict__ act_in, const uint8_t* __restrict__ keep,
+                                              const uint8_t* __restrict__ fine, int L_in, int* __restrict__ act_out) {
+  __shared__ int wc[32], wf[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (blockDim.x + 31) >> 5;
+  const int per = (L_in + blockDim.x - 1) / blockDim.x;
+  const int b = t * per, e = min(L_in, b + per);
+  int cc = 0, cf = 0;
+  for (int a = b; a < e; ++a) {
+    if (!keep[a]) continue;
+    int id = act_in ? act_in[a] : a;
+    if (fine && fine[id]) ++cf; else ++cc;
+  }
+  int ic = cc, jf = cf;   // inclusive warp scans of (cc, cf)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int vc = __shfl_up_sync(0xffffffffu, ic, o), vf = __shfl_up_sync(0xffffffffu, jf, o);
+    if (lane >= o) {
+      ic += vc;
+      jf += vf;
+    }
+  }
+  if (lane == 31) {
+    wc[w] = ic;
+    wf[w] = jf;
+  }
+  __syncthreads();
+  if (w == 0) {   // inclusive scan of the warp totals
+    int xc = lane < nw ? wc[lane] : 0, xf = lane < nw ? wf[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int vc = __shfl_up_sync(0xffffffffu, xc, o), vf = __shfl_up_sync(0xffffffffu, xf, o);
+      if (lane >= o) {
+        xc += vc;
+        xf += vf;
+      }
+    }
+    wc[lane] = xc;
+    wf[lane] = xf;
+  }
+  __syncthreads();
+  const int n_coarse = wc[nw - 1], n_fine = wf[nw - 1];
+  const int base_c = (w ? wc[w - 1] : 0) + ic - cc, base_f = (w ? wf[w - 1] : 0) + jf - cf;
+  int pc = base_c, pf = n_coarse + base_f;
+  for (int a = b; a < e; ++a) {
+    if (!keep[a]) continue;
+    int id = act_in ? act_in[a] : a;
+    if (fine && fine[id]) act_out[pf++] = id; else act_out[pc++] = id;
+  }
+  __syncthreads();   // wc / wf are read above by every thread
+  return make_int2(n_coarse + n_fine, n_coarse);
+}
+
+// K3 + K4 fused (see launch_update).  Block = 16 warps = RPB rows x NG warps: the NG warps of a
+// row sum its slot partials, 32 coordinates each, in fixed slot order (the association of every
+// consumer of the slot partials: a row's G is bitwise the same whatever path or GPU count reduces
+// it), then the row's first warp runs epilogue_core.  Few rows (L_in <= RPB, the tail of every
+// component): block 0 alone, compacting in shared memory; otherwise the block that finishes last
+// (ticket) compacts.
+template <int NG, bool F32>
+__global__ void __launch_bounds__(512) k_update(UpdateArgs u) {
+  constexpr int RPB = 16 / NG;
+  __shared__ double gsh[RPB][NG * 32];
+  __shared__ double s4sh[RPB];
+  __shared__ int s_keep[RPB];
+  __shared__ int s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = warp / NG, grp = warp - rb * NG;
+  const int t = u.ctl->t, k = u.ctl->k;
+  const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
+  const bool single = L_in <= RPB;   // grid-uniform
+  if (single && blockIdx.x != 0) return;
+  const int a = blockIdx.x * RPB + rb;
+  const bool row_ok = rb < RPB && a < L_in;
+  int l = 0;
+  double wo[NG], we[NG];
+  if (row_ok) {
+    l = u.act_in[a];
+    if (grp == 0) load_row<NG>(u, l, lane, wo, we);   // (in flight with the slot sums below)
+    const int n = grp * 32 + lane;
+    // (16 partials in flight per lane: with few active rows the slot chain is latency-bound; the
+    // association is the same sequential slot order whatever the depth)
+    gsh[rb][n] = n < u.N ? slot_sum<(NG >= 8 ? 8 : 16), (F32 ? 2 : 1)>(u.G, u.S, u.cap, u.ldg, a, n) : 0.0;
+    if (grp == 0 && lane == 0 && u.s4p)
+      s4sh[rb] = ordered_sum<16>(u.S, [&](int s) { return __ldg(u.s4p + (int64_t)s * u.cap + a); });
+  }
+  __syncthreads();
+  if (row_ok && grp == 0) {
+    double acc[NG];
+#pragma unroll
+    for (int v = 0; v < NG; ++v) acc[v] = gsh[rb][lane + 32 * v];
+    const bool kp = epilogue_core<NG>(l, lane, acc, u.s4p ? s4sh[rb] : 0.0, wo, we, u, k, t);
+    if (lane == 0) {
+      s_keep[rb] = kp ? 1 : 0;
+      if (!single) u.keep[a] = kp ? 1 : 0;
+    }
+  }
+  int2 r;
+  if (single) {   // K4 by one warp: kept coarse rows, then kept fine rows (k_compact's order)
+    __syncthreads();
+    if (warp == 0) {
+      const bool in = lane < L_in && s_keep[lane];
+      const int id = lane < L_in ? u.act_in[lane] : 0;
+      const bool isf = in && u.pr.fine && u.pr.fine[id];
+      const unsigned mc = __ballot_sync(0xffffffffu, in && !isf), mf = __ballot_sync(0xffffffffu, isf);
+      const unsigned lt = (1u << lane) - 1u;
+      const int n_coarse = __popc(mc);
+      const int pos = isf ? n_coarse + __popc(mf & lt) : __popc(mc & lt);
+      __syncwarp();
+      if (in) {
+        u.act_out[pos] = id;
+        if (u.copy_back) const_cast<int*>(u.act_in)[pos] = id;   // (all lanes read act_in above)
+      }
+      r = make_int2(n_coarse + __popc(mf), n_coarse);
+    }
+  } else {
+    // completion ticket: the block that finishes last sees every row's keep / fine / state
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned tk = atomicAdd(&u.ctl->done, 1u);
+      s_last = tk == gridDim.x - 1 ? 1 : 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    r = compact_block(u.act_in, u.keep, u.pr.fine, L_in, u.act_out);   // K4
+    if (u.copy_back) {
+      int* dst = const_cast<int*>(u.act_in);
+      for (int j = threadIdx.x; j < r.x; j += blockDim.x) dst[j] = u.act_out[j];
+    }
+  }
+  if (threadIdx.x == 0) {
+    u.cnt_out[0] = r.x;
+    u.cnt_out[1] = r.y;
+    if (u.host_mapped) {
+      ((volatile int*)u.host_mapped)[0] = r.x;
+      ((volatile int*)u.host_mapped)[1] = r.y;
+    }
+    u.ctl->done = 0u;
+    if (L_in > 0) {   // an executed iteration (a host-launched batch may enqueue a few beyond the last)
+      if (u.hist) {
+        u.hist[2 * t] = r.x;
+        u.hist[2 * t + 1] = r.y;
+      }
+      u.ctl->t = t + 1;
+      u.ctl->sum_active += L_in;
+    }
+    // do ... while (t < K and B != {})
+    if (u.loop) cudaGraphSetConditional(u.loop, (L_in > 0 && r.x > 0 && t + 1 <= u.K_loop) ? 1u : 0u);
+  }
+}
+
+__global__ void k_ctl_set(IterCtl* ctl, int t, int k) {
+  ctl->t = t;
+  ctl->k = k;
+  ctl->done = 0u;
+  ctl->sum_active = 0;
 }
 
 // Single-block, order-preserving compaction (deterministic), stably partitioned into coarse
@@ -318,98 +513,20 @@ __global__ void __launch_bounds__(1024) k_compact(const int* __restrict__ act_in
   }
 }
 
-__device__ __forceinline__ void operand_f32_elem(int64_t idx, int a, int n, const int* __restrict__ act,
-                                                 const double* __restrict__ W64, int N, float* __restrict__ W32) {
-  W32[idx] = n < N ? (float)W64[(int64_t)act[a] * N + n] : 0.f;
-}
-
-__global__ void k_operand_f32(const int* __restrict__ act, const int* __restrict__ Lact, int cap,
-                              const double* __restrict__ W64, int N, int NP, float* __restrict__ W32) {
+// operand rows 0..L-1 by candidate id from the fp64 master
+__global__ void k_operand_f32(int L, const double* __restrict__ W64, int N, int NP, float* __restrict__ W32) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int a = (int)(idx / NP), n = (int)(idx % NP);
-  if (a >= cap || a >= *Lact) return;
-  operand_f32_elem(idx, a, n, act, W64, N, W32);
+  if (idx >= (int64_t)L * NP) return;
+  int l = (int)(idx / NP), n = (int)(idx % NP);
+  W32[idx] = n < N ? (float)W64[(int64_t)l * N + n] : 0.f;
 }
 
-// Split fp16 operand: w is scaled by 2^4 (|w| <= 1 -> <= 16) so most w_lo stay normal fp16;
-// hi = fp16(2^4 w), lo = fp16(2^4 w - hi).  hi + lo = 2^4 w to ~2^-22 relative (absolute error
-// <= 3e-8 / 16 per coordinate from lo subnormals); both GEMM1 passes share one accumulator.
-// Coarse rows (fine[l] == 0) get lo = 0 (their contraction is the one-pass w_h product).
-__device__ __forceinline__ void operand_f16x2_elem(int64_t idx, int a, int n, const int* __restrict__ act,
-                                                   const double* __restrict__ W64, int N,
-                                                   const uint8_t* __restrict__ fine, __half* __restrict__ Whi,
-                                                   __half* __restrict__ Wlo) {
-  int l = act[a];
-  double w = n < N ? W64[(int64_t)l * N + n] * 16.0 : 0.0;
-  __half hi = __double2half(w);
-  __half lo = (fine && !fine[l]) ? __double2half(0.0) : __double2half(w - (double)__half2float(hi));
-  Whi[idx] = hi;
-  if (Wlo) Wlo[idx] = lo;
-}
-
-__global__ void k_operand_f16x2(const int* __restrict__ act, const int* __restrict__ Lact, int cap,
-                                const double* __restrict__ W64, int N, int NP, const uint8_t* __restrict__ fine,
+__global__ void k_operand_f16x2(int L, const double* __restrict__ W64, int N, int NP, const uint8_t* __restrict__ fine,
                                 __half* __restrict__ Whi, __half* __restrict__ Wlo) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int a = (int)(idx / NP), n = (int)(idx % NP);
-  if (a >= cap || a >= *Lact) return;
-  operand_f16x2_elem(idx, a, n, act, W64, N, fine, Whi, Wlo);
-}
-
-// Few active rows (<= 32): K3 epilogue (one warp per row), K4 compaction (warp ballots, the
-// same stable coarse-then-fine order as k_compact) and the next iteration's operand gather in
-// one single-block launch instead of three (each of those kernels is a few microseconds of pure
-// latency at this size).  Same per-row arithmetic as k_epilogue.
-template <int V>
-__global__ void __launch_bounds__(1024) k_iter_small(SlotPartials Gp, const double* __restrict__ s4p, int S,
-                                                     int64_t cap, int ldg, EvalPoint ev, const int* __restrict__ act,
-                                                     int L_ub, const double* __restrict__ Wacc, int k, int N,
-                                                     double M, double tol, int t, double* __restrict__ W64,
-                                                     double* __restrict__ alpha_old, int* __restrict__ iters,
-                                                     uint8_t* __restrict__ state, uint8_t* __restrict__ keep,
-                                                     Promotion pr, int* cnt, const uint8_t* __restrict__ fine,
-                                                     int* __restrict__ act_out, int* host_mapped, int* hist,
-                                                     int build, int NP, __half* __restrict__ Whi,
-                                                     __half* __restrict__ Wlo, float* __restrict__ W32) {
-  __shared__ int s_new;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int L_in = min(L_ub, cnt[0]);
-  if (warp < L_in)
-    epilogue_row<V>(warp, lane, Gp, s4p, S, cap, ldg, ev, act, Wacc, k, N, M, tol, t, W64, alpha_old, iters, state,
-                    keep, pr);
-  __syncthreads();
-  if (warp == 0) {   // stable partition: kept coarse rows, then kept fine rows (k_compact order)
-    const bool in = lane < L_in && keep[lane];
-    const int id = lane < L_in ? act[lane] : 0;
-    const bool isf = in && fine && fine[id];
-    const unsigned mc = __ballot_sync(0xffffffffu, in && !isf), mf = __ballot_sync(0xffffffffu, isf);
-    const unsigned lt = (1u << lane) - 1u;
-    const int n_coarse = __popc(mc), n_new = n_coarse + __popc(mf);
-    if (in) act_out[isf ? n_coarse + __popc(mf & lt) : __popc(mc & lt)] = id;
-    if (lane == 0) {
-      cnt[0] = n_new;
-      cnt[1] = n_coarse;
-      if (host_mapped) {
-        ((volatile int*)host_mapped)[0] = n_new;
-        ((volatile int*)host_mapped)[1] = n_coarse;
-      }
-      if (hist) {
-        hist[0] = n_new;
-        hist[1] = n_coarse;
-      }
-      s_new = n_new;
-    }
-  }
-  __syncthreads();
-  if (!build) return;
-  const int tot = s_new * NP;
-  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-    const int a = idx / NP, n = idx - a * NP;
-    if (Whi)
-      operand_f16x2_elem(idx, a, n, act_out, W64, N, fine, Whi, Wlo);
-    else
-      operand_f32_elem(idx, a, n, act_out, W64, N, W32);
-  }
+  if (idx >= (int64_t)L * NP) return;
+  int l = (int)(idx / NP), n = (int)(idx % NP);
+  operand_f16x2_coord(n < N ? W64[(int64_t)l * N + n] : 0.0, !fine || fine[l], Whi + idx, Wlo ? Wlo + idx : nullptr);
 }
 
 // G_out[a][n] = slot_sum(...) and s4_out[a] (fixed slot order), one block per (row, 32
@@ -450,14 +567,16 @@ __global__ void __launch_bounds__(256) k_slot_reduce(SlotPartials Gp, const doub
   }
 }
 
-// s4 = w_e . G_raw (identity sum_m y^3 (w_e.x) = sum_m y^4), rows by position; one warp per row.
-__global__ void k_s4_from_g(EvalPoint ev, const double* __restrict__ W, const double* __restrict__ G, int ldg, int L,
-                            int N, double* __restrict__ s4) {
+// s4 = w_e . G_raw (identity sum_m y^3 (w_e.x) = sum_m y^4), G rows by position; the evaluation
+// point of position a is candidate act[a] (identity if act is null); one warp per row.
+__global__ void k_s4_from_g(EvalPoint ev, const int* __restrict__ act, const double* __restrict__ G, int ldg, int L,
+                            int N, double* __restrict__ s4, const int* __restrict__ cnt) {
   int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   int lane = threadIdx.x & 31;
-  if (a >= L) return;
+  if (a >= L || (cnt && a >= cnt[0])) return;
+  const int l = act ? act[a] : a;
   double v = 0.0;
-  for (int n = lane; n < N; n += 32) v += eval_coord(ev, a, n, W[(int64_t)a * N + n]) * G[(int64_t)a * ldg + n];
+  for (int n = lane; n < N; n += 32) v += eval_coord(ev, l, n, 0.0) * G[(int64_t)a * ldg + n];
   v = warp_sum(v);
   if (lane == 0) s4[a] = v;
 }
@@ -473,28 +592,41 @@ int launch_cand_init(cudaStream_t st, uint64_t seed, int i, int64_t id_base, int
   return 1;
 }
 
-int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, EvalPoint ev,
-                    const int* act, int L_act, const double* Wacc, int k, int N, double M, double tol, int t,
-                    double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep, Promotion pr,
-                    const int* cnt) {
-  if (L_act <= 0) return 0;
-  int64_t threads = (int64_t)L_act * 32;
-  // coordinates per lane: only as many as N needs (bitwise the same as the 8-wide loop)
-  auto kern = N <= 32 ? k_epilogue<1> : N <= 64 ? k_epilogue<2> : N <= 128 ? k_epilogue<4> : k_epilogue<kMaxV>;
-  kern<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(Gp, s4p, S, cap, ldg, ev, act, L_act, Wacc, k, N, M, tol, t,
-                                                         W64, alpha_old, iters, state, keep, pr, cnt);
+int update_blocks(int L_ub, int NP) {
+  const int NG = (NP + 31) / 32, RPB = 16 / NG;
+  return (int)ceil_div(std::max(L_ub, 1), RPB);
+}
+
+int launch_update(cudaStream_t st, const UpdateArgs& u, int NP) {
+  if (u.L_ub <= 0) return 0;
+  const int NG = (NP + 31) / 32;
+  const unsigned nb = (unsigned)update_blocks(u.L_ub, NP);
+  // fp32 slot partials (tensor-core step, split parts possible) or fp64 (FP32 step, reduced sums)
+  const bool f32 = u.G.f32;
+#define OICA_UPD(g)                                                          \
+  case g:                                                                    \
+    if (f32)                                                                 \
+      k_update<g, true><<<nb, 512, 0, st>>>(u);                              \
+    else                                                                     \
+      k_update<g, false><<<nb, 512, 0, st>>>(u);                             \
+    break;
+  switch (NG) {
+    OICA_UPD(1)
+    OICA_UPD(2)
+    OICA_UPD(3)
+    OICA_UPD(4)
+    OICA_UPD(5)
+    OICA_UPD(6)
+    OICA_UPD(7)
+    OICA_UPD(8)
+    default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the update");
+  }
+#undef OICA_UPD
   return 1;
 }
 
-int launch_iter_small(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, EvalPoint ev,
-                      const int* act, int L_ub, const double* Wacc, int k, int N, double M, double tol, int t,
-                      double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep, Promotion pr,
-                      int* cnt, const uint8_t* fine, int* act_out, int* host_mapped, int* hist, bool build, int NP,
-                      __half* Whi, __half* Wlo, float* W32) {
-  if (L_ub <= 0) return 0;
-  auto kern = N <= 32 ? k_iter_small<1> : N <= 64 ? k_iter_small<2> : N <= 128 ? k_iter_small<4> : k_iter_small<kMaxV>;
-  kern<<<1, 1024, 0, st>>>(Gp, s4p, S, cap, ldg, ev, act, L_ub, Wacc, k, N, M, tol, t, W64, alpha_old, iters, state,
-                           keep, pr, cnt, fine, act_out, host_mapped, hist, build ? 1 : 0, NP, Whi, Wlo, W32);
+int launch_ctl_set(cudaStream_t st, IterCtl* ctl, int t, int k) {
+  k_ctl_set<<<1, 1, 0, st>>>(ctl, t, k);
   return 1;
 }
 
@@ -504,19 +636,18 @@ int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, cons
   return 1;
 }
 
-int launch_operand_f32(cudaStream_t st, const int* act, const int* Lact, int cap, const double* W64, int N, int NP,
-                       float* W32) {
-  if (cap <= 0) return 0;
-  int64_t tot = (int64_t)cap * NP;
-  k_operand_f32<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(act, Lact, cap, W64, N, NP, W32);
+int launch_operand_f32(cudaStream_t st, int L, const double* W64, int N, int NP, float* W32) {
+  if (L <= 0) return 0;
+  int64_t tot = (int64_t)L * NP;
+  k_operand_f32<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(L, W64, N, NP, W32);
   return 1;
 }
 
-int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact, int cap, const double* W64, int N, int NP,
-                         const uint8_t* fine, __half* Whi, __half* Wlo) {
-  if (cap <= 0) return 0;
-  int64_t tot = (int64_t)cap * NP;
-  k_operand_f16x2<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(act, Lact, cap, W64, N, NP, fine, Whi, Wlo);
+int launch_operand_f16x2(cudaStream_t st, int L, const double* W64, int N, int NP, const uint8_t* fine, __half* Whi,
+                         __half* Wlo) {
+  if (L <= 0) return 0;
+  int64_t tot = (int64_t)L * NP;
+  k_operand_f16x2<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(L, W64, N, NP, fine, Whi, Wlo);
   return 1;
 }
 
@@ -544,10 +675,10 @@ int launch_alpha_refresh(cudaStream_t st, const int* act, const int* cnt, int L_
   return 1;
 }
 
-int launch_s4_from_g(cudaStream_t st, EvalPoint ev, const double* W, const double* G, int ldg, int L, int N,
-                     double* s4) {
+int launch_s4_from_g(cudaStream_t st, EvalPoint ev, const int* act, const double* G, int ldg, int L, int N,
+                     double* s4, const int* cnt) {
   if (L <= 0) return 0;
-  k_s4_from_g<<<(unsigned)ceil_div((int64_t)L * 32, 256), 256, 0, st>>>(ev, W, G, ldg, L, N, s4);
+  k_s4_from_g<<<(unsigned)ceil_div((int64_t)L * 32, 256), 256, 0, st>>>(ev, act, G, ldg, L, N, s4, cnt);
   return 1;
 }
 

@@ -338,8 +338,8 @@ __global__ void k_alpha_reduce(const double* __restrict__ part, int nblk, double
 __global__ void k_finish(const double* __restrict__ W64, const int* __restrict__ iters, const int* __restrict__ counts,
                          const int* __restrict__ pc, const int* __restrict__ qc, const int* __restrict__ csize,
                          const double* __restrict__ s4c, int64_t id_base, int N, double M, uint32_t flags,
-                         int64_t sum_active, int n_iter, const int* __restrict__ nonfinite, RankSummary* sum,
-                         double* wsum) {
+                         int64_t sum_active, int n_iter, const int* __restrict__ nonfinite,
+                         const IterCtl* __restrict__ ctl, RankSummary* sum, double* wsum) {
   bool raw = flags & OICA_RAW_ARGMAX;
   for (int idx = threadIdx.x; idx < kMaxClusters * N; idx += blockDim.x) {
     int c = idx / N, n = idx % N;
@@ -366,8 +366,8 @@ __global__ void k_finish(const double* __restrict__ W64, const int* __restrict__
     sum->n_unconv = counts[1];
     sum->n_deg = counts[2];
     sum->n_domain = counts[3];
-    sum->sum_active = sum_active;
-    sum->n_iter = n_iter;
+    sum->sum_active = sum_active >= 0 ? sum_active : ctl->sum_active;
+    sum->n_iter = sum_active >= 0 ? n_iter : ctl->t - 1;
     sum->n_nonfinite = nonfinite ? *nonfinite : 0;
   }
 }
@@ -468,10 +468,10 @@ int launch_select_local(cudaStream_t st, const double* W64, const double* alpha_
 
 int launch_select_finish(cudaStream_t st, const double* W64, const int* iters, const int* counts, const int* pc,
                          const int* qc, const int* csize, const double* s4c, int64_t id_base, int N, double M_global,
-                         uint32_t flags, int64_t sum_active, int n_iter, const int* nonfinite, RankSummary* summary,
-                         double* wsum) {
+                         uint32_t flags, int64_t sum_active, int n_iter, const int* nonfinite, const IterCtl* ctl,
+                         RankSummary* summary, double* wsum) {
   k_finish<<<1, 256, 0, st>>>(W64, iters, counts, pc, qc, csize, s4c, id_base, N, M_global, flags, sum_active, n_iter,
-                              nonfinite, summary, wsum);
+                              nonfinite, ctl, summary, wsum);
   return 1;
 }
 

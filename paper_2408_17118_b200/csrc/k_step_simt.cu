@@ -19,7 +19,8 @@ constexpr int YS = R + 1;    // padded Y^3 row stride
 
 template <int NP>
 __global__ void __launch_bounds__(256, 1)
-k_step_simt(const float* __restrict__ X, int64_t ld, int64_t M, int N, const float* __restrict__ W32, int L_ub,
+k_step_simt(const float* __restrict__ X, int64_t ld, int64_t M, int N, const float* __restrict__ W32,
+            const int* __restrict__ act, int L_ub,
             int64_t slot_len, int flush, double* __restrict__ Gp, double* __restrict__ s4p, int64_t cap,
             const int* __restrict__ cnt) {
   const int L_act = cnt ? min(L_ub, cnt[0]) : L_ub;   // device count when the grid is an upper bound
@@ -39,7 +40,7 @@ k_step_simt(const float* __restrict__ X, int64_t ld, int64_t M, int N, const flo
 
   for (int idx = tid; idx < R * NP; idx += 256) {
     int r = idx / NP, n = idx % NP;
-    WT[n * R + r] = (row0 + r < L_act) ? W32[(int64_t)(row0 + r) * NP + n] : 0.f;
+    WT[n * R + r] = (row0 + r < L_act) ? W32[(int64_t)act[row0 + r] * NP + n] : 0.f;   // operand row by id
   }
 
   const int rg = tid >> 4, cg = tid & 15;     // phase 1: rows rg*4+i, cols cg+16j
@@ -142,7 +143,7 @@ k_step_simt(const float* __restrict__ X, int64_t ld, int64_t M, int N, const flo
 }
 
 template <int NP>
-void launch_np(cudaStream_t st, const float* X, int64_t ld, int64_t M, int N, const float* W32, int L_act,
+void launch_np(cudaStream_t st, const float* X, int64_t ld, int64_t M, int N, const float* W32, const int* act, int L_act,
                int64_t slot_len, int S, int flush, double* Gp, double* s4p, int64_t cap, const int* cnt) {
   size_t smem = sizeof(float) * ((size_t)NP * R + (size_t)NP * XS + (size_t)MC * YS + 16 * R);
   static bool attr = false;
@@ -151,20 +152,20 @@ void launch_np(cudaStream_t st, const float* X, int64_t ld, int64_t M, int N, co
     attr = true;
   }
   dim3 grid((unsigned)ceil_div(L_act, R), (unsigned)S);
-  k_step_simt<NP><<<grid, 256, smem, st>>>(X, ld, M, N, W32, L_act, slot_len, flush, Gp, s4p, cap, cnt);
+  k_step_simt<NP><<<grid, 256, smem, st>>>(X, ld, M, N, W32, act, L_act, slot_len, flush, Gp, s4p, cap, cnt);
 }
 
 }  // namespace
 
 int launch_step_simt(cudaStream_t st, const float* X, int64_t ld, int64_t M, int N, int NP, const float* W32,
-                     int L_act, int64_t slot_len, int S, int flush, double* Gp, double* s4p, int64_t cap,
+                     const int* act, int L_act, int64_t slot_len, int S, int flush, double* Gp, double* s4p, int64_t cap,
                      const int* cnt) {
   if (L_act <= 0) return 0;
   switch (NP) {
-    case 32: launch_np<32>(st, X, ld, M, N, W32, L_act, slot_len, S, flush, Gp, s4p, cap, cnt); break;
-    case 64: launch_np<64>(st, X, ld, M, N, W32, L_act, slot_len, S, flush, Gp, s4p, cap, cnt); break;
-    case 128: launch_np<128>(st, X, ld, M, N, W32, L_act, slot_len, S, flush, Gp, s4p, cap, cnt); break;
-    case 256: launch_np<256>(st, X, ld, M, N, W32, L_act, slot_len, S, flush, Gp, s4p, cap, cnt); break;
+    case 32: launch_np<32>(st, X, ld, M, N, W32, act, L_act, slot_len, S, flush, Gp, s4p, cap, cnt); break;
+    case 64: launch_np<64>(st, X, ld, M, N, W32, act, L_act, slot_len, S, flush, Gp, s4p, cap, cnt); break;
+    case 128: launch_np<128>(st, X, ld, M, N, W32, act, L_act, slot_len, S, flush, Gp, s4p, cap, cnt); break;
+    case 256: launch_np<256>(st, X, ld, M, N, W32, act, L_act, slot_len, S, flush, Gp, s4p, cap, cnt); break;
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the SIMT step");
   }
   return 1;

@@ -227,7 +227,8 @@ struct Cfg {
 template <int NP, bool SPLIT, int EPI, int CL, int RG>
 __global__ void __launch_bounds__(192, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
-          const __half* __restrict__ Whi, const __half* __restrict__ Wlo, int L_ub, int64_t M, int64_t slot_len,
+          const __half* __restrict__ Whi, const __half* __restrict__ Wlo, const int* __restrict__ act, int L_ub,
+          int64_t M, int64_t slot_len,
           float* __restrict__ Gp, int64_t cap, int n_coarse_h, int S_, const int* __restrict__ cnt, int s_base,
           int S_total, float* __restrict__ Gsub, int64_t sub_cap, const int* __restrict__ cnt_g, int split,
           const int8_t* __restrict__ xshift) {
@@ -446,9 +447,10 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     // W operand rows -> TMEM (A operand of GEMM1, fp16 pairs per 32-bit column)
     {
-      const uint32_t* wh = (const uint32_t*)(Whi + (int64_t)row * NP);
-      const uint32_t* wl = (const uint32_t*)(Wlo + (int64_t)row * NP);
       bool ok = row < L_act;
+      const int64_t id = ok ? (int64_t)__ldg(act + row) : 0;   // operand rows are stored by candidate id
+      const uint32_t* wh = (const uint32_t*)(Whi + id * NP);
+      const uint32_t* wl = (const uint32_t*)(Wlo + id * NP);
 #pragma unroll 1
       for (int c = 8 * h; c < NP / 2; c += 8 * NH) {   // NP/2 is a multiple of 8 columns
         uint32_t v[8];
@@ -615,7 +617,7 @@ CUtensorMap make_map(const __half* base, int64_t rows, int64_t cols, int64_t ld,
 
 template <int NP, bool SPLIT, int EPI, int CL, int RG>
 void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
+               const int* act, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
                const Upload& up, const SplitOut& so, const int8_t* xshift) {
   using C = Cfg<NP, SPLIT, RG>;
   auto kern = k_step_tc<NP, SPLIT, EPI, CL, RG>;
@@ -653,7 +655,7 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   lc.attrs = at;
   lc.numAttrs = 1;
   lc.gridDim = dim3((unsigned)(n_tiles * up.s_count));
-  OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, L_act, M, slot_len, Gp, cap, n_coarse, up.s_count, cnt,
+  OICA_CUDA(cudaLaunchKernelEx(&lc, kern, tx, tw, Whi, Wlo, act, L_act, M, slot_len, Gp, cap, n_coarse, up.s_count, cnt,
                                up.s_base, S, so.sub, so.sub_cap, so.cnt_g, so.enable, xshift));
 }
 
@@ -668,7 +670,7 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
 // out of the product library so no environment variable can change what the timed step does.
 template <int NP, bool SPLIT, int EPI>
 void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                    int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
+                    const int* act, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
                     const Upload& up, const SplitOut& so, const int8_t* xshift) {
   constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
   constexpr int RGN = NP <= 64 ? 3 : NP <= 128 ? 1 : 0;   // release Y-ring layout for this NP
@@ -678,68 +680,68 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
   const int cl = up.cl ? up.cl : cl_env ? cl_env : (NP > 64 && L_act > 128 ? 2 : 1);
   if constexpr (NP == 256) {   // 4-CTA multicast clusters
     if (cl == 4) {
-      launch_cl<NP, SPLIT, EPI, 4, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+      launch_cl<NP, SPLIT, EPI, 4, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
       return;
     }
   }
   if (NP <= 128 && ring == 4) {   // narrow 4 x 64-sample Y ring (measured slower)
     if (cl == 2)
-      launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+      launch_cl<NP, SPLIT, EPI, CL2, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
     else
-      launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+      launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
     return;
   }
   if (NP <= 64 && ring == 2) {   // small NP with 2 x 128-sample slots
-    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+    launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
     return;
   }
 #else
   const int cl = up.cl ? up.cl : (NP > 64 && L_act > 128 ? 2 : 1);
 #endif
   if (NP > 64 && cl == 2)
-    launch_cl<NP, SPLIT, EPI, CL2, RGN>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+    launch_cl<NP, SPLIT, EPI, CL2, RGN>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
   else
-    launch_cl<NP, SPLIT, EPI, 1, RGN>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+    launch_cl<NP, SPLIT, EPI, 1, RGN>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
 }
 
 template <int NP, bool SPLIT>
 void launch_epi(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
-                int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so, const int8_t* xshift) {
+                const int* act, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so, const int8_t* xshift) {
 #ifdef OICA_EXPERIMENTS
   static int epi = [] { const char* e = getenv("OICA_TC_EPI"); return e ? atoi(e) : 0; }();
   switch (epi) {
-    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
-    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
-    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
-    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
-    case 7: launch_variant<NP, SPLIT, 7>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
-    case 8: launch_variant<NP, SPLIT, 8>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 3: launch_variant<NP, SPLIT, 3>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 4: launch_variant<NP, SPLIT, 4>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 5: launch_variant<NP, SPLIT, 5>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 7: launch_variant<NP, SPLIT, 7>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 8: launch_variant<NP, SPLIT, 8>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
     default: break;
   }
 #endif
-  launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift);
+  launch_variant<NP, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift);
 }
 
 template <bool SPLIT>
 void launch_np(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi, const __half* Wlo,
-               int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so, const int8_t* xshift) {
+               const int* act, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int t0, const int* cnt, const Upload& up, const SplitOut& so, const int8_t* xshift) {
   switch (NP) {
-    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 64: launch_epi<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 144: launch_variant<144, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 160: launch_variant<160, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 176: launch_variant<176, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 192: launch_variant<192, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 208: launch_variant<208, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 224: launch_variant<224, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 240: launch_variant<240, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
-    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 16: launch_variant<16, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 32: launch_variant<32, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 48: launch_variant<48, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 64: launch_epi<64, SPLIT>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 80: launch_variant<80, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 96: launch_variant<96, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 112: launch_variant<112, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 128: launch_epi<128, SPLIT>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 144: launch_variant<144, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 160: launch_variant<160, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 176: launch_variant<176, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 192: launch_variant<192, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 208: launch_variant<208, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 224: launch_variant<224, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 240: launch_variant<240, SPLIT, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
+    case 256: launch_epi<256, SPLIT>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); break;
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the tensor-core step");
   }
 }
@@ -807,7 +809,7 @@ bool tc_supported(int N) { return N >= 1 && N <= 256; }
 int tc_np(int N) { return (int)round_up(N < 16 ? 16 : N, 16); }
 
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
-                   const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
+                   const __half* Wlo, const int* act, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
                    const int* cnt, bool lo_capable, const Upload& up, const SplitOut& so, const int8_t* xshift) {
   if (L_act <= 0) return 0;
 #ifdef OICA_EXPERIMENTS
@@ -815,9 +817,9 @@ int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, in
   lo_capable = lo_capable || force_lo;
 #endif
   if (lo_capable || n_coarse < L_act)   // fine rows (possibly): LO-capable layout, 2nd pass from tile n_coarse/128
-    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+    launch_np<true>(st, Xh, ldx, M, NP, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
   else
-    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, L_act, slot_len, S, Gp, cap, 0, cnt, up, so, xshift);
+    launch_np<false>(st, Xh, ldx, M, NP, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, 0, cnt, up, so, xshift);
   return 1;
 }
 

@@ -24,18 +24,21 @@ int launch_cand_init(cudaStream_t st, uint64_t seed, int i, int64_t id_base, int
 int launch_compact(cudaStream_t st, const int* act_in, const uint8_t* keep, const uint8_t* fine, int L_in,
                    int* act_out, int* out_dev, int* host_mapped, const int* cnt_in = nullptr, int* hist = nullptr);
 
-// Operand rows for the step kernel, gathered in active order from the fp64 master.
-int launch_operand_f32(cudaStream_t st, const int* act, const int* Lact_dev, int cap, const double* W64,
-                       int N, int NP, float* W32);
+// Operand rows of the step kernels, stored BY CANDIDATE ID (row l at l * NP): the step kernels
+// gather the rows of their active positions through the active list, and the fused update
+// (launch_update) rewrites a row whenever it updates that candidate.  These two build rows
+// 0..L-1 from the fp64 master (after the candidate draw; for oica_fixed_point_step).
+int launch_operand_f32(cudaStream_t st, int L, const double* W64, int N, int NP, float* W32);
 // Split-fp16 operand (TC path): hi = fp16(2^4 w), lo = fp16(2^4 w - hi) for fine rows, 0 for
-// coarse rows (fine == null: all rows fine), K-major rows in active order.
-int launch_operand_f16x2(cudaStream_t st, const int* act, const int* Lact_dev, int cap, const double* W64,
-                         int N, int NP, const uint8_t* fine, __half* Whi, __half* Wlo);
+// coarse rows (fine == null: all rows fine).
+int launch_operand_f16x2(cudaStream_t st, int L, const double* W64, int N, int NP, const uint8_t* fine, __half* Whi,
+                         __half* Wlo);
 
 // ---- K2b: fused GEMM-cube-GEMM on CUDA cores (PAPER.md:243-245 before the -3B term)
 // Gp[s][a][n] (stride ldg = NP), s4p[s][a] over slots s of slot_len samples.
+// act (device): the active list; position a uses operand row act[a] (W32 by candidate id).
 int launch_step_simt(cudaStream_t st, const float* X, int64_t ld, int64_t M, int N, int NP,
-                     const float* W32, int L_act, int64_t slot_len, int S, int flush,
+                     const float* W32, const int* act, int L_act, int64_t slot_len, int S, int flush,
                      double* Gp, double* s4p, int64_t cap, const int* cnt);
 
 // Slot partials of the step kernel: fp64 (SIMT) or fp32 (tensor cores: the exact TMEM value).
@@ -50,14 +53,29 @@ struct SlotPartials {
   const int* cnt_g = nullptr;
   int L_g_host = 0;
 };
-// The point the contraction was evaluated at, rows in ACTIVE order (stride NP): the -3w term
-// and the alpha~ identity use it so eq. (5) is evaluated consistently.
-// f16: (hi + lo) / 2^4 (lo may be null); f32: W32; all null: the fp64 master row.
+// The point the contraction was evaluated at: the operand rows, BY CANDIDATE ID (stride ld): the
+// -3w term and the alpha~ identity use it so eq. (5) is evaluated consistently.
+// f16: (hi + lo) / 2^4 (lo may be null); f32: W32; all null: the fp64 master row.  The fused
+// update reads a row's point and then overwrites the row with the next iteration's operand.
 struct EvalPoint {
-  const __half* hi;
-  const __half* lo;
-  const float* f32;
+  __half* hi;
+  __half* lo;
+  float* f32;
   int ld;
+};
+
+// Device iteration state of a context (DESIGN.md §5 "iteration"): t = the 1-based iteration the
+// next update applies (advanced by the update's last block when the iteration had active runs),
+// k = accepted rows the updates project against (0 in the reduced space), done = block tickets of
+// the running update (reset by its last block), sum_active = the component's algorithmic-work
+// counter.  Kept on the device so an iteration needs no host argument that changes (CUDA graph)
+// and a component needs no host round trip before its selection.
+struct IterCtl {
+  int t;
+  int k;
+  unsigned done;
+  int pad;
+  long long sum_active;   // sum over executed iterations of the active rows entering them
 };
 
 // ---- K3: fp64 epilogue: slot sum, /M - 3w, projection, normalise, convergence
@@ -74,20 +92,51 @@ struct Promotion {
   int t_force;
   int* nonfinite = nullptr;
 };
-int launch_epilogue(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
-                    EvalPoint ev, const int* act, int L_act, const double* Wacc, int k, int N, double M,
-                    double tol, int t, double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep,
-                    Promotion pr, const int* cnt);
+// K3 + K4 fused: one launch per iteration after the step (DESIGN.md §5 "iteration").  For the
+// L_in = min(L_ub, cnt_in[0]) active positions: the fixed-order slot sum of G (and s4), eq. (5) at
+// the evaluation point, projection against ctl->k rows of Wacc, normalisation, convergence test,
+// promotion, the new master row W64[l] and the next operand row (by id); then the LAST block to
+// finish compacts act_in -> act_out (kept coarse rows, then kept fine rows), writes cnt_out =
+// [L_act, n_coarse] (and host_mapped, hist[2t..2t+1] if given), copies act_out back over act_in
+// when copy_back (a fixed active-list buffer: CUDA-graph iterations), and advances ctl->t.
+// cnt_in may alias cnt_out (every block reads it before the last block writes it).
+struct UpdateArgs {
+  SlotPartials G;
+  const double* s4p;   // SIMT slot partials of sum y^4 (null: TC identity w_e . G)
+  int S;
+  int64_t cap;
+  int ldg;
+  EvalPoint ev;
+  const int* act_in;
+  int* act_out;
+  int copy_back;
+  int L_ub;
+  const int* cnt_in;
+  int* cnt_out;
+  int* host_mapped;
+  int* hist;
+  const double* Wacc;
+  int N;
+  double M;
+  double tol;
+  double* W64;
+  double* alpha_old;
+  int* iters;
+  uint8_t* state;
+  uint8_t* keep;
+  Promotion pr;
+  IterCtl* ctl;
+  // device-side loop (CUDA-graph WHILE node): the last block also sets the loop condition
+  // "runs remain active and t <= K_loop" (loop = 0 outside a graph)
+  cudaGraphConditionalHandle loop;
+  int K_loop;
+};
+int launch_update(cudaStream_t st, const UpdateArgs& u, int NP);
+// grid-size upper bound of launch_update for L_ub rows (blocks)
+int update_blocks(int L_ub, int NP);
+// ctl <- {t, k, 0} (component start; t = 1)
+int launch_ctl_set(cudaStream_t st, IterCtl* ctl, int t, int k);
 
-// <= 32 active rows: epilogue + compaction (act -> act_out, cnt = [L_act, n_coarse] updated in
-// place, host_mapped / hist as launch_compact) + the next operand rows (build: f16x2 when Whi,
-// else W32) in one single-block launch; same results as the three separate kernels.
-constexpr int kIterSmallRows = 32;
-int launch_iter_small(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg, EvalPoint ev,
-                      const int* act, int L_ub, const double* Wacc, int k, int N, double M, double tol, int t,
-                      double* W64, double* alpha_old, int* iters, uint8_t* state, uint8_t* keep, Promotion pr,
-                      int* cnt, const uint8_t* fine, int* act_out, int* host_mapped, int* hist, bool build, int NP,
-                      __half* Whi, __half* Wlo, float* W32);
 
 // Fixed-order slot sum into G_out (L x ldo) and s4_out (L).
 int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int S, int64_t cap, int ldg,
@@ -97,9 +146,10 @@ int launch_slot_reduce(cudaStream_t st, SlotPartials Gp, const double* s4p, int 
 int launch_alpha_refresh(cudaStream_t st, const int* act, const int* cnt, int L_ub, const double* s4, double M,
                          double* alpha_old);
 
-// s4 = w_eval . G (identity sum_m y^3 (w.x) = sum_m y^4), rows by position.
-int launch_s4_from_g(cudaStream_t st, EvalPoint ev, const double* W, const double* G, int ldg, int L, int N,
-                     double* s4);
+// s4 = w_eval . G (identity sum_m y^3 (w.x) = sum_m y^4), G rows by position; the evaluation point
+// of position a is row act[a] (act null: a).
+int launch_s4_from_g(cudaStream_t st, EvalPoint ev, const int* act, const double* G, int ldg, int L, int N,
+                     double* s4, const int* cnt = nullptr);   // cnt: rows a >= cnt[0] are skipped
 
 // ---- C4: hybrid L -> M tail: pack this rank's active rows as records
 // [w (d) | alpha_old | dprev | fine | global id] (dprev, fine may be null), unpack the gathered
@@ -136,10 +186,11 @@ int launch_select_local(cudaStream_t st, const double* W64, const double* alpha_
 // *out = converged candidates on this rank (L-shard: all-reduced into nconv_g of select_local)
 int launch_count_converged(cudaStream_t st, const uint8_t* state, int L, int* out);
 // nonfinite (device, may be null): this rank's count of rows retired by a non-finite update.
+// sum_active < 0: take sum_active and n_iter (= t - 1) from the device iteration state ctl.
 int launch_select_finish(cudaStream_t st, const double* W64, const int* iters, const int* counts,
                          const int* pc, const int* qc, const int* csize, const double* s4c,
                          int64_t id_base, int N, double M_global, uint32_t flags, int64_t sum_active,
-                         int n_iter, const int* nonfinite, RankSummary* summary, double* wsum);
+                         int n_iter, const int* nonfinite, const IterCtl* ctl, RankSummary* summary, double* wsum);
 // Merge all ranks' summaries (world x RankSummary, world x kMaxClusters x N), append the winner to
 // Wacc row k, write the record.
 int launch_merge_accept(cudaStream_t st, const RankSummary* all, const double* wall, int world, int N,
@@ -176,9 +227,11 @@ struct Upload {
 };
 // xshift (device, one int8 per 384-sample block of the local samples, launch_block_shift): the
 // fp16 range shift of the GEMM2 operand; null: no shift.
+// act (device): position a uses operand rows Whi / Wlo [act[a]] (by candidate id).
 int launch_step_tc(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, int NP, const __half* Whi,
-                   const __half* Wlo, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap,
-                   const int* cnt, bool lo_capable, const Upload& up, const SplitOut& so, const int8_t* xshift);
+                   const __half* Wlo, const int* act, int n_coarse, int L_act, int64_t slot_len, int S, float* Gp,
+                   int64_t cap, const int* cnt, bool lo_capable, const Upload& up, const SplitOut& so,
+                   const int8_t* xshift);
 // fp16 range of the tensor-core step (DESIGN.md §5 "range"): for every 384-sample block b of the
 // samples [m_lo, m_hi) (m_lo a multiple of 384), xshift[b] = the least dsh in [0, kMaxShift] with
 // 1.01 max ||x_m||_2 <= 2^(7 + dsh).  The y^3 operand is scaled by 2^(-3 dsh) before its fp16

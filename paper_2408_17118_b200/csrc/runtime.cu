@@ -52,6 +52,7 @@ constexpr int kMaxSlots = 128;
 constexpr int kFlush = 4096;            // fp32 -> fp64 flush period (samples)
 constexpr int64_t kSlotAlign = 384;       // multiple of every TC chunk width (64, 128, 192 samples)
 constexpr int64_t kTcMinSamples = 16384;    // OICA_PREC_AUTO switches to tensor cores at this M
+constexpr int64_t kSimtShortM = 65536;      // FP32 contexts below this M use short slots (plan_slots_for)
 constexpr double kPromoteD = 1e-6;          // TC precision promotion: stagnating d below this ...
 constexpr double kPromoteRatio = 0.3;       // ... (d > this * d_prev: stagnating) ...
 constexpr int kPromoteT = 40;               // ... or t >= this
@@ -152,6 +153,48 @@ struct oica_ctx {
   DevBuf<int8_t> xshift;   // fp16 range shift per 384-sample block (launch_block_shift)
   DevBuf<int> nonfinite;   // rows retired by a non-finite update in the current component
   DevBuf<int> nconv;       // converged count summed over ranks (L-shard selection, reading A4)
+  DevBuf<IterCtl> ctl;     // device iteration state (t, k, update tickets): kernels/kernels.cuh
+  // device-side do-while (CUDA graph with a WHILE node, DESIGN.md §5 "iteration"), rebuilt when a
+  // parameter baked into its kernels changes
+  struct LoopKey {
+    const void* X;
+    const void* Xh;
+    int64_t M, Mg, slot_len, ldx, vld;
+    int vN, vNP, S, L_ub, K, precision;
+    double tol;
+    bool operator==(const LoopKey& o) const { return std::memcmp(this, &o, sizeof(LoopKey)) == 0; }
+  };
+  struct LoopGraph {
+    bool valid = false;
+    LoopKey key{};
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+    void reset() {
+      if (x) cudaGraphExecDestroy(x);
+      if (g) cudaGraphDestroy(g);
+      x = nullptr;
+      g = nullptr;
+      valid = false;
+    }
+  } loop;
+  cudaEvent_t loop_ev0 = nullptr, loop_ev1 = nullptr;
+  // pinned read-back of a component's results (one host wait per component on the fast path):
+  // [ComponentRecord | IterCtl | w (256 doubles) | hist (2 (K + 1) ints)]
+  char* pin = nullptr;
+  size_t pin_bytes = 0;
+  void ensure_pin(int K) {
+    const size_t need = sizeof(ComponentRecord) + sizeof(IterCtl) + 256 * sizeof(double) + 2 * ((size_t)K + 1) * sizeof(int);
+    if (need <= pin_bytes) return;
+    if (pin) cudaFreeHost(pin);
+    pin = nullptr;
+    pin_bytes = 0;
+    OICA_CUDA(cudaHostAlloc((void**)&pin, need, cudaHostAllocDefault));
+    pin_bytes = need;
+  }
+  ComponentRecord* pin_rec() { return (ComponentRecord*)pin; }
+  IterCtl* pin_ctl() { return (IterCtl*)(pin + sizeof(ComponentRecord)); }
+  double* pin_w() { return (double*)(pin + sizeof(ComponentRecord) + sizeof(IterCtl)); }
+  int* pin_hist() { return (int*)(pin + sizeof(ComponentRecord) + sizeof(IterCtl) + 256 * sizeof(double)); }
   // the data the current component iterates on (DESIGN.md §5 "reduced X"): the full whitened X,
   // or X~ = G X in the d = N-k dimensional complement of the accepted rows (OICA_REDUCE_X)
   const float* vX = nullptr;
@@ -178,7 +221,6 @@ struct oica_ctx {
   DevBuf<float> Gsub;   // TC split-slot parts (few active rows, common.cuh split_parts)
   int64_t sub_cap = 0;
   DevBuf<int> Lg;       // global active count (lock-step L-shard: all-reduced every iteration)
-  DevBuf<double> Gred, s4red;   // slot-reduced G, s4 of <= kBatchRows rows
   DevBuf<double> Gfin, s4fin;   // final-w forward pass of the runs active at the cap
   DevBuf<float> W32;
   DevBuf<__half> Whi, Wlo;
@@ -402,7 +444,16 @@ void jacobi_eigh(std::vector<double>& A, int n, std::vector<double>& d, std::vec
 
 // Split-M slot plan: slot length is a function of the GLOBAL M only (determinism across GPU
 // counts, tilings and active-set sizes); the local slot count follows from the local M.
-void plan_slots_for(int64_t M_global, int64_t M_local, int64_t* slot_len, int* S_local) {
+void plan_slots_for(int64_t M_global, int64_t M_local, bool fp32, int64_t* slot_len, int* S_local) {
+  if (fp32 && M_global < kSimtShortM) {
+    // FP32 step at small M (the paper's own experiments, M = 1e4): one CTA per (64-row tile, slot)
+    // streams its slot chunk by chunk, so short slots (>= 128 samples, up to 128 of them, 64-aligned
+    // = the FP32 chunk) give the few row tiles enough CTAs: a 1e4-sample step 23 -> ~6 us
+    const int64_t S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, ceil_div(M_global, 128)));
+    *slot_len = round_up(ceil_div(M_global, S), 64);
+    *S_local = std::max(1, (int)ceil_div(M_local, *slot_len));
+    return;
+  }
   // one CTA per (row tile, slot): long slots amortise each CTA's set-up (TMEM allocation, W
   // load, pipeline fill, G flush: ~13% of the step at 8192-sample slots and N = 128), while up
   // to 30 slots (of >= 128 samples) keep enough CTAs per row tile for small L and small M
@@ -418,12 +469,13 @@ void plan_slots_for(int64_t M_global, int64_t M_local, int64_t* slot_len, int* S
   *S_local = std::max(1, (int)ceil_div(M_local, *slot_len));
 }
 
-void plan_slots(oica_ctx* c) { plan_slots_for(c->Mg, c->M, &c->slot_len, &c->S); }
+void plan_slots(oica_ctx* c) { plan_slots_for(c->Mg, c->M, !c->tc(), &c->slot_len, &c->S); }
 
 void ensure_candidate_buffers(oica_ctx* c) {
   size_t Ll = (size_t)c->Ll, N = (size_t)c->N, NP = (size_t)c->NP;
   c->nonfinite.ensure(1);
   c->nconv.ensure(1);
+  c->ctl.ensure(1);
   c->W64.ensure(Ll * N);
   c->alpha_old.ensure(Ll);
   c->iters.ensure(Ll);
@@ -433,8 +485,6 @@ void ensure_candidate_buffers(oica_ctx* c) {
   c->act1.ensure(Ll);
   c->Lact_dev.ensure(2);
   c->Lg.ensure(1);
-  c->Gred.ensure((size_t)kBatchRows * NP);
-  c->s4red.ensure(kBatchRows);
   c->fine.ensure(Ll);
   c->dprev.ensure(Ll);
   if (c->tc()) {
@@ -481,13 +531,46 @@ void sync_x(oica_ctx* c) {
 }
 
 
-// Build the step-kernel operand rows for the active list `act` (count in Lact_dev, <= cap).
-void build_operand(oica_ctx* c, const int* act, int cap) {
+// Step-kernel operand rows of candidates 0..L-1 (by id) from the fp64 master; afterwards the
+// fused update keeps the rows of the active candidates current.
+void build_operand(oica_ctx* c, int L) {
   if (c->tc())
-    c->count(launch_operand_f16x2(c->st, act, c->Lact_dev.p, cap, c->W64.p, c->vN, c->vNP, c->fine.p,
-                                  c->Whi.p, c->Wlo.p));
+    c->count(launch_operand_f16x2(c->st, L, c->W64.p, c->vN, c->vNP, c->fine.p, c->Whi.p, c->Wlo.p));
   else
-    c->count(launch_operand_f32(c->st, act, c->Lact_dev.p, cap, c->W64.p, c->vN, c->vNP, c->W32.p));
+    c->count(launch_operand_f32(c->st, L, c->W64.p, c->vN, c->vNP, c->W32.p));
+}
+
+// The fused update of one iteration (K3 + K4, kernels.cuh launch_update) over the L_ub (upper
+// bound) active positions of act_in, compacting into act_out.
+UpdateArgs update_args(oica_ctx* c, SlotPartials G, const double* s4, int S, int64_t cap, const int* act_in,
+                       int* act_out, int L_ub, double tol, int* hist) {
+  UpdateArgs u{};
+  u.G = G;
+  u.s4p = s4;
+  u.S = S;
+  u.cap = cap;
+  u.ldg = c->vNP;
+  u.ev = c->eval_point();
+  u.act_in = act_in;
+  u.act_out = act_out;
+  u.copy_back = 0;
+  u.L_ub = L_ub;
+  u.cnt_in = c->Lact_dev.p;
+  u.cnt_out = c->Lact_dev.p;
+  u.host_mapped = c->Lact_host;
+  u.hist = hist;
+  u.Wacc = c->Wacc.p;
+  u.N = c->vN;
+  u.M = (double)c->Mg;
+  u.tol = tol;
+  u.W64 = c->W64.p;
+  u.alpha_old = c->alpha_old.p;
+  u.iters = c->iters.p;
+  u.state = c->state.p;
+  u.keep = c->keep.p;
+  u.pr = c->promotion();
+  u.ctl = c->ctl.p;
+  return u;
 }
 
 #ifdef OICA_EXPERIMENTS
@@ -554,8 +637,8 @@ bool mixed_clusters(const oica_ctx* c, int L_act) {
 // One fused contraction over the active rows (positions 0..L_act-1; rows >= n_coarse are fine)
 // into the slots.  With cnt (device [L_act, n_coarse]) the host values are upper bounds that
 // only size the grid (iterations enqueued without a host round trip).
-void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* cnt_g, bool lo_capable, bool timed,
-              bool split = true) {
+void run_step(oica_ctx* c, const int* act, int L_act, int n_coarse, const int* cnt, const int* cnt_g, bool lo_capable,
+              bool timed, bool split = true) {
   const SplitOut so{c->Gsub.p, c->sub_cap, cnt_g, split ? 1 : 0};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
@@ -573,7 +656,7 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* c
       OICA_CUDA(cudaStreamWaitEvent(c->st, c->piece_ev[p], 0));
       const int s0 = p * spp, s1 = std::min(c->S, s0 + spp);
       if (s1 > s0)
-        n += launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
+        n += launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, act, n_coarse, L_act, c->slot_len,
                             c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{s0, s1 - s0}, so, c->xshift.p);
     }
     sync_x(c);
@@ -597,10 +680,10 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* c
       ~CtxRestore() { api.CtxSetCurrent(prev); }
     } restore(api);
     api.CtxSetCurrent(g.cA);
-    n = launch_step_tc((cudaStream_t)g.sA, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act,
+    n = launch_step_tc((cudaStream_t)g.sA, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, act, n_coarse, L_act,
                        c->slot_len, c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, S_a, 4}, so, c->xshift.p);
     api.CtxSetCurrent(g.cB);
-    n += launch_step_tc((cudaStream_t)g.sB, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act,
+    n += launch_step_tc((cudaStream_t)g.sB, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, act, n_coarse, L_act,
                         c->slot_len, c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{S_a, S_b, 2}, so, c->xshift.p);
     OICA_CUDA(cudaEventRecord(g.jA, (cudaStream_t)g.sA));
     OICA_CUDA(cudaEventRecord(g.jB, (cudaStream_t)g.sB));
@@ -622,20 +705,20 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* c
     }
     OICA_CUDA(cudaEventRecord(c->fork_ev, c->st));
     OICA_CUDA(cudaStreamWaitEvent(c->st2, c->fork_ev, 0));
-    n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len, c->S,
+    n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, act, n_coarse, L_act, c->slot_len, c->S,
                        c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, S_a, 4}, so, c->xshift.p);
-    n += launch_step_tc(c->st2, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len, c->S,
+    n += launch_step_tc(c->st2, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, act, n_coarse, L_act, c->slot_len, c->S,
                         c->Gp32.p, c->Ll, cnt, lo_capable, Upload{S_a, S_b, 2}, so, c->xshift.p);
     OICA_CUDA(cudaEventRecord(c->join_ev, c->st2));
     OICA_CUDA(cudaStreamWaitEvent(c->st, c->join_ev, 0));
 #endif
   } else if (c->tc()) {
     sync_x(c);
-    n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, n_coarse, L_act, c->slot_len,
+    n = launch_step_tc(c->st, c->vXh, c->ldx, c->M, c->vNP, c->Whi.p, c->Wlo.p, act, n_coarse, L_act, c->slot_len,
                        c->S, c->Gp32.p, c->Ll, cnt, lo_capable, Upload{0, c->S}, so, c->xshift.p);
   } else {
     sync_x(c);
-    n = launch_step_simt(c->st, c->vX, c->vld, c->M, c->vN, c->vNP, c->W32.p, L_act, c->slot_len, c->S, kFlush,
+    n = launch_step_simt(c->st, c->vX, c->vld, c->M, c->vN, c->vNP, c->W32.p, act, L_act, c->slot_len, c->S, kFlush,
                          c->Gp.p, c->s4p.p, c->Ll, cnt);
   }
   OICA_CUDA(cudaGetLastError());
@@ -648,8 +731,17 @@ void run_step(oica_ctx* c, int L_act, int n_coarse, const int* cnt, const int* c
 }
 
 // Work counters of one executed iteration with L_act rows, n_coarse of them coarse.
-void account_iteration(oica_ctx* c, int L_act, int n_coarse, int64_t M_work = -1) {
+void account_iteration(oica_ctx* c, int L_act, int n_coarse, int64_t M_work = -1, bool timed = true) {
   if (M_work < 0) M_work = c->M;
+  if (!timed) {   // an iteration of the device-side loop: counted, its step not timed on its own
+    c->stats.iterations += 1;
+    c->stats.sum_active += L_act;
+    c->stats.graph_iterations += 1;
+    c->stats.graph_flops += (double)L_act * (4.0 * (double)c->vN * (double)c->Mg + 3.0 * (double)c->Mg) *
+                            ((double)M_work / (double)c->Mg);
+    if (c->tc()) c->stats.fine_rows += L_act - n_coarse;
+    return;
+  }
   double issued;
   if (c->tc()) {
     int64_t tiles = ceil_div(L_act, 128), lo_tiles = n_coarse < L_act ? tiles - n_coarse / 128 : 0;
@@ -817,11 +909,11 @@ void refresh_unconverged_alpha(oica_ctx* c, const int* act, int L_fin, int n_coa
   const bool tc = c->tc();
   c->Gfin.ensure((size_t)c->Ll * c->vNP);
   c->s4fin.ensure((size_t)c->Ll);
-  build_operand(c, act, L_fin);
   c->cur_t = 0;
+  // (the operand rows of the active runs already hold their final w: the last update wrote them)
   // no split-slot parts: they would depend on the global count, which other ranks may not join
   // here; the plain slot sums make alpha~ of a row the same for any GPU count
-  run_step(c, L_fin, n_coarse, cnt, nullptr, false, false, false);
+  run_step(c, act, L_fin, n_coarse, cnt, nullptr, false, false, false);
   const SlotPartials G = tc ? SlotPartials{c->Gp32.p, true} : SlotPartials{c->Gp.p, false};
   c->count(launch_slot_reduce(st, G, tc ? nullptr : c->s4p.p, c->S, c->Ll, c->vNP, L_fin, vN, c->Gfin.p, c->vNP,
                               c->s4fin.p, cnt));
@@ -830,7 +922,7 @@ void refresh_unconverged_alpha(oica_ctx* c, const int* act, int L_fin, int n_coa
     c->exchange([&] { OICA_NCCL(nc.AllReduce(c->Gfin.p, c->Gfin.p, (size_t)L_fin * c->vNP, ncclFloat64, ncclSum, c->comm, st)); });
     if (!tc) c->exchange([&] { OICA_NCCL(nc.AllReduce(c->s4fin.p, c->s4fin.p, (size_t)L_fin, ncclFloat64, ncclSum, c->comm, st)); });
   }
-  if (tc) c->count(launch_s4_from_g(st, c->eval_point(), c->W64.p, c->Gfin.p, c->vNP, L_fin, vN, c->s4fin.p));
+  if (tc) c->count(launch_s4_from_g(st, c->eval_point(), act, c->Gfin.p, c->vNP, L_fin, vN, c->s4fin.p, cnt));
   c->count(launch_alpha_refresh(st, act, cnt, L_fin, c->s4fin.p, (double)c->Mg, c->alpha_old.p));
   check_launch();
 }
@@ -927,6 +1019,11 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
     pr.fine = tb.fine.p;
     pr.dprev = tb.dprev.p;
   }
+  // operand rows of the gathered runs (by tail index); the updates keep them current
+  if (tc)
+    c->count(launch_operand_f16x2(st, T, tb.W64.p, vN, NP, tb.fine.p, tb.Whi.p, tb.Wlo.p));
+  else
+    c->count(launch_operand_f32(st, T, tb.W64.p, vN, NP, tb.W32.p));
   c->wait();
   int L_ub = ((volatile int*)c->Lact_host)[0], nc_ub = ((volatile int*)c->Lact_host)[1];
   const int nc_first = nc_ub;
@@ -938,21 +1035,18 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
     for (int b = 0; b < B; ++b) {
       ++t;
       const int* cnt = c->Lact_dev.p;
-      if (tc)
-        c->count(launch_operand_f16x2(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.fine.p, tb.Whi.p, tb.Wlo.p));
-      else
-        c->count(launch_operand_f32(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.W32.p));
       cudaEvent_t e0 = c->event();
       c->cur_t = t;
       c->mark_pair();
       OICA_CUDA(cudaEventRecord(e0, st));
       int n = 0;
       if (s_cnt > 0 && tc)
-        n = launch_step_tc(st, c->vXh, c->ldx, c->M, NP, tb.Whi.p, tb.Wlo.p, nc_ub, L_ub, slot_len, S_all, tb.Gp32.p, T,
-                           cnt, B > 1 && !c->split(), Upload{s0, s_cnt}, SplitOut{nullptr, 0, nullptr, 0}, c->xshift.p);
+        n = launch_step_tc(st, c->vXh, c->ldx, c->M, NP, tb.Whi.p, tb.Wlo.p, a_cur, nc_ub, L_ub, slot_len, S_all,
+                           tb.Gp32.p, T, cnt, B > 1 && !c->split(), Upload{s0, s_cnt}, SplitOut{nullptr, 0, nullptr, 0},
+                           c->xshift.p);
       else if (s_cnt > 0)
-        n = launch_step_simt(st, c->vX + m0, c->vld, M_r, vN, NP, tb.W32.p, L_ub, slot_len, s_cnt, kFlush, tb.Gp.p,
-                             tb.s4p.p, T, cnt);
+        n = launch_step_simt(st, c->vX + m0, c->vld, M_r, vN, NP, tb.W32.p, a_cur, L_ub, slot_len, s_cnt, kFlush,
+                             tb.Gp.p, tb.s4p.p, T, cnt);
       check_launch();
       c->count(n);
       c->stats.step_launches += n;
@@ -963,11 +1057,16 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
                                   tb.s4sum.p));
       c->exchange([&] { OICA_NCCL(nc.AllReduce(tb.Gsum.p, tb.Gsum.p, (size_t)L_ub * NP, ncclFloat64, ncclSum, c->comm, st)); });
       if (!tc) c->exchange([&] { OICA_NCCL(nc.AllReduce(tb.s4sum.p, tb.s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st)); });
-      c->count(launch_epilogue(st, SlotPartials{tb.Gsum.p, false}, tc ? nullptr : tb.s4sum.p, 1, T, NP, ev, a_cur,
-                               L_ub, c->Wacc.p, kk, vN, (double)c->Mg, tol, t, tb.W64.p, tb.alpha.p, tb.iters.p,
-                               tb.state.p, tb.keep.p, pr, cnt));
-      c->count(launch_compact(st, a_cur, tb.keep.p, tc ? tb.fine.p : nullptr, L_ub, a_nxt, c->Lact_dev.p,
-                              c->Lact_host, cnt, tb.hist.p + 2 * t));
+      UpdateArgs u = update_args(c, SlotPartials{tb.Gsum.p, false}, tc ? nullptr : tb.s4sum.p, 1, T, a_cur, a_nxt,
+                                 L_ub, tol, tb.hist.p);
+      u.ev = ev;
+      u.W64 = tb.W64.p;
+      u.alpha_old = tb.alpha.p;
+      u.iters = tb.iters.p;
+      u.state = tb.state.p;
+      u.keep = tb.keep.p;
+      u.pr = pr;
+      c->count(launch_update(st, u, NP));
       std::swap(a_cur, a_nxt);
       check_launch();
     }
@@ -977,22 +1076,18 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
   }
   if (L_ub > 0) {   // runs capped in the tail: alpha at their final w (A15; identical on every rank)
     const int* cnt = c->Lact_dev.p;
-    if (tc)
-      c->count(launch_operand_f16x2(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.fine.p, tb.Whi.p, tb.Wlo.p));
-    else
-      c->count(launch_operand_f32(st, a_cur, cnt, L_ub, tb.W64.p, vN, NP, tb.W32.p));
     if (s_cnt > 0 && tc)
-      c->count(launch_step_tc(st, c->vXh, c->ldx, c->M, NP, tb.Whi.p, tb.Wlo.p, nc_ub, L_ub, slot_len, S_all,
+      c->count(launch_step_tc(st, c->vXh, c->ldx, c->M, NP, tb.Whi.p, tb.Wlo.p, a_cur, nc_ub, L_ub, slot_len, S_all,
                               tb.Gp32.p, T, cnt, false, Upload{s0, s_cnt}, SplitOut{nullptr, 0, nullptr, 0}, c->xshift.p));
     else if (s_cnt > 0)
-      c->count(launch_step_simt(st, c->vX + m0, c->vld, M_r, vN, NP, tb.W32.p, L_ub, slot_len, s_cnt, kFlush, tb.Gp.p,
-                                tb.s4p.p, T, cnt));
+      c->count(launch_step_simt(st, c->vX + m0, c->vld, M_r, vN, NP, tb.W32.p, a_cur, L_ub, slot_len, s_cnt, kFlush,
+                                tb.Gp.p, tb.s4p.p, T, cnt));
     SlotPartials part = tc ? SlotPartials{tb.Gp32.p + (size_t)s0 * T * NP, true} : SlotPartials{tb.Gp.p, false};
     c->count(launch_slot_reduce(st, part, tc ? nullptr : tb.s4p.p, s_cnt, T, NP, L_ub, vN, tb.Gsum.p, NP,
                                 tb.s4sum.p));
     c->exchange([&] { OICA_NCCL(nc.AllReduce(tb.Gsum.p, tb.Gsum.p, (size_t)L_ub * NP, ncclFloat64, ncclSum, c->comm, st)); });
     if (!tc) c->exchange([&] { OICA_NCCL(nc.AllReduce(tb.s4sum.p, tb.s4sum.p, (size_t)L_ub, ncclFloat64, ncclSum, c->comm, st)); });
-    if (tc) c->count(launch_s4_from_g(st, ev, tb.W64.p, tb.Gsum.p, NP, L_ub, vN, tb.s4sum.p));
+    if (tc) c->count(launch_s4_from_g(st, ev, a_cur, tb.Gsum.p, NP, L_ub, vN, tb.s4sum.p, cnt));
     c->count(launch_alpha_refresh(st, a_cur, cnt, L_ub, tb.s4sum.p, (double)c->Mg, tb.alpha.p));
     check_launch();
   }
@@ -1015,6 +1110,71 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
     ++c->stats.tail_iterations;
   }
   return c->cfg.rank == 0 ? sum_active : 0;
+}
+
+// The do-while of PAPER.md:241-256 for short iterations, on the device: a CUDA graph whose WHILE
+// node runs [fused step over the active list act0 (grid sized for L_ub rows); fused update act0 ->
+// act1 with copy-back, whose last block also sets the loop condition] until no run is active or
+// t > K.  One graph launch (and one
+// host wait) per component instead of a host round trip per batch of iterations; the kernels are
+// those of the host-launched loop with the same upper-bound sizing, so results are bitwise equal
+// (tests/test_gpu_parity.py::test_device_loop_bitwise).  Enqueues only (no host wait).
+void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
+  cudaStream_t st = c->st;
+  const oica_ctx::LoopKey key{c->vX, c->vXh, c->M, c->Mg, c->slot_len, c->ldx, c->vld, c->vN, c->vNP, c->S,
+                              L_ub, K, c->precision, tol};
+  if (!(c->loop.valid && c->loop.key == key)) {
+    c->loop.reset();
+    OICA_CUDA(cudaGraphCreate(&c->loop.g, 0));
+    cudaGraphConditionalHandle h;
+    OICA_CUDA(cudaGraphConditionalHandleCreate(&h, c->loop.g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    OICA_CUDA(cudaGraphAddNode(&wnode, c->loop.g, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    OICA_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    try {
+      const int* cnt = c->Lact_dev.p;
+      run_step(c, c->act0.p, L_ub, nc_ub, cnt, cnt, c->tc() && !c->split(), false);
+      UpdateArgs u = update_args(c, c->partials(cnt, L_ub), c->tc() ? nullptr : c->s4p.p, c->S, c->Ll, c->act0.p,
+                                 c->act1.p, L_ub, tol, c->hist.p);
+      u.copy_back = 1;
+      u.loop = h;
+      u.K_loop = K;
+      launch_update(st, u, c->vNP);
+      check_launch();
+    } catch (...) {
+      cudaGraph_t junk;
+      cudaStreamEndCapture(st, &junk);
+      c->loop.reset();
+      throw;
+    }
+    cudaGraph_t captured;
+    OICA_CUDA(cudaStreamEndCapture(st, &captured));
+    OICA_CUDA(cudaGraphInstantiate(&c->loop.x, c->loop.g, 0));
+    c->loop.key = key;
+    c->loop.valid = true;
+  }
+  if (!c->loop_ev0) {
+    OICA_CUDA(cudaEventCreate(&c->loop_ev0));
+    OICA_CUDA(cudaEventCreate(&c->loop_ev1));
+  }
+  OICA_CUDA(cudaEventRecord(c->loop_ev0, st));
+  OICA_CUDA(cudaGraphLaunch(c->loop.x, st));
+  OICA_CUDA(cudaEventRecord(c->loop_ev1, st));
+}
+
+// counters of a finished device-side loop of `iters` iterations (after the host wait)
+void finish_loop_graph(oica_ctx* c, int iters) {
+  float ms = 0.f;
+  OICA_CUDA(cudaEventElapsedTime(&ms, c->loop_ev0, c->loop_ev1));
+  c->stats.graph_ms += ms;
+  c->count(2 * std::max(iters, 1));
+  c->stats.step_launches += std::max(iters, 1);
 }
 
 void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t flags, const double* W_prefix,
@@ -1090,16 +1250,23 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     else
       c->count(launch_cand_init(st, c->seed, i, c->id_base, c->Ll, N, c->Wacc.p, k, c->W64.p, c->state.p, c->keep.p,
                                 c->fine.p, c->split() ? 1 : 0, c->dprev.p));
+    // one rank, short iterations (the paper's own experiment sizes): the component -- draw,
+    // device-side do-while, alpha refresh, selection, accept -- is enqueued without a host round
+    // trip and its counters are read back once at the end (DESIGN.md §5 "iteration")
+    const bool fast = !c->collective() && !c->reduced && !(flags & OICA_EAGER) &&
+                      (double)c->M * (double)c->vNP < kBatchMaxWork;
     c->count(launch_compact(st, nullptr, c->keep.p, c->fine_flags(), (int)c->Ll, c->act0.p, c->Lact_dev.p,
-                            c->Lact_host));
+                            c->Lact_host, nullptr, c->hist.p));   // hist[0..1]: runs entering iteration 1
     OICA_CUDA(cudaMemsetAsync(c->nonfinite.p, 0, sizeof(int), st));
-    c->wait();
+    c->count(launch_ctl_set(st, c->ctl.p, 1, kk));   // iteration t = 1, k accepted rows projected out
+    build_operand(c, (int)c->Ll);
+    if (!fast) c->wait();
     trace.mark("init");
-    int L_act = ((volatile int*)c->Lact_host)[0];
-    int n_coarse = ((volatile int*)c->Lact_host)[1];
+    // fast: upper bounds (every kernel takes the true counts from the device)
+    int L_act = fast ? (int)c->Ll : ((volatile int*)c->Lact_host)[0];
+    int n_coarse = fast ? (c->split() ? 0 : (int)c->Ll) : ((volatile int*)c->Lact_host)[1];
     int* act = c->act0.p;
     int* act_next = c->act1.p;
-    build_operand(c, act, L_act);
     // a2-a6: the do-while of PAPER.md:241-256.  Iterations are enqueued in batches without a
     // host round trip once few rows remain (every kernel takes the true active count from the
     // device counters; the host value is an upper bound that sizes the grids); the per-iteration
@@ -1123,7 +1290,11 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     };
     if (lockstep) OICA_CUDA(cudaMemsetAsync(c->hist.p, 0, sizeof(int) * 2 * ((size_t)K + 1), st));
     bool to_tail = lockstep && refresh();
-    while (!to_tail && (lockstep ? G_ub : L_ub) > 0 && t < K) {
+    if (fast) {   // the whole do-while on the device (one graph launch)
+      sync_x(c);   // (a pipelined upload is waited for: the graph is captured on the context stream)
+      enqueue_loop_graph(c, L_ub, nc_ub, K, tol);
+    }
+    while (!fast && !to_tail && (lockstep ? G_ub : L_ub) > 0 && t < K) {
       // batches only where an iteration is short next to a host round trip (one row tile over
       // M samples: ~M NP 512 flop); elsewhere the exact count sizes every launch (grid, clusters)
       const bool short_iter = (double)c->M * (double)c->vNP < kBatchMaxWork;
@@ -1140,7 +1311,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         }
         if (L_ub == 0) continue;   // lock step: this rank idles while others iterate
         c->cur_t = t;
-        run_step(c, L_ub, nc_ub, cnt, cnt_g, B > 1 && c->tc() && !c->split(), true);
+        run_step(c, act, L_ub, nc_ub, cnt, cnt_g, B > 1 && c->tc() && !c->split(), true);
         const bool tc = c->tc();
         SlotPartials G = c->partials(cnt_g, L_ub);
         const double* s4 = tc ? nullptr : c->s4p.p;   // TC: alpha~ from the identity w_e . G (K3)
@@ -1155,31 +1326,11 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
           s4 = tc ? nullptr : c->s4sum.p;
           S = 1;
           cap = c->Ll;
-        } else if (L_ub <= kBatchRows) {
-          // few rows: the S (x P) partial sums of an element are a serial chain; reduce them with
-          // one thread per (row, coordinate) first (same function, same order: bitwise the same)
-          c->count(launch_slot_reduce(st, G, s4, c->S, c->Ll, c->vNP, L_ub, vN, c->Gred.p, c->vNP, c->s4red.p, cnt));
-          G = SlotPartials{c->Gred.p, false};
-          s4 = tc ? nullptr : c->s4red.p;
-          S = 1;
-          cap = kBatchRows;
         }
-        if (!c->mshard() && L_ub <= kIterSmallRows) {   // epilogue + compaction + operand: one launch
-          c->count(launch_iter_small(st, G, s4, S, cap, c->vNP, c->eval_point(), act, L_ub, c->Wacc.p, kk, vN,
-                                     (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p,
-                                     c->keep.p, c->promotion(), c->Lact_dev.p, c->fine_flags(), act_next,
-                                     c->Lact_host, c->hist.p + 2 * t, t < K, c->vNP, tc ? c->Whi.p : nullptr,
-                                     tc ? c->Wlo.p : nullptr, tc ? nullptr : c->W32.p));
-          std::swap(act, act_next);
-        } else {
-          c->count(launch_epilogue(st, G, s4, S, cap, c->vNP, c->eval_point(), act, L_ub, c->Wacc.p, kk, vN,
-                                   (double)c->Mg, tol, t, c->W64.p, c->alpha_old.p, c->iters.p, c->state.p,
-                                   c->keep.p, c->promotion(), cnt));
-          c->count(launch_compact(st, act, c->keep.p, c->fine_flags(), L_ub, act_next, c->Lact_dev.p, c->Lact_host,
-                                  cnt, c->hist.p + 2 * t));
-          std::swap(act, act_next);
-          if (t < K) build_operand(c, act, L_ub);
-        }
+        // K3 + K4 in one launch: slot sums, eq. (5), projection, convergence, next operand rows,
+        // compaction by the last block (DESIGN.md §5 "iteration")
+        c->count(launch_update(st, update_args(c, G, s4, S, cap, act, act_next, L_ub, tol, c->hist.p), c->vNP));
+        std::swap(act, act_next);
         check_launch();
       }
       trace.batch_enqueued();
@@ -1197,30 +1348,34 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     // point); where they can be selected (reading A4: no run converged, or
     // OICA_INCLUDE_UNCONVERGED) rank them by alpha at their final w, as PAPER.md:257-258 does:
     // one more forward pass over those rows (L-shard / single GPU; M-shard sums ranks).
-    if (!to_tail && L_ub > 0 && t >= K) refresh_unconverged_alpha(c, act, L_ub, nc_ub, vN);
+    // (fast: always enqueued -- its kernels do nothing when no run is active at the cap)
+    if (fast || (!to_tail && L_ub > 0 && t >= K)) refresh_unconverged_alpha(c, act, L_ub, nc_ub, vN);
     trace.mark("iterate");
-    // per-iteration counts: entering iteration t' the active set had hist[t'-1] rows (t' >= 2)
-    std::vector<int> hist(2 * (size_t)(t_bulk + 1), 0);
-    if (t_bulk > 0) {
-      OICA_CUDA(cudaMemcpyAsync(hist.data(), c->hist.p, sizeof(int) * 2 * (size_t)(t_bulk + 1), cudaMemcpyDeviceToHost,
-                                st));
-      c->wait();
+    int64_t sum_active = -1;   // fast: the selection takes it (and n_iter) from the device state
+    if (!fast) {
+      // per-iteration counts: entering iteration t' the active set had hist[t'-1] rows (t' >= 2)
+      std::vector<int> hist(2 * (size_t)(t_bulk + 1), 0);
+      if (t_bulk > 0) {
+        OICA_CUDA(cudaMemcpyAsync(hist.data(), c->hist.p, sizeof(int) * 2 * (size_t)(t_bulk + 1),
+                                  cudaMemcpyDeviceToHost, st));
+        c->wait();
+      }
+      sum_active = 0;
+      int t_exec = 0;
+      for (int tt = 1; tt <= t_bulk; ++tt) {
+        int Lin = tt == 1 ? L0 : hist[2 * (tt - 1)], ncin = tt == 1 ? nc0 : hist[2 * (tt - 1) + 1];
+        if (Lin <= 0) break;
+        account_iteration(c, Lin, ncin);
+        sum_active += Lin;
+        rows_at[tt] = {Lin, ncin};
+        t_exec = tt;
+      }
+      if (to_tail) {   // the tail's rows were counted by rank 0 (the merge sums ranks)
+        sum_active += tail_active;
+        t_exec = t;
+      }
+      t = t_exec;
     }
-    int64_t sum_active = 0;
-    int t_exec = 0;
-    for (int tt = 1; tt <= t_bulk; ++tt) {
-      int Lin = tt == 1 ? L0 : hist[2 * (tt - 1)], ncin = tt == 1 ? nc0 : hist[2 * (tt - 1) + 1];
-      if (Lin <= 0) break;
-      account_iteration(c, Lin, ncin);
-      sum_active += Lin;
-      rows_at[tt] = {Lin, ncin};
-      t_exec = tt;
-    }
-    if (to_tail) {   // the tail's rows were counted by rank 0 (the merge sums ranks)
-      sum_active += tail_active;
-      t_exec = t;
-    }
-    t = t_exec;
     // a7: selection and accept
     sync_x(c);   // the exact-alpha pass reads X (a rank may reach here without running a step)
     const int* nconv_g = nullptr;
@@ -1235,8 +1390,8 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     if (c->mshard())
       c->exchange([&] { OICA_NCCL(Nccl::get().AllReduce(c->s4c.p, c->s4c.p, kMaxClusters, ncclFloat64, ncclSum, c->comm, st)); });
     c->count(launch_select_finish(st, c->W64.p, c->iters.p, c->counts.p, c->pc.p, c->qc.p, c->csize.p, c->s4c.p,
-                                  c->id_base, vN, (double)c->Mg, flags, sum_active, t, c->nonfinite.p, c->summary.p,
-                                  c->wsum.p));
+                                  c->id_base, vN, (double)c->Mg, flags, sum_active, t, c->nonfinite.p, c->ctl.p,
+                                  c->summary.p, c->wsum.p));
     const RankSummary* all = c->summary.p;
     const double* wall = c->wsum.p;
     int world = 1;
@@ -1254,19 +1409,42 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
                                  c->reduced ? c->Wacc_scratch.p : c->Wacc.p, c->reduced ? 0 : k, c->rec.p,
                                  c->w_out.p));
     check_launch();
-    OICA_CUDA(cudaMemcpyAsync(&rec_h, c->rec.p, sizeof(ComponentRecord), cudaMemcpyDeviceToHost, st));
-    OICA_CUDA(cudaMemcpyAsync(b_host.data(), c->w_out.p, sizeof(double) * vN, cudaMemcpyDeviceToHost, st));
-    c->harvest_events();
-    for (const auto& pr : c->pairs) {   // per-iteration log: launches of executed iterations
-      const int tt = pr.first;
-      if (tt < 1 || tt > K || rows_at[tt].first <= 0) continue;
+    c->ensure_pin(K);
+    OICA_CUDA(cudaMemcpyAsync(c->pin_rec(), c->rec.p, sizeof(ComponentRecord), cudaMemcpyDeviceToHost, st));
+    OICA_CUDA(cudaMemcpyAsync(c->pin_w(), c->w_out.p, sizeof(double) * vN, cudaMemcpyDeviceToHost, st));
+    if (fast) {
+      OICA_CUDA(cudaMemcpyAsync(c->pin_ctl(), c->ctl.p, sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
+      OICA_CUDA(cudaMemcpyAsync(c->pin_hist(), c->hist.p, sizeof(int) * 2 * ((size_t)K + 1), cudaMemcpyDeviceToHost,
+                                st));
+    }
+    c->harvest_events();   // the component's one host wait on the fast path
+    rec_h = *c->pin_rec();
+    std::copy(c->pin_w(), c->pin_w() + vN, b_host.begin());
+    if (fast) {   // counters of the device-side loop
+      t = c->pin_ctl()->t - 1;
+      const int* hh = c->pin_hist();
+      for (int tt = 1; tt <= t; ++tt) {
+        const int Lin = hh[2 * (tt - 1)], ncin = hh[2 * (tt - 1) + 1];
+        if (Lin <= 0) break;
+        account_iteration(c, Lin, ncin, -1, false);
+        rows_at[tt] = {Lin, ncin};
+      }
+      finish_loop_graph(c, t);
+    }
+    // per-iteration log: every executed iteration; step_ms from its launch's events, or -1 for the
+    // iterations of the device-side loop (not timed one by one)
+    std::vector<double> step_ms_at((size_t)K + 2, -1.0);
+    for (const auto& pr : c->pairs)
+      if (pr.first >= 1 && pr.first <= K) step_ms_at[pr.first] = std::max(0.0, step_ms_at[pr.first]) + pr.second;
+    for (int tt = 1; tt <= t; ++tt) {
+      if (rows_at[tt].first <= 0) continue;
       const int Lin = rows_at[tt].first, ncin = rows_at[tt].second;
       oica_iteration_record r{};
       r.component = i;
       r.iteration = tt;
       r.L_act = Lin;
       r.fine_rows = Lin - ncin;
-      r.step_ms = pr.second;
+      r.step_ms = step_ms_at[tt];
       r.flops = (double)Lin * (4.0 * vN + 3.0) * (double)c->M;
       c->iter_log.push_back(r);
     }
@@ -1448,6 +1626,14 @@ oica_status oica_destroy(oica_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   if (c->comm) Nccl::get().CommDestroy(c->comm);
   for (auto e : c->ev) cudaEventDestroy(e);
+  for (auto& e : c->xev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c->loop.reset();
+  if (c->loop_ev0) cudaEventDestroy(c->loop_ev0);
+  if (c->loop_ev1) cudaEventDestroy(c->loop_ev1);
+  if (c->pin) cudaFreeHost(c->pin);
   if (c->Lact_host) cudaFreeHost(c->Lact_host);
   if (c->cst) {
     cudaStreamSynchronize(c->cst);
@@ -1692,13 +1878,13 @@ oica_status oica_fixed_point_step_mixed(oica_ctx* c, const double* W_dev, int64_
     else
       OICA_CUDA(cudaMemsetAsync(c->fine.p, c->split() ? 1 : 0, L, c->st));   // one precision for all rows
     c->count(launch_compact(c->st, nullptr, c->keep.p, nullptr, (int)L, c->act0.p, c->Lact_dev.p, nullptr));
-    build_operand(c, c->act0.p, (int)L);
-    run_step(c, (int)L, n_coarse, nullptr, nullptr, false, true);
+    build_operand(c, (int)L);
+    run_step(c, c->act0.p, (int)L, n_coarse, nullptr, nullptr, false, true);
     account_iteration(c, (int)L, n_coarse);
     bool tc = c->tc();
     c->count(launch_slot_reduce(c->st, c->partials(nullptr, (int)L), tc ? nullptr : c->s4p.p, c->S, c->Ll, (int)c->NP, (int)L,
                                 (int)c->N, G_dev, (int)c->N, s4_dev));
-    if (tc) c->count(launch_s4_from_g(c->st, c->eval_point(), c->W64.p, G_dev, (int)c->N, (int)L, (int)c->N, s4_dev));
+    if (tc) c->count(launch_s4_from_g(c->st, c->eval_point(), nullptr, G_dev, (int)c->N, (int)L, (int)c->N, s4_dev));
     check_launch();
     c->harvest_events();
   });
@@ -1779,10 +1965,14 @@ oica_status oica_synchronize(oica_ctx* c) {
   return guard(c, [&] { c->wait(); });
 }
 
-oica_status oica_slot_plan(int64_t M_global, int64_t M_local, int64_t* slot_len, int32_t* S_local) {
-  if (!slot_len || !S_local || M_global < 1 || M_local < 1 || M_local > M_global) return OICA_ERR_INVALID_ARGUMENT;
+oica_status oica_slot_plan(int32_t precision, int64_t M_global, int64_t M_local, int64_t* slot_len,
+                           int32_t* S_local) {
+  if (!slot_len || !S_local || M_global < 1 || M_local < 1 || M_local > M_global || precision < OICA_PREC_AUTO ||
+      precision > OICA_PREC_TC_SPLIT)
+    return OICA_ERR_INVALID_ARGUMENT;
   int s = 0;
-  plan_slots_for(M_global, M_local, slot_len, &s);
+  const bool fp32 = precision == OICA_PREC_FP32 || (precision == OICA_PREC_AUTO && M_global < kTcMinSamples);
+  plan_slots_for(M_global, M_local, fp32, slot_len, &s);
   *S_local = s;
   return OICA_OK;
 }

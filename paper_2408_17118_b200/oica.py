@@ -28,7 +28,7 @@ STATUS = ["OK", "INVALID_ARGUMENT", "DIMENSION_MISMATCH", "RANK_DEFICIENT", "ALL
 
 PREC_AUTO, PREC_FP32, PREC_TC, PREC_TC_SPLIT = 0, 1, 2, 3
 SHARD_L, SHARD_M, SHARD_HYBRID = 0, 1, 2
-INCLUDE_UNCONVERGED, STOP_ON_GAUSSIANITY, RAW_ARGMAX, REDUCE_X = 0x1, 0x2, 0x4, 0x8
+INCLUDE_UNCONVERGED, STOP_ON_GAUSSIANITY, RAW_ARGMAX, REDUCE_X, EAGER = 0x1, 0x2, 0x4, 0x8, 0x10
 MAX_CLUSTERS = 8
 
 
@@ -62,7 +62,8 @@ class Stats(C.Structure):
                 ("step_flops", C.c_double), ("iterations", C.c_int64), ("sum_active", C.c_int64),
                 ("precision", C.c_int32), ("slots", C.c_int32), ("step_issued_flops", C.c_double),
                 ("fine_rows", C.c_int64), ("tail_iterations", C.c_int64), ("exchange_ms", C.c_double),
-                ("exchange_calls", C.c_int64)]
+                ("exchange_calls", C.c_int64), ("graph_iterations", C.c_int64), ("graph_ms", C.c_double),
+                ("graph_flops", C.c_double)]
 
 
 class IterationRecord(C.Structure):
@@ -104,7 +105,7 @@ SIGNATURES = {
     "oica_merge_records": (C.c_int, [_P(ClusterRecord), _P(C.c_double), C.c_int32, C.c_int32, _P(C.c_int32),
                                      _P(C.c_int64), _P(C.c_uint8)]),
     "oica_complement_basis": (C.c_int, [_P(C.c_double), C.c_int32, C.c_int32, _P(C.c_double)]),
-    "oica_slot_plan": (C.c_int, [C.c_int64, C.c_int64, _P(C.c_int64), _P(C.c_int32)]),
+    "oica_slot_plan": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, _P(C.c_int64), _P(C.c_int32)]),
     "oica_split_parts": (C.c_int, [C.c_int32, C.c_int32, _P(C.c_int32)]),
     "oica_deflate_basis": (C.c_int, [_P(C.c_double), C.c_int32, C.c_int32, _P(C.c_double), _P(C.c_double)]),
 }
@@ -188,10 +189,11 @@ def complement_basis(W, N):
     return G
 
 
-def slot_plan(M_global, M_local=None):
+def slot_plan(M_global, M_local=None, precision=PREC_TC):
     """Host-only (oica_slot_plan): (slot_len, S_local) of the step kernels' split-M slots."""
     ln, S = C.c_int64(), C.c_int32()
-    _check(lib().oica_slot_plan(M_global, M_global if M_local is None else M_local, C.byref(ln), C.byref(S)))
+    _check(lib().oica_slot_plan(precision, M_global, M_global if M_local is None else M_local, C.byref(ln),
+                                C.byref(S)))
     return ln.value, S.value
 
 

@@ -133,15 +133,20 @@ def test_split_parts_host():
 
 @pytest.mark.parametrize("M", [1, 2000, 5003, 20000, 150001, 250000, 1_000_000, 4_000_000, 40_000_000])
 def test_slot_plan_host(M):
-    """Slots (the fixed fp32-accumulation units of every row): a function of the global M only,
-    384-aligned (a multiple of every kernel chunk width), covering M; an M-sharded rank's slots
-    have the same length and cover its samples."""
-    ln, S = oica.slot_plan(M)
-    assert ln % 384 == 0 and 1 <= S <= 128 and (S - 1) * ln < M <= S * ln
-    for world in (2, 8):
-        ml = -(-M // world)
-        ln2, S2 = oica.slot_plan(M, min(ml, M))
-        assert ln2 == ln and (S2 - 1) * ln2 < min(ml, M) <= S2 * ln2
+    """Slots (the fixed fp32-accumulation units of every row): a function of the global M and the
+    precision only, a multiple of the kernel chunk widths (tensor cores: 384; FP32 at small M: 64),
+    covering M; an M-sharded rank's slots have the same length and cover its samples."""
+    for prec in (oica.PREC_TC, oica.PREC_FP32, oica.PREC_AUTO):
+        ln, S = oica.slot_plan(M, precision=prec)
+        fp32 = prec == oica.PREC_FP32 or (prec == oica.PREC_AUTO and M < 16384)
+        align = 64 if fp32 and M < 65536 else 384
+        assert ln % align == 0 and 1 <= S <= 128 and (S - 1) * ln < M <= S * ln, (prec, ln, S)
+        if fp32 and M < 65536:
+            assert ln >= min(128, 64 * -(-M // 64)) and (S == 128 or ln <= 192)   # short slots: many CTAs
+        for world in (2, 8):
+            ml = -(-M // world)
+            ln2, S2 = oica.slot_plan(M, min(ml, M), precision=prec)
+            assert ln2 == ln and (S2 - 1) * ln2 < min(ml, M) <= S2 * ln2
 
 
 def test_bench_refuses_experiment_variables():

@@ -133,10 +133,12 @@ def test_step_mixed_precision_tile_independent(name, boundary):
     assert ef < 0.5 * ec, (ef, ec)
 
 
-@pytest.mark.parametrize("name,flags", [("p_tc_n128", 0), ("p_n40", 0), ("p_tc_n128", oica.REDUCE_X)])
+@pytest.mark.parametrize("name,flags", [("p_tc_n128", 0), ("p_n40", 0), ("p_tc_n128", oica.REDUCE_X),
+                                        ("p_tc_n128", oica.EAGER), ("p_n40", oica.EAGER)])
 def test_iteration_log(name, flags):
     """oica_get_iteration_log (SURVEY §8(d) per-iteration logs): one record per executed iteration,
-    consistent with the per-component result counters."""
+    consistent with the per-component result counters; step_ms per launch for host-launched
+    iterations (OICA_EAGER, the reduced form), -1 inside the device-side loop."""
     cfg, ctx = ctx_for(name)
     with ctx:
         res = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=flags)
@@ -147,10 +149,30 @@ def test_iteration_log(name, flags):
         assert [r["iteration"] for r in recs] == list(range(1, len(recs) + 1))
         assert len(recs) == res.n_iter[k]
         assert sum(r["L_act"] for r in recs) == res.sum_active[k]
-        assert all(r["L_act"] >= max(1, r["fine_rows"]) and r["step_ms"] > 0 for r in recs)
+        timed = bool(flags & oica.EAGER) or bool(flags & oica.REDUCE_X and k > 0)   # (reduced: from component 2)
+        assert all(r["L_act"] >= max(1, r["fine_rows"]) and (r["step_ms"] > 0 if timed else r["step_ms"] == -1)
+                   for r in recs)
         assert all(a["L_act"] >= b["L_act"] for a, b in zip(recs, recs[1:]))   # runs only leave
         d = cfg.N - k if flags & oica.REDUCE_X and k else cfg.N
         assert all(r["flops"] == pytest.approx(r["L_act"] * (4 * d + 3) * cfg.M) for r in recs)
+
+
+@pytest.mark.parametrize("name,precision", [("p_n40", oica.PREC_FP32), ("p_tc_n128", oica.PREC_AUTO),
+                                            ("p_tc_n32", oica.PREC_TC_SPLIT), ("p_ragged", oica.PREC_TC)])
+def test_device_loop_bitwise(name, precision):
+    """The device-side do-while (one CUDA-graph WHILE loop per component, DESIGN.md §5 "iteration")
+    gives bitwise the result of host-launched iterations (OICA_EAGER), also at a small cap K where
+    runs stop at t = K, and with unconverged runs competing (their final-w alpha refresh)."""
+    cfg, ctx = ctx_for(name, precision)
+    with ctx:
+        for K, fl in ((cfg.K, 0), (4, oica.INCLUDE_UNCONVERGED)):
+            g = ctx.extract(cfg.N_out, K, cfg.tol, flags=fl)
+            st = ctx.stats()
+            e = ctx.extract(cfg.N_out, K, cfg.tol, flags=fl | oica.EAGER)
+            assert st["graph_iterations"] > 0
+            for f in ("W", "alpha", "index", "iters", "n_iter", "cluster_size", "n_converged", "sum_active"):
+                assert np.array_equal(getattr(g, f), getattr(e, f)), f
+            ctx.reset_stats()
 
 
 def _compare(res_gpu, res_or, W_or, X64, st_or=None):
