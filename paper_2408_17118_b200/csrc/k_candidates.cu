@@ -337,6 +337,27 @@ __device__ __forceinline__ int2 compact_block(const int* __restrict__ act_in, co
   return make_int2(n_coarse + n_fine, n_coarse);
 }
 
+// End of an iteration (one thread): counts, history, iteration state, loop condition.
+__device__ __forceinline__ void finish_iteration(const UpdateArgs& u, int2 r, int L_in, int t) {
+  u.cnt_out[0] = r.x;
+  u.cnt_out[1] = r.y;
+  if (u.host_mapped) {
+    ((volatile int*)u.host_mapped)[0] = r.x;
+    ((volatile int*)u.host_mapped)[1] = r.y;
+  }
+  u.ctl->done = 0u;
+  if (L_in > 0) {   // an executed iteration (a host-launched batch may enqueue a few beyond the last)
+    if (u.hist) {
+      u.hist[2 * t] = r.x;
+      u.hist[2 * t + 1] = r.y;
+    }
+    u.ctl->t = t + 1;
+    u.ctl->sum_active += L_in;
+  }
+  // do ... while (t < K and B != {})
+  if (u.loop) cudaGraphSetConditional(u.loop, (L_in > 0 && r.x > 0 && t + 1 <= u.K_loop) ? 1u : 0u);
+}
+
 // K3 + K4 fused (see launch_update).  Block = 16 warps = RPB rows x NG warps: the NG warps of a
 // row sum its slot partials, 32 coordinates each, in fixed slot order (the association of every
 // consumer of the slot partials: a row's G is bitwise the same whatever path or GPU count reduces
@@ -354,8 +375,8 @@ __global__ void __launch_bounds__(512) k_update(UpdateArgs u) {
   const int rb = warp / NG, grp = warp - rb * NG;
   const int t = u.ctl->t, k = u.ctl->k;
   const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
-  const bool single = L_in <= RPB;   // grid-uniform
-  if (single && blockIdx.x != 0) return;
+  const bool single = L_in <= RPB && u.compact;   // grid-uniform
+  if (L_in <= RPB && blockIdx.x != 0) return;
   const int a = blockIdx.x * RPB + rb;
   const bool row_ok = rb < RPB && a < L_in;
   int l = 0;
@@ -378,9 +399,10 @@ __global__ void __launch_bounds__(512) k_update(UpdateArgs u) {
     const bool kp = epilogue_core<NG>(l, lane, acc, u.s4p ? s4sh[rb] : 0.0, wo, we, u, k, t);
     if (lane == 0) {
       s_keep[rb] = kp ? 1 : 0;
-      if (!single) u.keep[a] = kp ? 1 : 0;
+      if (!single || !u.compact) u.keep[a] = kp ? 1 : 0;
     }
   }
+  if (!u.compact) return;   // (k_compact follows)
   int2 r;
   if (single) {   // K4 by one warp: kept coarse rows, then kept fine rows (k_compact's order)
     __syncthreads();
@@ -416,25 +438,45 @@ __global__ void __launch_bounds__(512) k_update(UpdateArgs u) {
       for (int j = threadIdx.x; j < r.x; j += blockDim.x) dst[j] = u.act_out[j];
     }
   }
-  if (threadIdx.x == 0) {
-    u.cnt_out[0] = r.x;
-    u.cnt_out[1] = r.y;
-    if (u.host_mapped) {
-      ((volatile int*)u.host_mapped)[0] = r.x;
-      ((volatile int*)u.host_mapped)[1] = r.y;
-    }
-    u.ctl->done = 0u;
-    if (L_in > 0) {   // an executed iteration (a host-launched batch may enqueue a few beyond the last)
-      if (u.hist) {
-        u.hist[2 * t] = r.x;
-        u.hist[2 * t + 1] = r.y;
-      }
-      u.ctl->t = t + 1;
-      u.ctl->sum_active += L_in;
-    }
-    // do ... while (t < K and B != {})
-    if (u.loop) cudaGraphSetConditional(u.loop, (L_in > 0 && r.x > 0 && t + 1 <= u.K_loop) ? 1u : 0u);
+  if (threadIdx.x == 0) finish_iteration(u, r, L_in, t);
+}
+
+// K3 for many rows (L_ub > kUpdateCompactRows: the HBM-bound regime, where occupancy and not the
+// latency of one row matters): one warp per row with V coordinates per lane (slot sums in the same
+// sequential order as k_update), 8 rows per block; keep[] for k_compact_iter.
+template <int V, bool F32>
+__global__ void __launch_bounds__(256) k_update_rows(UpdateArgs u) {
+  const int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const int t = u.ctl->t, k = u.ctl->k;
+  const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
+  if (a >= L_in) return;
+  const int l = u.act_in[a];
+  double wo[V], we[V], acc[V];
+  load_row<V>(u, l, lane, wo, we);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int n = lane + 32 * v;
+    acc[v] = n < u.N ? slot_sum<(V >= 8 ? 2 : 8 / V), (F32 ? 2 : 1)>(u.G, u.S, u.cap, u.ldg, a, n) : 0.0;
   }
+  double s4 = 0.0;
+  if (u.s4p && lane == 0) s4 = ordered_sum(u.S, [&](int s) { return __ldg(u.s4p + (int64_t)s * u.cap + a); });
+  const bool kp = epilogue_core<V>(l, lane, acc, s4, wo, we, u, k, t);
+  if (lane == 0) u.keep[a] = kp ? 1 : 0;
+}
+
+// K4 for many rows after launch_update with compact = 0: one 1024-thread block scans the list
+// (k_compact's arithmetic) and ends the iteration like the update's last block would.
+__global__ void __launch_bounds__(1024) k_compact_iter(UpdateArgs u) {
+  const int t = u.ctl->t;
+  const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
+  __syncthreads();   // every thread read cnt_in (may alias cnt_out) before thread 0 writes it
+  const int2 r = compact_block(u.act_in, u.keep, u.pr.fine, L_in, u.act_out);
+  if (u.copy_back) {
+    int* dst = const_cast<int*>(u.act_in);
+    for (int j = threadIdx.x; j < r.x; j += blockDim.x) dst[j] = u.act_out[j];
+  }
+  if (threadIdx.x == 0) finish_iteration(u, r, L_in, t);
 }
 
 __global__ void k_ctl_set(IterCtl* ctl, int t, int k) {
@@ -600,6 +642,19 @@ int update_blocks(int L_ub, int NP) {
 int launch_update(cudaStream_t st, const UpdateArgs& u, int NP) {
   if (u.L_ub <= 0) return 0;
   const int NG = (NP + 31) / 32;
+  if (!u.compact) {   // many rows: warp per row (k_compact_iter compacts)
+    const unsigned nbr = (unsigned)ceil_div((int64_t)u.L_ub * 32, 256);
+    const bool f = u.G.f32;
+    if (NG <= 1)
+      f ? k_update_rows<1, true><<<nbr, 256, 0, st>>>(u) : k_update_rows<1, false><<<nbr, 256, 0, st>>>(u);
+    else if (NG <= 2)
+      f ? k_update_rows<2, true><<<nbr, 256, 0, st>>>(u) : k_update_rows<2, false><<<nbr, 256, 0, st>>>(u);
+    else if (NG <= 4)
+      f ? k_update_rows<4, true><<<nbr, 256, 0, st>>>(u) : k_update_rows<4, false><<<nbr, 256, 0, st>>>(u);
+    else
+      f ? k_update_rows<8, true><<<nbr, 256, 0, st>>>(u) : k_update_rows<8, false><<<nbr, 256, 0, st>>>(u);
+    return 1;
+  }
   const unsigned nb = (unsigned)update_blocks(u.L_ub, NP);
   // fp32 slot partials (tensor-core step, split parts possible) or fp64 (FP32 step, reduced sums)
   const bool f32 = u.G.f32;
@@ -622,6 +677,12 @@ int launch_update(cudaStream_t st, const UpdateArgs& u, int NP) {
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the update");
   }
 #undef OICA_UPD
+  return 1;
+}
+
+int launch_compact_iter(cudaStream_t st, const UpdateArgs& u) {
+  if (u.L_ub <= 0) return 0;
+  k_compact_iter<<<1, 1024, 0, st>>>(u);
   return 1;
 }
 

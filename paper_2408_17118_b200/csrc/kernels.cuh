@@ -130,8 +130,16 @@ struct UpdateArgs {
   // "runs remain active and t <= K_loop" (loop = 0 outside a graph)
   cudaGraphConditionalHandle loop;
   int K_loop;
+  // 0: no compaction here (many rows: the caller launches k_compact, whose 1024 threads scan the
+  // list faster than one block of the update could); keep[] and the row state are written
+  int compact;
 };
+// launch_update compacts inside (last block) up to this many upper-bound rows; above, one warp per
+// row updates (the HBM-bound regime) and launch_compact_iter compacts
+constexpr int kUpdateCompactRows = 2048;
 int launch_update(cudaStream_t st, const UpdateArgs& u, int NP);
+// after launch_update with compact = 0: the compaction and the end of the iteration
+int launch_compact_iter(cudaStream_t st, const UpdateArgs& u);
 // grid-size upper bound of launch_update for L_ub rows (blocks)
 int update_blocks(int L_ub, int NP);
 // ctl <- {t, k, 0} (component start; t = 1)

@@ -570,7 +570,16 @@ UpdateArgs update_args(oica_ctx* c, SlotPartials G, const double* s4, int S, int
   u.keep = c->keep.p;
   u.pr = c->promotion();
   u.ctl = c->ctl.p;
+  u.compact = 1;
   return u;
+}
+
+// the fused update, with the compaction inside for up to kUpdateCompactRows rows, else a 1024-thread
+// compaction kernel after it (which then also ends the iteration)
+void run_update(oica_ctx* c, UpdateArgs u) {
+  u.compact = u.L_ub <= kUpdateCompactRows ? 1 : 0;
+  c->count(launch_update(c->st, u, c->vNP));
+  if (!u.compact) c->count(launch_compact_iter(c->st, u));
 }
 
 #ifdef OICA_EXPERIMENTS
@@ -1066,7 +1075,7 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
       u.state = tb.state.p;
       u.keep = tb.keep.p;
       u.pr = pr;
-      c->count(launch_update(st, u, NP));
+      run_update(c, u);
       std::swap(a_cur, a_nxt);
       check_launch();
     }
@@ -1145,7 +1154,7 @@ void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
       u.copy_back = 1;
       u.loop = h;
       u.K_loop = K;
-      launch_update(st, u, c->vNP);
+      run_update(c, u);
       check_launch();
     } catch (...) {
       cudaGraph_t junk;
@@ -1329,7 +1338,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         }
         // K3 + K4 in one launch: slot sums, eq. (5), projection, convergence, next operand rows,
         // compaction by the last block (DESIGN.md §5 "iteration")
-        c->count(launch_update(st, update_args(c, G, s4, S, cap, act, act_next, L_ub, tol, c->hist.p), c->vNP));
+        run_update(c, update_args(c, G, s4, S, cap, act, act_next, L_ub, tol, c->hist.p));
         std::swap(act, act_next);
         check_launch();
       }
