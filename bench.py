@@ -94,12 +94,41 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks, power and clock-event (throttle) reasons sampled DURING the timed region: NVML
+    every ~5 ms from a thread (plus one sample at entry and one at exit, so a region shorter than
+    the period still has a record), falling back to `nvidia-smi -lms 200`."""
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+        self.gpu, self.rows, self.proc, self.nvml, self.stop = gpu, [], None, None, None
+
+    def _nvml_sample(self):
+        m = self.nvml
+        try:
+            h = self.handle
+            self.rows.append((float(m.nvmlDeviceGetClockInfo(h, m.NVML_CLOCK_SM)),
+                              float(m.nvmlDeviceGetMaxClockInfo(h, m.NVML_CLOCK_SM)),
+                              m.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                              int(m.nvmlDeviceGetCurrentClocksEventReasons(h))))
+        except Exception:
+            pass
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self._physical_index())
+            self.stop = threading.Event()
+            self._nvml_sample()
+
+            def loop():
+                while not self.stop.wait(0.005):
+                    self._nvml_sample()
+            self.t = threading.Thread(target=loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         q = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active"
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
@@ -111,6 +140,15 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _physical_index(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[self.gpu])
+            except (ValueError, IndexError):
+                pass
+        return self.gpu
+
     def _read(self):
         for line in self.proc.stdout:
             p = [s.strip() for s in line.split(",")]
@@ -121,6 +159,14 @@ class ClockSampler:
                     pass
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self.stop.set()
+            self.t.join(timeout=1)
+            self._nvml_sample()
+            try:
+                self.nvml.nvmlShutdown()
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -138,7 +184,8 @@ class ClockSampler:
                 if r[3] & bit and bit != 0x1:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in load),
-                "power_w_max": max(r[2] for r in load), "samples": len(load), "reasons": sorted(reasons)}
+                "power_w_max": max(r[2] for r in load), "samples": len(load), "reasons": sorted(reasons),
+                "sampler": "nvml 5 ms" if self.nvml is not None else "nvidia-smi 200 ms"}
 
 
 def measured_peaks():

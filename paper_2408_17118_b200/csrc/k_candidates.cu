@@ -355,7 +355,10 @@ __device__ __forceinline__ void finish_iteration(const UpdateArgs& u, int2 r, in
     u.ctl->sum_active += L_in;
   }
   // do ... while (t < K and B != {})
-  if (u.loop) cudaGraphSetConditional(u.loop, (L_in > 0 && r.x > 0 && t + 1 <= u.K_loop) ? 1u : 0u);
+  const int t_next = L_in > 0 ? t + 1 : t;
+  const bool more = r.x > 0 && t_next <= u.K_loop;
+  if (u.loop) cudaGraphSetConditional(u.loop, (L_in > 0 && more && r.x > u.loop_thr) ? 1u : 0u);
+  if (u.loop_next) cudaGraphSetConditional(u.loop_next, more ? 1u : 0u);
 }
 
 // K3 + K4 fused (see launch_update).  Block = 16 warps = RPB rows x NG warps: the NG warps of a

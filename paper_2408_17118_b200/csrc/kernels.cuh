@@ -126,9 +126,12 @@ struct UpdateArgs {
   uint8_t* keep;
   Promotion pr;
   IterCtl* ctl;
-  // device-side loop (CUDA-graph WHILE node): the last block also sets the loop condition
-  // "runs remain active and t <= K_loop" (loop = 0 outside a graph)
+  // device-side loop (CUDA-graph WHILE nodes, one per grid-size tier): the end of the iteration
+  // sets this tier's condition "more than loop_thr runs remain and t <= K_loop" and the next
+  // tier's "runs remain and t <= K_loop" (loop / loop_next = 0: none)
   cudaGraphConditionalHandle loop;
+  cudaGraphConditionalHandle loop_next;
+  int loop_thr;
   int K_loop;
   // 0: no compaction here (many rows: the caller launches k_compact, whose 1024 threads scan the
   // list faster than one block of the update could); keep[] and the row state are written

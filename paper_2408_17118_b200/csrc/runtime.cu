@@ -1134,36 +1134,50 @@ void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
                               L_ub, K, c->precision, tol};
   if (!(c->loop.valid && c->loop.key == key)) {
     c->loop.reset();
+    // grid-size tiers: the loop over L_ub rows hands over to one sized for 2048, then 128, then 32
+    // rows once that few remain (few-row iterations: tight grids, the few-row update path)
+    std::vector<int> tiers{L_ub};
+    for (int x : {2048, 128, 32})
+      if (x < tiers.back()) tiers.push_back(x);
+    const int nt = (int)tiers.size();
     OICA_CUDA(cudaGraphCreate(&c->loop.g, 0));
-    cudaGraphConditionalHandle h;
-    OICA_CUDA(cudaGraphConditionalHandleCreate(&h, c->loop.g, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams cp{};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t wnode;
-    OICA_CUDA(cudaGraphAddNode(&wnode, c->loop.g, nullptr, 0, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    OICA_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    try {
-      const int* cnt = c->Lact_dev.p;
-      run_step(c, c->act0.p, L_ub, nc_ub, cnt, cnt, c->tc() && !c->split(), false);
-      UpdateArgs u = update_args(c, c->partials(cnt, L_ub), c->tc() ? nullptr : c->s4p.p, c->S, c->Ll, c->act0.p,
-                                 c->act1.p, L_ub, tol, c->hist.p);
-      u.copy_back = 1;
-      u.loop = h;
-      u.K_loop = K;
-      run_update(c, u);
-      check_launch();
-    } catch (...) {
-      cudaGraph_t junk;
-      cudaStreamEndCapture(st, &junk);
-      c->loop.reset();
-      throw;
+    std::vector<cudaGraphConditionalHandle> hs((size_t)nt);
+    for (int i = 0; i < nt; ++i)   // the first loop starts (do-while); the next ones when handed over
+      OICA_CUDA(cudaGraphConditionalHandleCreate(&hs[i], c->loop.g, i == 0 ? 1 : 0, cudaGraphCondAssignDefault));
+    cudaGraphNode_t prev = nullptr;
+    for (int i = 0; i < nt; ++i) {
+      cudaGraphNodeParams cp{};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = hs[i];
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t wnode;
+      OICA_CUDA(cudaGraphAddNode(&wnode, c->loop.g, prev ? &prev : nullptr, prev ? 1 : 0, &cp));
+      prev = wnode;
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      OICA_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      try {
+        const int* cnt = c->Lact_dev.p;
+        const int Lt = tiers[i];
+        run_step(c, c->act0.p, Lt, std::min(nc_ub, Lt), cnt, cnt, c->tc() && !c->split(), false);
+        UpdateArgs u = update_args(c, c->partials(cnt, Lt), c->tc() ? nullptr : c->s4p.p, c->S, c->Ll, c->act0.p,
+                                   c->act1.p, Lt, tol, c->hist.p);
+        u.copy_back = 1;
+        u.loop = hs[i];
+        u.loop_next = i + 1 < nt ? hs[i + 1] : 0;
+        u.loop_thr = i + 1 < nt ? tiers[i + 1] : 0;
+        u.K_loop = K;
+        run_update(c, u);
+        check_launch();
+      } catch (...) {
+        cudaGraph_t junk;
+        cudaStreamEndCapture(st, &junk);
+        c->loop.reset();
+        throw;
+      }
+      cudaGraph_t captured;
+      OICA_CUDA(cudaStreamEndCapture(st, &captured));
     }
-    cudaGraph_t captured;
-    OICA_CUDA(cudaStreamEndCapture(st, &captured));
     OICA_CUDA(cudaGraphInstantiate(&c->loop.x, c->loop.g, 0));
     c->loop.key = key;
     c->loop.valid = true;
