@@ -103,3 +103,141 @@ def test_lshard_selection_two_ranks_gloo():
     _, res = ordering.extract(X, cfg.L, cfg.K, cfg.tol, 1, cfg.cand_seed)
     assert out[0][1] == res[0].index and out[0][2] == res[0].cluster_size
     assert out[0][3] == pytest.approx(res[0].alpha, rel=1e-12)
+
+
+# ---- M-shard: every rank holds all runs but only its samples; per iteration the
+# fp64 partial sums sum_m y^3 x and sum_m y^4 over its samples are all-reduced, and every rank
+# applies the same epilogue to the same sums (PAPER.md:243-252 with M = the global count)
+def _mshard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = datagen.PARITY["p_ragged"].with_(L=40)
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X = Xw.astype(np.float32).astype(np.float64)
+    N, M = X.shape
+    lo, hi = M * rank // world, M * (rank + 1) // world          # the M-shard sample split
+    ln, S = oica.slot_plan(M, hi - lo)                           # the rank's slots cover its samples
+    assert (S - 1) * ln < hi - lo <= S * ln
+    Xr = X[:, lo:hi]
+    ids = np.arange(cfg.L)
+    from oracle import rng
+    Wc = rng.candidates(cfg.cand_seed, 1, ids, N)
+    Wc /= np.linalg.norm(Wc, axis=1, keepdims=True)
+    active = np.arange(cfg.L)
+    conv = np.zeros(cfg.L, dtype=bool)
+    snapshots = []
+    for t in range(1, cfg.K + 1):
+        B = Wc[active]
+        Y = B @ Xr
+        Graw = (Y ** 3) @ Xr.T                                   # this rank's samples only
+        s4 = np.sum(Y ** 4, axis=1)
+        buf = torch.from_numpy(np.concatenate([Graw, s4[:, None]], axis=1).copy())
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM)               # fp64, every rank the same bits
+        G = buf[:, :N].numpy() / M - 3.0 * B                     # eq. (5) with the GLOBAL M
+        Wn = G / np.linalg.norm(G, axis=1, keepdims=True)
+        d = ordering.convergence_distance(Wn, B)
+        c = d <= cfg.tol
+        Wc[active] = Wn
+        conv[active[c]] = True
+        active = active[~c]
+        snapshots.append(Wc.copy())
+        if active.size == 0:
+            break
+    # exact alpha at the final w: all-reduced partial sums of y^4
+    s4 = torch.from_numpy(np.sum((Wc @ Xr) ** 4, axis=1).copy())
+    dist.all_reduce(s4, op=dist.ReduceOp.SUM)
+    alpha = s4.numpy() / M - 3.0
+    e = np.nonzero(conv)[0]
+    from oracle import select
+    s = select.select(ids[e], Wc[e], alpha[e])
+    q.put((rank, int(s["id_q"]), float(s["alpha_q"]), Wc.tobytes(), len(snapshots)))
+    dist.destroy_process_group()
+
+
+def test_mshard_decomposition_two_ranks_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mshard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # identical decisions and bitwise-identical iterates on both ranks (same all-reduced sums) ...
+    assert out[0][1:] == out[1][1:]
+    # ... within tolerance of the single-process oracle (the sample sum is re-associated by rank)
+    cfg = datagen.PARITY["p_ragged"].with_(L=40)
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X = Xw.astype(np.float32).astype(np.float64)
+    W1, res = ordering.extract(X, cfg.L, cfg.K, cfg.tol, 1, cfg.cand_seed)
+    assert out[0][1] == res[0].index
+    assert out[0][2] == pytest.approx(res[0].alpha, rel=1e-10)
+    Wq = np.frombuffer(out[0][3]).reshape(cfg.L, cfg.N)[res[0].index]
+    assert 1.0 - abs(float(Wq @ res[0].w)) <= 1e-12
+
+
+# ---- reading A4 across ranks: "no run converged" is a GLOBAL decision.  With a cap
+# K at which one rank's runs all miss the test while the other rank has converged runs, the
+# rank without converged runs must contribute no record (its unconverged runs would compete only
+# if NO rank had converged runs) -- the single-process oracle's decision
+def _a4_worker(rank, world, port, K, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = datagen.PARITY["p_ragged"].with_(L=12)
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X = Xw.astype(np.float32).astype(np.float64)
+    N, L = cfg.N, cfg.L
+    lo, hi = L * rank // world, L * (rank + 1) // world
+    ids = np.arange(lo, hi)
+    W, iters, conv, deg, _, _ = ordering.run_component(X, np.zeros((0, N)), 1, cfg.cand_seed, ids, K, cfg.tol)
+    n = torch.tensor([int(conv.sum())])
+    dist.all_reduce(n, op=dist.ReduceOp.SUM)                    # the global converged count
+    elig = conv if int(n.item()) > 0 else ~deg                   # reading A4, decided globally
+    recs, rows = local_records(X, W, ids, elig, N)
+    R = [torch.zeros(MAXC, 6, dtype=torch.float64) for _ in range(world)]
+    Wl = [torch.zeros(MAXC, N, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(R, torch.from_numpy(recs))
+    dist.all_gather(Wl, torch.from_numpy(rows))
+    allr = torch.cat(R).numpy()
+    allw = torch.cat(Wl).numpy()
+    recl = [dict(upsilon=r[0], alpha=r[1], q=int(r[2]), size=int(r[3]), iters=0, valid=int(r[5])) for r in allr]
+    m = oica.merge_records(recl, allw)
+    q.put((rank, int(conv.sum()), int(allr[m["winner"]][2]), int(recs[:, 5].sum())))
+    dist.destroy_process_group()
+
+
+def test_a4_global_converged_count_two_ranks_gloo():
+    cfg = datagen.PARITY["p_ragged"].with_(L=12)
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X = Xw.astype(np.float32).astype(np.float64)
+    # a cap at which the second half of the ids has no converged run and the first half has some
+    # (at L = 12 the halves' fastest runs need 6 and 7 updates)
+    _, _, st = ordering.extract(X, cfg.L, 200, cfg.tol, 1, cfg.cand_seed, keep_candidates=True)
+    it = st[0].iters
+    h = cfg.L // 2
+    K = int(it[h:].min()) - 1
+    assert K >= 1 and (it[:h] <= K).any(), (it[:h].min(), it[h:].min())
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a4_worker, args=(r, world, port, K, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out[0][1] > 0 and out[1][1] == 0                       # rank 1 converged nothing ...
+    assert out[0][3] > 0 and out[1][3] == 0                       # ... and submits no record
+    _, res = ordering.extract(X, cfg.L, K, cfg.tol, 1, cfg.cand_seed)
+    assert not res[0].no_converged
+    assert out[0][2] == out[1][2] == res[0].index                # the single-process decision
+    assert out[0][1:3] == out[1][1:3] or out[0][2] == out[1][2]
