@@ -8,7 +8,10 @@ target is required for tcgen05) and linked into paper_2408_17118_b200/liboica.so
 of DESIGN.md §7 (modes that skip work, cluster / ring / slot / promotion overrides read from
 OICA_* environment variables).  The product library never contains them; the experiment
 library is loaded only when OICA_LIB points at it (scripts/tc_variants.py), and bench.py
-refuses to run with OICA_LIB set.
+refuses to run with OICA_LIB set.  `--debug-checks` builds liboica_dbg.so with -DOICA_DEBUG_CHECKS:
+device-side bounds checks of the active lists / compaction counts and bounded mbarrier waits in
+the tensor-core step (a lost arrival traps instead of hanging the GPU) -- run the GPU tests
+against it with OICA_LIB (scripts/gpu_debug_checks.sh; compute-sanitizer is closed on the pool).
 """
 from __future__ import annotations
 
@@ -26,6 +29,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build", "oica")
 LIB = os.path.join(HERE, "liboica.so")
 LIB_EXP = os.path.join(HERE, "liboica_exp.so")
+LIB_DBG = os.path.join(HERE, "liboica_dbg.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -51,10 +55,11 @@ def _stale(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, jobs: int = 8, verbose: bool = False, experiments: bool = False) -> str:
-    bdir = BUILD + ("_exp" if experiments else "")
-    out = LIB_EXP if experiments else LIB
-    extra = ["-DOICA_EXPERIMENTS"] if experiments else []
+def build(force: bool = False, jobs: int = 8, verbose: bool = False, experiments: bool = False,
+          debug_checks: bool = False) -> str:
+    bdir = BUILD + ("_exp" if experiments else "") + ("_dbg" if debug_checks else "")
+    out = LIB_EXP if experiments else LIB_DBG if debug_checks else LIB
+    extra = (["-DOICA_EXPERIMENTS"] if experiments else []) + (["-DOICA_DEBUG_CHECKS"] if debug_checks else [])
     os.makedirs(bdir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     cc = nvcc()
@@ -92,5 +97,7 @@ if __name__ == "__main__":
     ap.add_argument("-j", type=int, default=8)
     ap.add_argument("-v", action="store_true")
     ap.add_argument("--experiments", action="store_true", help="build liboica_exp.so with -DOICA_EXPERIMENTS")
+    ap.add_argument("--debug-checks", action="store_true",
+                    help="build liboica_dbg.so with -DOICA_DEBUG_CHECKS (device bounds checks, bounded mbarrier waits)")
     a = ap.parse_args()
-    print(build(a.force, a.j, a.v, a.experiments))
+    print(build(a.force, a.j, a.v, a.experiments, a.debug_checks))

@@ -339,6 +339,12 @@ __device__ __forceinline__ int2 compact_block(const int* __restrict__ act_in, co
 
 // End of an iteration (one thread): counts, history, iteration state, loop condition.
 __device__ __forceinline__ void finish_iteration(const UpdateArgs& u, int2 r, int L_in, int t) {
+#ifdef OICA_DEBUG_CHECKS
+  if (r.x < 0 || r.x > L_in || r.y < 0 || r.y > r.x || t < 1 || (u.K_loop > 0 && t > u.K_loop + 1)) {
+    printf("oica debug: iteration %d: compaction kept %d (coarse %d) of %d rows\n", t, r.x, r.y, L_in);
+    __trap();
+  }
+#endif
   u.cnt_out[0] = r.x;
   u.cnt_out[1] = r.y;
   if (u.host_mapped) {
@@ -386,6 +392,13 @@ __global__ void __launch_bounds__(512) k_update(UpdateArgs u) {
   double wo[NG], we[NG];
   if (row_ok) {
     l = u.act_in[a];
+#ifdef OICA_DEBUG_CHECKS
+    if (l < 0 || l >= u.cap || L_in > u.L_ub) {
+      printf("oica debug: update row %d -> candidate %d (cap %lld, L_in %d, L_ub %d)\n", a, l, (long long)u.cap,
+             L_in, u.L_ub);
+      __trap();
+    }
+#endif
     if (grp == 0) load_row<NG>(u, l, lane, wo, we);   // (in flight with the slot sums below)
     const int n = grp * 32 + lane;
     // (16 partials in flight per lane: with few active rows the slot chain is latency-bound; the

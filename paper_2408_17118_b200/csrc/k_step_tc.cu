@@ -69,6 +69,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef OICA_DEBUG_CHECKS
+// debug build (build.py --debug-checks): a bounded wait -- a phase that never completes (a lost
+// arrival, a wrong parity) traps instead of hanging the GPU; ~2^26 polls of <= 10 ms suspend hint
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  for (uint32_t polls = 0;; ++polls) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+    if (done) return;
+    if (polls > (1u << 26)) {
+      printf("oica debug: mbarrier wait timed out (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x, parity);
+      __trap();
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -80,6 +101,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(0x989680u)
       : "memory");
 }
+#endif
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -449,6 +471,12 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     {
       bool ok = row < L_act;
       const int64_t id = ok ? (int64_t)__ldg(act + row) : 0;   // operand rows are stored by candidate id
+#ifdef OICA_DEBUG_CHECKS
+      if (ok && (id < 0 || id >= cap)) {
+        printf("oica debug: step row %d -> candidate %lld outside [0, %lld)\n", row, (long long)id, (long long)cap);
+        __trap();
+      }
+#endif
       const uint32_t* wh = (const uint32_t*)(Whi + id * NP);
       const uint32_t* wl = (const uint32_t*)(Wlo + id * NP);
 #pragma unroll 1
