@@ -11,7 +11,7 @@ library is loaded only when OICA_LIB points at it (scripts/tc_variants.py), and 
 refuses to run with OICA_LIB set.  `--debug-checks` builds liboica_dbg.so with -DOICA_DEBUG_CHECKS:
 device-side bounds checks of the active lists / compaction counts and bounded mbarrier waits in
 the tensor-core step (a lost arrival traps instead of hanging the GPU) -- run the GPU tests
-against it with OICA_LIB (scripts/gpu_debug_checks.sh; compute-sanitizer is closed on the pool).
+against it with OICA_LIB (scripts/gpu_jobs.sh debug-checks; compute-sanitizer is closed on the pool).
 """
 from __future__ import annotations
 

@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """Time k_step_tc variants (dev experiment): python scripts/tc_variants.py <mode> [N]
-Runs oica_fixed_point_step on random data at the cfg4/cfg3 shapes; prints algorithmic TFLOP/s."""
+Runs oica_fixed_point_step on random data at the cfg4/cfg3 shapes; prints algorithmic TFLOP/s.
+The variants (OICA_TC_EPI, OICA_TC_CL, OICA_TC_RING, ...) exist only in the experiment build:
+python -m paper_2408_17118_b200.build --experiments, then OICA_LIB=.../liboica_exp.so."""
 import json
 import os
 import sys
