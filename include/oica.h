@@ -110,6 +110,8 @@ typedef struct {
   int32_t stopped;        /* 1 if the Gaussianity test ended extraction   */
   int32_t* dim;           /* dimension the component's iteration ran in: N, or N-i+1 with   */
                           /* OICA_REDUCE_X (algorithmic work = sum_active (4 dim M + 3 M))   */
+  double* objective;      /* sum_m y^4 / M at the accepted w (the quantity alpha + 3 of eq. (2), */
+                          /* the north_star's objective), from the exact fp64 pass            */
 } oica_result;
 
 /* Flags for oica_extract_components. */
@@ -279,14 +281,8 @@ typedef struct {
   int64_t size;
   int32_t iters;
   int32_t valid;          /* 0 = empty slot */
+  double objective;       /* sum y^4 / M of member q (alpha + 3)                             */
 } oica_cluster_record;
-
-/* Merge n records (from all ranks, records[k].w = w + k*N) into the global decision of
- * reading A6: records whose rows satisfy 1 - |w_a . w_b| <= 1e-6 are one cluster (sizes add,
- * q = minimum id, its record supplies alpha/upsilon/iters/w); the winner is the cluster of
- * largest upsilon (ties -> lowest q); near_tie if the runner-up is within 1e-6 relative.
- * Host pointers; pure function.  Writes the winner index into `records` (*winner) and the
- * merged size / near-tie flag. */
 /* Host-only helpers of OICA_REDUCE_X (pure functions, no device).  oica_complement_basis: W is
  * k x N with orthonormal rows (k < N); writes G, (N-k) x N, rows orthonormal and orthogonal to
  * every row of W (the last N-k columns of Q in the Householder QR of W^T).  oica_deflate_basis:
@@ -307,6 +303,12 @@ oica_status oica_slot_plan(int32_t precision, int64_t M_global, int64_t M_local,
 oica_status oica_split_parts(int32_t L_global, int32_t S, int32_t* P);
 oica_status oica_deflate_basis(double* G, int32_t d, int32_t N, const double* b, double* G_out);
 
+/* Merge n records (from all ranks, records[k].w = w + k*N) into the global decision of
+ * reading A6: records whose rows satisfy 1 - |w_a . w_b| <= 1e-6 are one cluster (sizes add,
+ * q = minimum id, its record supplies alpha/upsilon/iters/w); the winner is the cluster of
+ * largest upsilon (ties -> lowest q); near_tie if the runner-up is within 1e-6 relative.
+ * Host pointers; pure function (the device accept kernel runs the same source).  Writes the
+ * winner's index into `records` to *winner and the merged size / near-tie flag. */
 oica_status oica_merge_records(const oica_cluster_record* records, const double* w, int32_t n,
                                int32_t N, int32_t* winner, int64_t* merged_size,
                                uint8_t* near_tie);

@@ -351,8 +351,10 @@ __global__ void k_finish(const double* __restrict__ W64, const int* __restrict__
     int r = raw ? pc[c] : (pc[c] >= 0 ? qc[c] : -1);
     oica_cluster_record rec{};
     if (r >= 0) {
-      double a = s4c[c] / M - 3.0;                      // eq. (2) at the final w
+      const double obj = s4c[c] / M;                    // sum y^4 / M at the final w
+      double a = obj - 3.0;                             // eq. (2)
       rec.alpha = a;
+      rec.objective = obj;
       rec.upsilon = upsilon_of(a);                      // eq. (1)
       rec.q = id_base + r;
       rec.size = raw ? 1 : csize[c];
@@ -410,6 +412,7 @@ __global__ void k_merge_accept(const RankSummary* __restrict__ all, const double
   }
   r.w_alpha = win.alpha;
   r.w_upsilon = win.upsilon;
+  r.w_objective = win.objective;
   r.q = win.q;
   r.iters = win.iters;
   r.cluster_size = m.merged_size;

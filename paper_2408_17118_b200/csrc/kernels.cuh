@@ -177,7 +177,7 @@ int launch_tail_scatter(cudaStream_t st, int T, const int64_t* ids, const double
 // ---- K5: device-side argmax, cluster assignment, exact alpha, merge + accept
 struct SelectWork;  // defined in k_select.cu
 struct ComponentRecord {
-  double w_alpha, w_upsilon;
+  double w_alpha, w_upsilon, w_objective;
   int64_t q, cluster_size, n_conv, n_unconv, n_deg, sum_active, n_nonfinite;
   int32_t iters, n_iter, status, gaussian, near_tie, n_domain;
 };

@@ -1506,6 +1506,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     bool stop = (flags & OICA_STOP_ON_GAUSSIANITY) && rec_h.gaussian;
     if (out->W && !stop) std::memcpy(out->W + (size_t)k * N, w_host.data(), sizeof(double) * N);
     if (out->alpha) out->alpha[k] = rec_h.w_alpha;
+    if (out->objective) out->objective[k] = rec_h.w_objective;
     if (out->upsilon) out->upsilon[k] = rec_h.w_upsilon;
     if (out->index) out->index[k] = rec_h.q;
     if (out->iters) out->iters[k] = rec_h.iters;

@@ -54,7 +54,7 @@ class Result(C.Structure):
                 ("cluster_size", _P(C.c_int32)), ("n_converged", _P(C.c_int32)), ("n_unconverged", _P(C.c_int32)),
                 ("n_degenerate", _P(C.c_int32)), ("sum_active", _P(C.c_int64)), ("gaussian_flag", _P(C.c_uint8)),
                 ("near_tie", _P(C.c_uint8)), ("n_extracted", C.c_int32), ("stopped", C.c_int32),
-                ("dim", _P(C.c_int32))]
+                ("dim", _P(C.c_int32)), ("objective", _P(C.c_double))]
 
 
 class Stats(C.Structure):
@@ -73,7 +73,7 @@ class IterationRecord(C.Structure):
 
 class ClusterRecord(C.Structure):
     _fields_ = [("upsilon", C.c_double), ("alpha", C.c_double), ("q", C.c_int64), ("size", C.c_int64),
-                ("iters", C.c_int32), ("valid", C.c_int32)]
+                ("iters", C.c_int32), ("valid", C.c_int32), ("objective", C.c_double)]
 
 
 # every symbol include/oica.h declares (checked by tests/test_abi.py)
@@ -172,7 +172,8 @@ def merge_records(records, W):
     n = len(records)
     arr = (ClusterRecord * max(n, 1))()
     for k, r in enumerate(records):
-        arr[k] = ClusterRecord(r["upsilon"], r["alpha"], r["q"], r["size"], r.get("iters", 0), r.get("valid", 1))
+        arr[k] = ClusterRecord(r["upsilon"], r["alpha"], r["q"], r["size"], r.get("iters", 0), r.get("valid", 1),
+                               r.get("objective", r["alpha"] + 3.0))
     W = np.ascontiguousarray(W, dtype=np.float64)
     win, size, tie = C.c_int32(-1), C.c_int64(0), C.c_uint8(0)
     st = lib().oica_merge_records(arr, _np_ptr(W, C.c_double), n, W.shape[1] if W.ndim == 2 else 1,
@@ -232,10 +233,7 @@ class Extraction:
     n_extracted: int
     stopped: bool
     dim: np.ndarray = None
-
-    @property
-    def objective(self):
-        return self.alpha + 3.0
+    objective: np.ndarray = None   # sum y^4 / M at the accepted w (oica_result.objective)
 
 
 class Context:
@@ -330,13 +328,13 @@ class Context:
                  n_converged=np.zeros(N_out, np.int32), n_unconverged=np.zeros(N_out, np.int32),
                  n_degenerate=np.zeros(N_out, np.int32), sum_active=np.zeros(N_out, np.int64),
                  gaussian_flag=np.zeros(N_out, np.uint8), near_tie=np.zeros(N_out, np.uint8),
-                 dim=np.zeros(N_out, np.int32))
+                 dim=np.zeros(N_out, np.int32), objective=np.zeros(N_out))
         if Wp is not None:
             a["W"][:k] = Wp
         ct = dict(W=C.c_double, alpha=C.c_double, upsilon=C.c_double, index=C.c_int64, iters=C.c_int32,
                   n_iter=C.c_int32, cluster_size=C.c_int32, n_converged=C.c_int32, n_unconverged=C.c_int32,
                   n_degenerate=C.c_int32, sum_active=C.c_int64, gaussian_flag=C.c_uint8, near_tie=C.c_uint8,
-                  dim=C.c_int32)
+                  dim=C.c_int32, objective=C.c_double)
         res = Result(**{f: _np_ptr(a[f], ct[f]) for f in ct}, n_extracted=0, stopped=0)
         self._c(lib().oica_extract_components(self.h, N_out, max_iter, tol, flags,
                                               _np_ptr(Wp, C.c_double), k, C.byref(res)))

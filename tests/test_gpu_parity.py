@@ -223,6 +223,10 @@ def test_extract_parity(name, precision):
     W_or, res_or, st_or = oracle_run(name)
     rep = _compare(res, res_or, W_or, X64, st_or)
     assert np.abs(res.W @ res.W.T - np.eye(cfg.N_out)).max() < 1e-10
+    # the ABI's objective output (sum y^4 / M, exact fp64 pass) against the oracle's
+    obj_o = np.array([r.alpha + 3.0 for r in res_or])
+    assert np.all(np.abs(res.objective - obj_o) <= 1e-4 * obj_o)
+    assert np.allclose(res.objective, res.alpha + 3.0, rtol=1e-14, atol=0)
     # convergence census: every run converges in both arithmetics on these workloads (K = 200 is
     # far above the iteration counts), so the counts agree up to runs whose step distance sits at
     # d ~ tol in the last iterations; 2% of L (reading A28)
