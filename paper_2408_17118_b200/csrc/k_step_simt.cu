@@ -8,14 +8,12 @@
 // adding the partial into its private fp64 slot (no atomics: bitwise deterministic, and the
 // result for a row does not depend on which other rows share its tile).
 #include "kernels.cuh"
+#include "simt_unit.cuh"
 
 namespace oica {
 namespace {
 
-constexpr int R = 64;        // rows per CTA
-constexpr int MC = 64;       // samples per chunk
-constexpr int XS = MC + 1;   // padded X row stride (conflict-free column reads)
-constexpr int YS = R + 1;    // padded Y^3 row stride
+using namespace simt;
 
 template <int NP>
 __global__ void __launch_bounds__(256, 1)
@@ -25,127 +23,14 @@ k_step_simt(const float* __restrict__ X, int64_t ld, int64_t M, int N, const flo
             const int* __restrict__ cnt) {
   const int L_act = cnt ? min(L_ub, cnt[0]) : L_ub;   // device count when the grid is an upper bound
   if ((int)(blockIdx.x * R) >= L_act) return;
-  constexpr int TN = NP / 32;
   extern __shared__ float smem[];
-  float* WT = smem;                 // [NP][R]   W tile, transposed
-  float* Xs = WT + NP * R;          // [NP][XS]  X chunk
-  float* Y3 = Xs + NP * XS;         // [MC][YS]  y^3 chunk
-  float* S4 = Y3 + MC * YS;         // [16][R]   s4 partials for the fixed-order reduction
-
-  const int tid = threadIdx.x;
-  const int row0 = blockIdx.x * R;
-  const int s = blockIdx.y;
-  const int64_t m_begin = (int64_t)s * slot_len;
-  const int64_t m_end = min(M, m_begin + slot_len);
-
-  for (int idx = tid; idx < R * NP; idx += 256) {
-    int r = idx / NP, n = idx % NP;
-    WT[n * R + r] = (row0 + r < L_act) ? W32[(int64_t)act[row0 + r] * NP + n] : 0.f;   // operand row by id
-  }
-
-  const int rg = tid >> 4, cg = tid & 15;     // phase 1: rows rg*4+i, cols cg+16j
-  const int rg2 = tid >> 5, ng = tid & 31;    // phase 2: rows rg2*8+i, n = ng+32k
-  float acc[8][TN];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int k = 0; k < TN; ++k) acc[i][k] = 0.f;
-  float s4a[4] = {0.f, 0.f, 0.f, 0.f};
-  bool first = true;
-  int since = 0;
-
-  for (int64_t m0 = m_begin; m0 < m_end; m0 += MC) {
-    __syncthreads();
-    for (int idx = tid; idx < NP * MC; idx += 256) {
-      int n = idx / MC, j = idx % MC;
-      int64_t m = m0 + j;
-      Xs[n * XS + j] = (n < N && m < m_end) ? __ldg(X + (int64_t)n * ld + m) : 0.f;
-    }
-    __syncthreads();
-    // phase 1: y = W x (fixed n order per output)
-    float y[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) y[i][j] = 0.f;
-#pragma unroll 4
-    for (int n = 0; n < NP; ++n) {
-      float4 w4 = *reinterpret_cast<const float4*>(&WT[n * R + rg * 4]);
-      float xv[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) xv[j] = Xs[n * XS + cg + 16 * j];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        y[0][j] = fmaf(w4.x, xv[j], y[0][j]);
-        y[1][j] = fmaf(w4.y, xv[j], y[1][j]);
-        y[2][j] = fmaf(w4.z, xv[j], y[2][j]);
-        y[3][j] = fmaf(w4.w, xv[j], y[3][j]);
-      }
-    }
-    // cube and fourth power (eq. (2))
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float y2 = y[i][j] * y[i][j];
-        s4a[i] = fmaf(y2, y2, s4a[i]);
-        Y3[(cg + 16 * j) * YS + rg * 4 + i] = y2 * y[i][j];
-      }
-    __syncthreads();
-    // phase 2: G += y^3 x^T (fixed m order per output)
-#pragma unroll 2
-    for (int j = 0; j < MC; ++j) {
-      float a[8], xv[TN];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = Y3[j * YS + rg2 * 8 + i];
-#pragma unroll
-      for (int k = 0; k < TN; ++k) xv[k] = Xs[(ng + 32 * k) * XS + j];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int k = 0; k < TN; ++k) acc[i][k] = fmaf(a[i], xv[k], acc[i][k]);
-    }
-    since += MC;
-    if (since >= flush || m0 + MC >= m_end) {
-      // flush fp32 partials into this CTA's private fp64 slot, fixed order
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        int a = row0 + rg2 * 8 + i;
-        if (a < L_act) {
-#pragma unroll
-          for (int k = 0; k < TN; ++k) {
-            int n = ng + 32 * k;
-            if (n < N) {
-              double* p = Gp + ((int64_t)s * cap + a) * NP + n;
-              *p = (first ? 0.0 : *p) + (double)acc[i][k];
-            }
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < TN; ++k) acc[i][k] = 0.f;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        S4[cg * R + rg * 4 + i] = s4a[i];
-        s4a[i] = 0.f;
-      }
-      __syncthreads();
-      if (tid < R && row0 + tid < L_act) {
-        double v = 0.0;
-        for (int c = 0; c < 16; ++c) v += (double)S4[c * R + tid];
-        double* p = s4p + (int64_t)s * cap + row0 + tid;
-        *p = (first ? 0.0 : *p) + v;
-      }
-      first = false;
-      since = 0;
-    }
-  }
+  simt_step_unit<NP>(X, ld, M, N, W32, act, L_act, slot_len, flush, Gp, s4p, cap, blockIdx.x, blockIdx.y, smem);
 }
 
 template <int NP>
 void launch_np(cudaStream_t st, const float* X, int64_t ld, int64_t M, int N, const float* W32, const int* act, int L_act,
                int64_t slot_len, int S, int flush, double* Gp, double* s4p, int64_t cap, const int* cnt) {
-  size_t smem = sizeof(float) * ((size_t)NP * R + (size_t)NP * XS + (size_t)MC * YS + 16 * R);
+  const size_t smem = unit_smem_bytes<NP>();
   static bool attr = false;
   if (!attr) {
     OICA_CUDA(cudaFuncSetAttribute(k_step_simt<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

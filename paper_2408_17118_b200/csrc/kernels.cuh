@@ -145,6 +145,12 @@ int launch_update(cudaStream_t st, const UpdateArgs& u, int NP);
 int launch_compact_iter(cudaStream_t st, const UpdateArgs& u);
 // grid-size upper bound of launch_update for L_ub rows (blocks)
 int update_blocks(int L_ub, int NP);
+// The whole do-while of one component for the FP32 step at tiny sizes, as ONE cooperative launch
+// (k_loop_simt.cu): step units, update, compaction per iteration with grid barriers, until no run
+// is active or t > K.  u: the update arguments (G = the fp64 slot partials, act_in = the active list
+// kept in place, act_out = scratch, ctl, hist, ...).  NP = 32 or 64.
+int launch_loop_simt(cudaStream_t st, const float* X, int64_t ld, int64_t M, int64_t slot_len, int S, int flush,
+                     int K, const UpdateArgs& u, int NP, int num_sms);
 // ctl <- {t, k, 0} (component start; t = 1)
 int launch_ctl_set(cudaStream_t st, IterCtl* ctl, int t, int k);
 

@@ -178,6 +178,7 @@ struct oica_ctx {
     }
   } loop;
   cudaEvent_t loop_ev0 = nullptr, loop_ev1 = nullptr;
+  bool loop_persistent = false;   // the last device-side loop was the persistent FP32 kernel
   // pinned read-back of a component's results (one host wait per component on the fast path):
   // [ComponentRecord | IterCtl | w (256 doubles) | hist (2 (K + 1) ints)]
   char* pin = nullptr;
@@ -448,7 +449,9 @@ void plan_slots_for(int64_t M_global, int64_t M_local, bool fp32, int64_t* slot_
   if (fp32 && M_global < kSimtShortM) {
     // FP32 step at small M (the paper's own experiments, M = 1e4): one CTA per (64-row tile, slot)
     // streams its slot chunk by chunk, so short slots (>= 128 samples, up to 128 of them, 64-aligned
-    // = the FP32 chunk) give the few row tiles enough CTAs: a 1e4-sample step 23 -> ~6 us
+    // = the FP32 chunk) give the few row tiles enough CTAs: a 1e4-sample step 23 -> 12 us.  (One
+    // 64-sample chunk per slot, up to 256 slots, measured slower: a unit's fixed latencies dominate
+    // and the update then sums twice the partials.)
     const int64_t S = std::max<int64_t>(1, std::min<int64_t>(kMaxSlots, ceil_div(M_global, 128)));
     *slot_len = round_up(ceil_div(M_global, S), 64);
     *S_local = std::max(1, (int)ceil_div(M_local, *slot_len));
@@ -1130,6 +1133,7 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
 // (tests/test_gpu_parity.py::test_device_loop_bitwise).  Enqueues only (no host wait).
 void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
   cudaStream_t st = c->st;
+  c->loop_persistent = false;
   const oica_ctx::LoopKey key{c->vX, c->vXh, c->M, c->Mg, c->slot_len, c->ldx, c->vld, c->vN, c->vNP, c->S,
                               L_ub, K, c->precision, tol};
   if (!(c->loop.valid && c->loop.key == key)) {
@@ -1196,8 +1200,36 @@ void finish_loop_graph(oica_ctx* c, int iters) {
   float ms = 0.f;
   OICA_CUDA(cudaEventElapsedTime(&ms, c->loop_ev0, c->loop_ev1));
   c->stats.graph_ms += ms;
-  c->count(2 * std::max(iters, 1));
-  c->stats.step_launches += std::max(iters, 1);
+  if (c->loop_persistent) {
+    c->count(1);
+    c->stats.step_launches += 1;
+  } else {
+    c->count(2 * std::max(iters, 1));
+    c->stats.step_launches += std::max(iters, 1);
+  }
+}
+
+// Tiny FP32 problems (the paper's own experiment sizes): the persistent cooperative loop
+constexpr int64_t kPersistentMaxRows = 512;
+bool persistent_loop_ok(const oica_ctx* c) {
+  return !c->tc() && !c->reduced && c->Ll <= kPersistentMaxRows && c->M < kSimtShortM &&
+         (c->vNP == 32 || c->vNP == 64);
+}
+
+void enqueue_loop_simt(oica_ctx* c, int K, double tol) {
+  cudaStream_t st = c->st;
+  if (!c->loop_ev0) {
+    OICA_CUDA(cudaEventCreate(&c->loop_ev0));
+    OICA_CUDA(cudaEventCreate(&c->loop_ev1));
+  }
+  UpdateArgs u = update_args(c, SlotPartials{c->Gp.p, false}, c->s4p.p, c->S, c->Ll, c->act0.p, c->act1.p, (int)c->Ll,
+                             tol, c->hist.p);
+  u.copy_back = 1;
+  OICA_CUDA(cudaEventRecord(c->loop_ev0, st));
+  launch_loop_simt(st, c->vX, c->vld, c->M, c->slot_len, c->S, kFlush, K, u, c->vNP, c->num_sms);
+  check_launch();
+  OICA_CUDA(cudaEventRecord(c->loop_ev1, st));
+  c->loop_persistent = true;
 }
 
 void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t flags, const double* W_prefix,
@@ -1313,9 +1345,12 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     };
     if (lockstep) OICA_CUDA(cudaMemsetAsync(c->hist.p, 0, sizeof(int) * 2 * ((size_t)K + 1), st));
     bool to_tail = lockstep && refresh();
-    if (fast) {   // the whole do-while on the device (one graph launch)
+    if (fast) {   // the whole do-while on the device
       sync_x(c);   // (a pipelined upload is waited for: the graph is captured on the context stream)
-      enqueue_loop_graph(c, L_ub, nc_ub, K, tol);
+      if (persistent_loop_ok(c))
+        enqueue_loop_simt(c, K, tol);      // tiny FP32 problems: one cooperative launch
+      else
+        enqueue_loop_graph(c, L_ub, nc_ub, K, tol);   // one graph launch
     }
     while (!fast && !to_tail && (lockstep ? G_ub : L_ub) > 0 && t < K) {
       // batches only where an iteration is short next to a host round trip (one row tile over

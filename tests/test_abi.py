@@ -139,10 +139,12 @@ def test_slot_plan_host(M):
     for prec in (oica.PREC_TC, oica.PREC_FP32, oica.PREC_AUTO):
         ln, S = oica.slot_plan(M, precision=prec)
         fp32 = prec == oica.PREC_FP32 or (prec == oica.PREC_AUTO and M < 16384)
-        align = 64 if fp32 and M < 65536 else 384
+        short = fp32 and M < 65536
+        align = 64 if short else 384
         assert ln % align == 0 and 1 <= S <= 128 and (S - 1) * ln < M <= S * ln, (prec, ln, S)
-        if fp32 and M < 65536:
-            assert ln >= min(128, 64 * -(-M // 64)) and (S == 128 or ln <= 192)   # short slots: many CTAs
+        if short:   # slots of >= 128 samples, up to 128 of them: many CTAs for few row tiles
+            n_s = min(128, -(-M // 128))
+            assert ln == 64 * -(-(-(-M // n_s)) // 64), (M, ln)
         for world in (2, 8):
             ml = -(-M // world)
             ln2, S2 = oica.slot_plan(M, min(ml, M), precision=prec)
