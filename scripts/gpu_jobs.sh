@@ -8,6 +8,8 @@
 #   bash scripts/gpu_jobs.sh bench-all                bench lines of cfgs 0-3 (steps, all components, eager)
 #   bash scripts/gpu_jobs.sh parity                   golden + tier-C parity with the printed worst cases
 #   bash scripts/gpu_jobs.sh debug-checks             parity suite against liboica_dbg.so (bounds checks)
+#   bash scripts/gpu_jobs.sh ncu-step CFG...          ncu --set full of one full-L step launch per config
+#                                                     (summaries + raw csv; the roofline `traffic` source)
 set -u
 mkdir -p gpurun_out
 job=${1:-tests}
@@ -85,6 +87,17 @@ debug-checks)
   OICA_LIB=$PWD/paper_2408_17118_b200/liboica_dbg.so timeout 600 python scripts/sanitize_run.py \
     >> gpurun_out/debug_checks.log 2>&1
   echo "sanitize_run rc=$?"; tail -3 gpurun_out/debug_checks.log
+  ;;
+ncu-step)
+  ncu --query-metrics 2>/dev/null | grep -i -E "tmem|tensor_mem|utc|pipe_tensor" > gpurun_out/ncu_tensor_metric_names.txt
+  for CFG in "${@:-cfg4_scaling}"; do
+    CMD="python bench.py --config $CFG --steps 1 --warmup 3 --no-e2e --no-all --no-cpu-baseline --data device --eager"
+    timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:k_step_tc -s 2 -c 1 \
+      -o /tmp/prof_step_$CFG $CMD > gpurun_out/ncu_full_$CFG.log 2>&1; echo "full_$CFG rc=$?"
+    python scripts/ncu_summary.py full /tmp/prof_step_$CFG.ncu-rep > gpurun_out/ncu_full_${CFG}.json 2>&1
+    ncu -i /tmp/prof_step_$CFG.ncu-rep --page raw --csv > gpurun_out/ncu_raw_${CFG}.csv 2>/dev/null
+    ncu -i /tmp/prof_step_$CFG.ncu-rep --page details --csv > gpurun_out/ncu_details_${CFG}.csv 2>/dev/null
+  done
   ;;
 *)
   echo "unknown job $job"; exit 2

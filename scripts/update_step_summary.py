@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Refresh profiles/<round>/ncu_step_summary.json (the roofline `traffic` bench.py reports) from the
-`ncu --set full` summaries scripts/gpu_final.sh writes (ncu_full_<cfg>_final.json).
+`ncu --set full` summaries `scripts/gpu_jobs.sh ncu-step` writes (ncu_full_<cfg>.json; round 1:
+ncu_full_<cfg>_final.json).
 
-    python scripts/update_step_summary.py profiles/r01/final profiles/r01/ncu_step_summary.json
+    python scripts/update_step_summary.py profiles/r02/ncu profiles/r02/ncu_step_summary.json
 """
 import json
 import os
@@ -27,8 +28,10 @@ def main():
     import datagen
     src, dst = sys.argv[1], sys.argv[2]
     out = json.load(open(dst)) if os.path.exists(dst) else {}
-    for cfg_name in ("cfg4_scaling", "cfg3_large"):
-        p = os.path.join(src, f"ncu_full_{cfg_name}_final.json")
+    for cfg_name in ("cfg4_scaling", "cfg3_large", "cfg2_eeg_shaped"):
+        p = os.path.join(src, f"ncu_full_{cfg_name}.json")
+        if not os.path.exists(p):
+            p = os.path.join(src, f"ncu_full_{cfg_name}_final.json")
         if not os.path.exists(p):
             continue
         d = json.load(open(p))[0]
@@ -43,7 +46,7 @@ def main():
             "dram_bytes_per_launch": rd + wr,
             "dram_read": rd,
             "dram_write": wr,
-            "launch": f"third step launch of bench.py --steps 1 --warmup 3 (component 1, full L), grid {grid} CTAs",
+            "launch": f"third step launch of bench.py --steps 1 --warmup 3 --eager (component 1, full L), grid {grid} CTAs",
             "duration_ms_under_ncu": value(d["gpu__time_duration.sum"]),
             "algorithmic_bytes_per_launch": 2 * cfg.N * cfg.M + 2 * cfg.L * NP + 4 * S * cfg.L * NP,
             "algorithmic_bytes_note": f"X fp16 once (2 N M) + fp16 operand rows in (2 L NP) + fp32 slot partials out "
@@ -51,6 +54,8 @@ def main():
             "source": p,
             "tensor_pipe_active_pct": value(
                 d["TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"]),
+            "tensor_memory_active_pct": value(d["sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"])
+            if "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed" in d else None,
         }
     json.dump(out, open(dst, "w"), indent=1)
     print(json.dumps(out, indent=1))
