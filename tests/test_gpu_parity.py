@@ -508,6 +508,34 @@ def test_exchange_paths_single_rank(name, precision, shard):
         assert np.array_equal(plain.W, res.W) and np.array_equal(plain.index, res.index)
 
 
+@pytest.mark.parametrize("shard", [oica.SHARD_L, oica.SHARD_M])
+def test_distribute_data_single_rank(shard):
+    """oica_distribute_data (C3) over a one-rank communicator: the broadcast path (contiguous, and one
+    broadcast per row into a strided buffer) and the M-shard path deliver root's data bitwise; the
+    distributed data then extracts like the original."""
+    cfg, X32, _ = prepared("p_n40")
+    Xr = torch.from_numpy(X32).cuda()
+    with oica.Context(0, oica.PREC_AUTO, rank=0, world=1, shard_mode=shard, nccl_id=oica.nccl_unique_id()) as ctx:
+        out = torch.zeros_like(Xr)
+        ctx.distribute_data(Xr, cfg.N, cfg.M, out)
+        assert torch.equal(out, Xr)
+        wide = torch.zeros(cfg.N, cfg.M + 40, device="cuda")
+        ctx.distribute_data(Xr, cfg.N, cfg.M, wide[:, : cfg.M])
+        assert torch.equal(wide[:, : cfg.M], Xr) and not wide[:, cfg.M:].any()
+        ctx.set_data(out, M_global=cfg.M)
+        ctx.init_candidates(cfg.cand_seed, cfg.L)
+        a = ctx.extract(2, cfg.K, cfg.tol)
+        assert ctx.stats()["exchange_calls"] >= 1
+    with oica.Context(0, oica.PREC_AUTO) as ctx:   # no communicator: a device copy
+        out2 = torch.zeros_like(Xr)
+        ctx.distribute_data(Xr, cfg.N, cfg.M, out2)
+        assert torch.equal(out2, Xr)
+        ctx.set_data(Xr)
+        ctx.init_candidates(cfg.cand_seed, cfg.L)
+        b = ctx.extract(2, cfg.K, cfg.tol)
+    assert np.array_equal(a.index, b.index) and np.allclose(a.W, b.W, atol=1e-12)
+
+
 def test_hybrid_tail_from_first_iteration(tmp_path):
     """OICA_SHARD_HYBRID with OICA_HYBRID_ROWS above L: every iteration runs in the gathered,
     M-sharded tail (several row tiles, tail slot plan, per-iteration all-reduce over a one-rank
