@@ -24,6 +24,9 @@
  *   - CUDA / NCCL failures return OICA_ERR_CUDA / OICA_ERR_NCCL and leave the context
  *     usable only for oica_destroy.
  *   - A context is single-threaded: one context per device and rank.
+ *   - The library works on the context's stream (cfg->stream, or its own non-blocking stream)
+ *     and does not order itself after other streams: device inputs must be complete when a
+ *     call is made (the Python binding synchronizes torch's current stream before passing one).
  *   - With world > 1 every call that computes is COLLECTIVE: all ranks call it with
  *     identical scalar arguments.
  */

@@ -94,11 +94,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@P1 bra DONE;\n\t"
       "bra LAB_WAIT;\n\t"
       "DONE:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)
+      "r"(parity)
       : "memory");
 }
 #endif
@@ -230,6 +230,10 @@ struct Cfg {
   // RG = 3 (NP <= 64): 2 slots of 192 samples -- more tensor work per chunk hand-off where the
   // narrow MMAs are short (the hand-offs, not the MMAs, pace small NP)
   static constexpr int MT = WIDE ? 64 : RG == 1 ? 128 : RG == 3 ? 192 : 64;   // samples per chunk (GEMM1 N)
+  // epilogue warps (one per TMEM lane quadrant; the kernel also runs with two per quadrant, each
+  // taking every other 32-column group)
+  static constexpr int NW = 4;   // (8 for the small-NP layout measured no faster: cfg 2 step 875 vs 881 TFLOP/s)
+  static constexpr int THREADS = 64 + 32 * NW;
   static constexpr int R = (!WIDE && RG == 0) ? 4 : 2;           // Y slots in TMEM (GEMM1 look-ahead R-1)
   static constexpr int XB = NP * 128;                            // bytes of one [NP][64] swizzled box
   static constexpr int X_STAGE = NP * MT * 2;                    // bytes per X stage
@@ -247,14 +251,14 @@ struct Cfg {
 
 // CL = cluster size sharing each X chunk (multicast); RG = Y-ring variant (Cfg)
 template <int NP, bool SPLIT, int EPI, int CL, int RG>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(Cfg<NP, SPLIT, RG>::THREADS, 1)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
           const __half* __restrict__ Whi, const __half* __restrict__ Wlo, const int* __restrict__ act, int L_ub,
           int64_t M, int64_t slot_len,
           float* __restrict__ Gp, int64_t cap, int n_coarse_h, int S_, const int* __restrict__ cnt, int s_base,
           int S_total, float* __restrict__ Gsub, int64_t sub_cap, const int* __restrict__ cnt_g, int split,
           const int8_t* __restrict__ xshift) {
-  constexpr int NW = 4;   // epilogue warps
+  constexpr int NW = Cfg<NP, SPLIT, RG>::NW;   // epilogue warps
   using C = Cfg<NP, SPLIT, RG>;
   constexpr int MT = C::MT;
   // MODE 0 = the step; timing experiments (scripts/tc_variants.py): 3 = no
@@ -672,7 +676,7 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
   int n_tiles = (int)round_up(ceil_div(L_act, 128), CL);
   if (so.enable) n_tiles = std::max<int>(n_tiles, (int)round_up(std::max(1, kSplitTarget / std::max(S, 1)), CL));
   cudaLaunchConfig_t lc = {};
-  lc.blockDim = dim3(192);
+  lc.blockDim = dim3(C::THREADS);
   lc.dynamicSmemBytes = C::SMEM;
   lc.stream = st;
   cudaLaunchAttribute at[1];

@@ -141,6 +141,13 @@ def _dptr(t) -> int:
     return t.data_ptr()
 
 
+def _ready(t):
+    """The library's stream does not order itself after torch's: make the caller's pending work on
+    this tensor (e.g. an asynchronous host-to-device copy) complete before the library reads it."""
+    import torch
+    torch.cuda.current_stream(t.device).synchronize()
+
+
 def _np_ptr(a, ctype):
     return a.ctypes.data_as(_P(ctype)) if a is not None else None
 
@@ -276,6 +283,7 @@ class Context:
     # -- boundary
     def whiten(self, X, Xw_out, eig_floor: float = 1e-12):
         N, M = X.shape
+        _ready(X)
         mean = np.zeros(N)
         V = np.zeros((N, N))
         eig = np.zeros(N)
@@ -289,6 +297,7 @@ class Context:
             raise OicaError(1, "Xw must be an fp32 row-major CUDA tensor")
         N, M = Xw.shape
         self._keep = Xw
+        _ready(Xw)
         self._c(lib().oica_set_data(self.h, _dptr(Xw), N, M, Xw.stride(0), M if M_global is None else M_global))
         self.N, self.M = N, M
 
@@ -309,6 +318,7 @@ class Context:
     def distribute_data(self, X_root, N: int, M_global: int, X_out, root: int = 0):
         """C3: root's device fp32 N x M_global whitened data -> X_out on every rank (replicated for
         L-shard / hybrid, this rank's column block for M-shard).  X_root may be None off root."""
+        _ready(X_out if X_root is None else X_root)
         self._c(lib().oica_distribute_data(self.h, _dptr(X_root) if X_root is not None else None, N, M_global,
                                            X_root.stride(0) if X_root is not None else M_global, _dptr(X_out),
                                            X_out.stride(0), root))
@@ -346,6 +356,7 @@ class Context:
     def fixed_point_step(self, W, G_out, s4_out, fine: Optional[np.ndarray] = None):
         """One contraction; `fine` (host uint8 per row, fine rows last): per-row precision."""
         L = W.shape[0]
+        _ready(W)
         if fine is None:
             self._c(lib().oica_fixed_point_step(self.h, _dptr(W), L, _dptr(G_out), _dptr(s4_out)))
         else:
