@@ -19,7 +19,7 @@ def golden(name: str) -> dict:
     return json.load(open(os.path.join(HERE, "golden", f"oracle_{name}.json")))
 
 
-@functools.lru_cache(maxsize=2)
+@functools.lru_cache(maxsize=None)
 def golden_input(name: str):
     """(cfg, X32) of tests/golden/oracle_<name>.json; cfg carries the golden's L and N_out."""
     g = golden(name)
