@@ -76,17 +76,23 @@ def golden_path(cfg):
     return None
 
 
-def golden_match(path, W, index, alpha, n):
-    """Compare the all-components leg with the stored oracle results (north_star gates)."""
+def golden_match(path, W, index, alpha, n, sum_active=None, L=None):
+    """Compare the all-components leg with the stored oracle results (north_star gates).  When the
+    golden ran the same L (tier A), also the ratio of row-iterations (sum_t L_act) the GPU needed to
+    the fp64 oracle's: the algorithmic TFLOP/s count the GPU's own iterations."""
     import numpy as np
     g = json.load(open(path))
     comps = g["components"][:n]
     same = sum(int(index[k]) == c["index"] for k, c in enumerate(comps))
     cos = [abs(float(np.dot(W[k], c["w"]))) for k, c in enumerate(comps)]
     rel = [abs((alpha[k] + 3.0) - (c["alpha"] + 3.0)) / abs(c["alpha"] + 3.0) for k, c in enumerate(comps)]
-    return {"golden": os.path.relpath(path, ROOT), "golden_L": g["L"], "components": len(comps),
-            "index_match": same, "min_abs_cos": min(cos) if cos else None, "max_objective_rel_err": max(rel) if rel else None,
-            "pass": bool(same == len(comps) and comps and min(cos) >= 0.9999 and max(rel) <= 1e-4)}
+    out = {"golden": os.path.relpath(path, ROOT), "golden_L": g["L"], "components": len(comps),
+           "index_match": same, "min_abs_cos": min(cos) if cos else None, "max_objective_rel_err": max(rel) if rel else None,
+           "pass": bool(same == len(comps) and comps and min(cos) >= 0.9999 and max(rel) <= 1e-4)}
+    if sum_active is not None and L == g["L"] and all("sum_active" in c for c in comps):
+        out["row_iterations_gpu_over_oracle"] = float(sum(int(v) for v in sum_active[: len(comps)])) / \
+            float(sum(c["sum_active"] for c in comps))
+    return out
 
 
 def dist_env():
@@ -434,7 +440,8 @@ def run_oica(args, cfg):
         all_leg = {"seconds": ams / 1e3, "components": int(ra.n_extracted), "value": aflops / (ams / 1e3) / 1e12,
                    "unit": "TFLOP/s", "indices": [int(v) for v in ra.index[: ra.n_extracted]]}
         if gpath is not None:
-            all_leg["golden_match"] = golden_match(gpath, ra.W, ra.index, ra.alpha, int(ra.n_extracted))
+            all_leg["golden_match"] = golden_match(gpath, ra.W, ra.index, ra.alpha, int(ra.n_extracted), ra.sum_active,
+                                                   cfg.L)
 
     # per-rank breakdown (multi-GPU diagnosis: step kernel / NCCL exchange / tail, communicator init)
     st_now = ctx.stats()
