@@ -156,9 +156,10 @@ struct oica_ctx {
   DevBuf<IterCtl> ctl;     // device iteration state (t, k, update tickets): kernels/kernels.cuh
   // device-side do-while (CUDA graph with a WHILE node, DESIGN.md §5 "iteration"), rebuilt when a
   // parameter baked into its kernels changes
-  struct LoopKey {
+  struct LoopKey {   // every value a captured kernel parameter depends on (buffers by address)
     const void* X;
     const void* Xh;
+    const void* buf[12];
     int64_t M, Mg, slot_len, ldx, vld;
     int vN, vNP, S, L_ub, K, precision;
     double tol;
@@ -1134,8 +1135,25 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
 void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
   cudaStream_t st = c->st;
   c->loop_persistent = false;
-  const oica_ctx::LoopKey key{c->vX, c->vXh, c->M, c->Mg, c->slot_len, c->ldx, c->vld, c->vN, c->vNP, c->S,
-                              L_ub, K, c->precision, tol};
+  oica_ctx::LoopKey key;
+  std::memset(&key, 0, sizeof key);   // (padding bytes take part in the comparison)
+  key.X = c->vX;
+  key.Xh = c->vXh;
+  const void* bufs[12] = {c->act0.p, c->act1.p, c->W64.p, c->Whi.p, c->Wlo.p, c->W32.p, c->Gp32.p, c->Gsub.p,
+                          c->Gp.p, c->s4p.p, c->hist.p, c->xshift.p};
+  std::memcpy(key.buf, bufs, sizeof bufs);
+  key.M = c->M;
+  key.Mg = c->Mg;
+  key.slot_len = c->slot_len;
+  key.ldx = c->ldx;
+  key.vld = c->vld;
+  key.vN = c->vN;
+  key.vNP = c->vNP;
+  key.S = c->S;
+  key.L_ub = L_ub;
+  key.K = K;
+  key.precision = c->precision;
+  key.tol = tol;
   if (!(c->loop.valid && c->loop.key == key)) {
     c->loop.reset();
     // grid-size tiers: the loop over L_ub rows hands over to one sized for 2048, then 128, then 32
