@@ -133,6 +133,11 @@ typedef struct {
  * (bitwise the same results); OICA_EAGER launches every iteration from the host instead, which
  * times each step launch for oica_get_iteration_log / oica_stats.step_ms. */
 #define OICA_EAGER               0x10u
+/* Tiny FP32 problems (L <= 512, M < 65536, one rank) run the device-side loop as ONE cooperative
+ * kernel whose grid barriers need its blocks co-resident; several extractions running concurrently
+ * on one GPU (one context / stream each) are better served by the CUDA-graph loop: this flag
+ * selects it (bitwise the same results). */
+#define OICA_NO_PERSISTENT       0x20u
 
 /* Counters of the last extract / step call (for benchmarks; all host values). */
 typedef struct {

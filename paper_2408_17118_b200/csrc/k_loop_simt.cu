@@ -37,7 +37,7 @@ struct LoopSimtArgs {
 };
 
 template <int NP, int NG>
-__global__ void __launch_bounds__(256) k_loop_simt(LoopSimtArgs a) {
+__global__ void __launch_bounds__(256, 2) k_loop_simt(LoopSimtArgs a) {
   constexpr int RPB = 8 / NG;
   __shared__ double gsh[RPB][NG * 32];
   __shared__ double s4sh[RPB];

@@ -1365,7 +1365,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     bool to_tail = lockstep && refresh();
     if (fast) {   // the whole do-while on the device
       sync_x(c);   // (a pipelined upload is waited for: the graph is captured on the context stream)
-      if (persistent_loop_ok(c))
+      if (persistent_loop_ok(c) && !(flags & OICA_NO_PERSISTENT))
         enqueue_loop_simt(c, K, tol);      // tiny FP32 problems: one cooperative launch
       else
         enqueue_loop_graph(c, L_ub, nc_ub, K, tol);   // one graph launch

@@ -28,7 +28,7 @@ STATUS = ["OK", "INVALID_ARGUMENT", "DIMENSION_MISMATCH", "RANK_DEFICIENT", "ALL
 
 PREC_AUTO, PREC_FP32, PREC_TC, PREC_TC_SPLIT = 0, 1, 2, 3
 SHARD_L, SHARD_M, SHARD_HYBRID = 0, 1, 2
-INCLUDE_UNCONVERGED, STOP_ON_GAUSSIANITY, RAW_ARGMAX, REDUCE_X, EAGER = 0x1, 0x2, 0x4, 0x8, 0x10
+INCLUDE_UNCONVERGED, STOP_ON_GAUSSIANITY, RAW_ARGMAX, REDUCE_X, EAGER, NO_PERSISTENT = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 MAX_CLUSTERS = 8
 
 

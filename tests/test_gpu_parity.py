@@ -169,9 +169,11 @@ def test_device_loop_bitwise(name, precision):
             g = ctx.extract(cfg.N_out, K, cfg.tol, flags=fl)
             st = ctx.stats()
             e = ctx.extract(cfg.N_out, K, cfg.tol, flags=fl | oica.EAGER)
+            p = ctx.extract(cfg.N_out, K, cfg.tol, flags=fl | oica.NO_PERSISTENT)   # the graph loop for FP32 too
             assert st["graph_iterations"] > 0
             for f in ("W", "alpha", "index", "iters", "n_iter", "cluster_size", "n_converged", "sum_active"):
                 assert np.array_equal(getattr(g, f), getattr(e, f)), f
+                assert np.array_equal(getattr(p, f), getattr(e, f)), f
             ctx.reset_stats()
 
 
