@@ -143,6 +143,13 @@ __global__ void __launch_bounds__(1024) k_compact_iter(UpdateArgs u) {
   if (threadIdx.x == 0) finish_iteration(u, r, L_in, t);
 }
 
+// First node of the device-side loop graph: the first WHILE node starts only if runs are active
+// and t <= K (a pipelined upload may have run iteration 1 already: with K = 1 nothing is left)
+__global__ void k_loop_gate(cudaGraphConditionalHandle h, const int* __restrict__ cnt, const IterCtl* __restrict__ ctl,
+                            int K) {
+  cudaGraphSetConditional(h, (cnt[0] > 0 && ctl->t <= K) ? 1u : 0u);
+}
+
 __global__ void k_ctl_set(IterCtl* ctl, int t, int k) {
   ctl->t = t;
   ctl->k = k;
@@ -348,6 +355,18 @@ int launch_compact_iter(cudaStream_t st, const UpdateArgs& u) {
   if (u.L_ub <= 0) return 0;
   k_compact_iter<<<1, 1024, 0, st>>>(u);
   return 1;
+}
+
+void add_loop_gate_node(cudaGraph_t g, cudaGraphNode_t* node, cudaGraphConditionalHandle h, const int* cnt,
+                        const IterCtl* ctl, int K) {
+  void* args[] = {(void*)&h, (void*)&cnt, (void*)&ctl, (void*)&K};
+  cudaKernelNodeParams kp{};
+  kp.func = (void*)k_loop_gate;
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(1);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  OICA_CUDA(cudaGraphAddKernelNode(node, g, nullptr, 0, &kp));
 }
 
 int launch_ctl_set(cudaStream_t st, IterCtl* ctl, int t, int k) {

@@ -17,6 +17,32 @@ namespace {
 constexpr double kRefineMarginRel = 1e-2;   // clusters refined: Upsilon~ >= max - 1%
 constexpr double kRefineMarginAbs = 1e-7;
 
+// w_l . w_p as one warp computes it: lane j sums coordinates j, j + 32, ... (fma chain from 0),
+// then the xor butterfly of warp_sum.  The cluster test of every selection path uses exactly this
+// arithmetic, so membership never depends on which kernel (and so on the L-shard split) decides it.
+__device__ __forceinline__ double dot_warp(const double* __restrict__ a, const double* __restrict__ b, int N,
+                                           int lane) {
+  double d = 0.0;
+  for (int n = lane; n < N; n += 32) d = fma(a[n], b[n], d);
+  return warp_sum(d);
+}
+// The same value computed by ONE thread (few coordinates, many rows): the 32 lane partial sums,
+// then the butterfly's tree (lane 0 of xor 16, 8, 4, 2, 1 adds (v0 + v16) + (v8 + v24) + ...).
+__device__ __forceinline__ double dot_thread(const double* __restrict__ a, const double* __restrict__ b, int N) {
+  double v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double d = 0.0;
+    for (int n = j; n < N; n += 32) d = fma(a[n], b[n], d);
+    v[j] = d;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int j = 0; j < o; ++j) v[j] = v[j] + v[j + o];
+  return v[0];
+}
+
 __device__ __forceinline__ bool eligible(uint8_t st, bool include_unconv, int n_conv) {
   return st == ST_CONVERGED || (st == ST_ACTIVE && (include_unconv || n_conv == 0));
 }
@@ -118,9 +144,7 @@ __global__ void k_assign(const double* __restrict__ W64, const double* __restric
   bool inc = flags & OICA_INCLUDE_UNCONVERGED;
   if (!eligible(state[l], inc, nconv_g ? *nconv_g : counts[0]) || cluster[l] >= 0 || !(alpha[l] > kAlphaFloor)) return;
   if ((flags & OICA_RAW_ARGMAX) && l != p) return;   // raw argmax: singleton records
-  double d = 0.0;
-  for (int n = lane; n < N; n += 32) d += W64[(int64_t)l * N + n] * W64[(int64_t)p * N + n];
-  d = warp_sum(d);
+  const double d = dot_warp(W64 + (int64_t)l * N, W64 + (int64_t)p * N, N, lane);
   if (1.0 - fabs(d) <= kClusterDelta && lane == 0) {
     cluster[l] = c;
     atomicMin(&qc[c], l);
@@ -133,6 +157,8 @@ __global__ void k_assign(const double* __restrict__ W64, const double* __restric
 // k_argmax and k_assign: block reductions with the same tie rule, the same refine margin, the same
 // cluster test; q_c = min id and the sizes are order-independent (atomics).
 constexpr int kSelectSmallL = 2048;   // above: the multi-block assign is faster (cfg 2, L = 4096: 250 vs 350 us)
+constexpr int kSelectThreadN = 64;    // up to this N the single block assigns one candidate per thread
+constexpr int kSelectSmallLThread = 4096;   // ... and takes up to this many candidates
 __global__ void __launch_bounds__(1024) k_select_small(const double* __restrict__ W64,
                                                        const double* __restrict__ alpha,
                                                        const uint8_t* __restrict__ state, int L, int N,
@@ -143,6 +169,7 @@ __global__ void __launch_bounds__(1024) k_select_small(const double* __restrict_
   __shared__ int sl[32];
   __shared__ int s_p;
   __shared__ double s_um;
+  __shared__ double s_wp[kSelectThreadN];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const bool inc = flags & OICA_INCLUDE_UNCONVERGED;
   const bool raw = flags & OICA_RAW_ARGMAX;
@@ -216,16 +243,29 @@ __global__ void __launch_bounds__(1024) k_select_small(const double* __restrict_
       done = true;
       continue;
     }
-    for (int l = w; l < L; l += blockDim.x >> 5) {   // one warp per candidate row
-      if (!eligible(state[l], inc, n_conv) || cluster[l] >= 0 || !(alpha[l] > kAlphaFloor)) continue;
-      if (raw && l != p) continue;
-      double d = 0.0;
-      for (int n = lane; n < N; n += 32) d += W64[(int64_t)l * N + n] * W64[(int64_t)p * N + n];
-      d = warp_sum(d);
-      if (1.0 - fabs(d) <= kClusterDelta && lane == 0) {
-        cluster[l] = c;
-        atomicMin(&qc[c], l);
-        atomicAdd(&csize[c], 1);
+    if (N <= kSelectThreadN) {   // one thread per candidate row, w_p in shared memory
+      for (int n = tid; n < N; n += blockDim.x) s_wp[n] = W64[(int64_t)p * N + n];
+      __syncthreads();
+      for (int l = tid; l < L; l += blockDim.x) {
+        if (!eligible(state[l], inc, n_conv) || cluster[l] >= 0 || !(alpha[l] > kAlphaFloor)) continue;
+        if (raw && l != p) continue;
+        const double d = dot_thread(W64 + (int64_t)l * N, s_wp, N);
+        if (1.0 - fabs(d) <= kClusterDelta) {
+          cluster[l] = c;
+          atomicMin(&qc[c], l);
+          atomicAdd(&csize[c], 1);
+        }
+      }
+    } else {
+      for (int l = w; l < L; l += blockDim.x >> 5) {   // one warp per candidate row
+        if (!eligible(state[l], inc, n_conv) || cluster[l] >= 0 || !(alpha[l] > kAlphaFloor)) continue;
+        if (raw && l != p) continue;
+        const double d = dot_warp(W64 + (int64_t)l * N, W64 + (int64_t)p * N, N, lane);
+        if (1.0 - fabs(d) <= kClusterDelta && lane == 0) {
+          cluster[l] = c;
+          atomicMin(&qc[c], l);
+          atomicAdd(&csize[c], 1);
+        }
       }
     }
     __syncthreads();
@@ -448,7 +488,7 @@ int launch_select_local(cudaStream_t st, const double* W64, const double* alpha_
                         int* counts, double* part, int nblk, double* s4c, const int* nconv_g) {
   (void)iters;
   int launches = 0;
-  if (L_local <= kSelectSmallL) {
+  if (L_local <= kSelectSmallL || (N <= kSelectThreadN && L_local <= kSelectSmallLThread)) {
     k_select_small<<<1, 1024, 0, st>>>(W64, alpha_old, state, L_local, N, flags, counts, cluster, ups_max, pc, qc,
                                        csize, nconv_g);
     ++launches;

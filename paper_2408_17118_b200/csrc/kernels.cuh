@@ -151,6 +151,10 @@ int update_blocks(int L_ub, int NP);
 // kept in place, act_out = scratch, ctl, hist, ...).  NP = 32 or 64.
 int launch_loop_simt(cudaStream_t st, const float* X, int64_t ld, int64_t M, int64_t slot_len, int S, int flush,
                      int K, const UpdateArgs& u, int NP, int num_sms);
+// Adds the loop graph's first node: sets h = (cnt[0] > 0 && ctl->t <= K) (the first WHILE node's
+// condition, so the loop also runs zero times when nothing is left to iterate)
+void add_loop_gate_node(cudaGraph_t g, cudaGraphNode_t* node, cudaGraphConditionalHandle h, const int* cnt,
+                        const IterCtl* ctl, int K);
 // ctl <- {t, k, 0} (component start; t = 1)
 int launch_ctl_set(cudaStream_t st, IterCtl* ctl, int t, int k);
 

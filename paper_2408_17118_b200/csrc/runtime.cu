@@ -1164,9 +1164,10 @@ void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
     const int nt = (int)tiers.size();
     OICA_CUDA(cudaGraphCreate(&c->loop.g, 0));
     std::vector<cudaGraphConditionalHandle> hs((size_t)nt);
-    for (int i = 0; i < nt; ++i)   // the first loop starts (do-while); the next ones when handed over
-      OICA_CUDA(cudaGraphConditionalHandleCreate(&hs[i], c->loop.g, i == 0 ? 1 : 0, cudaGraphCondAssignDefault));
+    for (int i = 0; i < nt; ++i)   // the gate starts the first loop; each loop hands over to the next
+      OICA_CUDA(cudaGraphConditionalHandleCreate(&hs[i], c->loop.g, 0, cudaGraphCondAssignDefault));
     cudaGraphNode_t prev = nullptr;
+    add_loop_gate_node(c->loop.g, &prev, hs[0], c->Lact_dev.p, c->ctl.p, K);
     for (int i = 0; i < nt; ++i) {
       cudaGraphNodeParams cp{};
       cp.type = cudaGraphNodeTypeConditional;
@@ -1364,7 +1365,19 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     if (lockstep) OICA_CUDA(cudaMemsetAsync(c->hist.p, 0, sizeof(int) * 2 * ((size_t)K + 1), st));
     bool to_tail = lockstep && refresh();
     if (fast) {   // the whole do-while on the device
-      sync_x(c);   // (a pipelined upload is waited for: the graph is captured on the context stream)
+      if (c->x_pending && c->tc()) {
+        // a pipelined host upload is in flight (oica_set_data_host): iteration 1 is launched here,
+        // its step piece by piece as the upload lands -- the kernels and sizes of
+        // the graph body, so the same arithmetic -- and the graph continues from t = 2
+        const int* cnt = c->Lact_dev.p;
+        run_step(c, act, L_ub, nc_ub, cnt, cnt, c->tc() && !c->split(), false);
+        UpdateArgs u = update_args(c, c->partials(cnt, L_ub), nullptr, c->S, c->Ll, act, c->act1.p, L_ub, tol,
+                                   c->hist.p);
+        u.copy_back = 1;
+        run_update(c, u);
+        check_launch();
+      }
+      sync_x(c);   // (the rest of the loop is a graph captured on the context stream)
       if (persistent_loop_ok(c) && !(flags & OICA_NO_PERSISTENT))
         enqueue_loop_simt(c, K, tol);      // tiny FP32 problems: one cooperative launch
       else

@@ -669,6 +669,18 @@ def test_host_upload_bitwise(name, precision):
             outs.append(ctx.extract(cfg.N_out, cfg.K, cfg.tol))
         ctx.set_data_host(X32)
         red = ctx.extract(cfg.N_out, cfg.K, cfg.tol, flags=oica.REDUCE_X)
+        # small caps: the upload-overlapped first iteration of the device-side loop, then nothing
+        # (K = 1) or a few more iterations in the graph
+        caps = {}
+        for K in (1, 3):
+            ctx.set_data(torch.from_numpy(X32).cuda())
+            d_k = ctx.extract(cfg.N_out, K, cfg.tol, flags=oica.INCLUDE_UNCONVERGED)
+            ctx.set_data_host_ptr(pinned.data_ptr(), cfg.N, cfg.M, cfg.M)
+            h_k = ctx.extract(cfg.N_out, K, cfg.tol, flags=oica.INCLUDE_UNCONVERGED)
+            caps[K] = (d_k, h_k)
     for o in outs:
         assert np.array_equal(o.W, dev.W) and np.array_equal(o.index, dev.index) and np.array_equal(o.alpha, dev.alpha)
     assert np.array_equal(red.W, dev_red.W) and np.array_equal(red.index, dev_red.index)
+    for K, (d_k, h_k) in caps.items():
+        assert np.array_equal(d_k.W, h_k.W) and np.array_equal(d_k.index, h_k.index), K
+        assert np.all(d_k.n_iter[: cfg.N_out] <= K), (K, d_k.n_iter)
