@@ -264,7 +264,8 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   // MODE 0 = the step; timing experiments (scripts/tc_variants.py): 3 = no
   // epilogue (MMA + data), 4 = GEMM1 only, 5 = GEMM2 only, 6 = no MMA (X streaming only),
   // 7 = GEMM1 only with an fp16 accumulator, 8 = step with an fp16 GEMM1 accumulator read as the
-  // low half of each 32-bit TMEM cell (probe of the 16-bit accumulator layout)
+  // low half of each 32-bit TMEM cell (probe of the 16-bit accumulator layout), 9 = step without
+  // the X stream (stale stages), 10 = MMAs only (no X stream, no epilogue)
   constexpr int MODE = EPI;
   constexpr int EPI_ARRIVALS = 32 * NW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -353,6 +354,10 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         int st = j % C::STAGES;
         if (j >= C::STAGES) mbar_wait(&empty[st], ((j / C::STAGES) - 1) & 1);
         int m0 = (int)(m_begin + (int64_t)j * MT);
+        if (MODE == 9 || MODE == 10) {   // experiment: no X stream (MMAs / epilogue on stale stages)
+          mbar_arrive(&full[st]);
+          continue;
+        }
         mbar_expect_tx(&full[st], C::X_STAGE);
         uint8_t* dst = s_x + st * C::X_STAGE;
         for (int h = 0; h < MT / 64; ++h) {
@@ -508,7 +513,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const uint32_t t_y = tmem + lane_off + C::C_Y0 + b * MT;
       mbar_wait(&yfull[b], (j / C::R) & 1);
       tc_fence_after();
-      if ((MODE >= 3 && MODE != 8) || idle) {   // idle tile; experiment: no TMEM traffic (MMA pipeline upper bound)
+      if ((MODE >= 3 && MODE != 8 && MODE != 9) || idle) {   // idle tile; experiment: no TMEM traffic (MMA pipeline upper bound)
         tc_fence_before();
         mbar_arrive(&y3ready[b]);
         continue;
@@ -748,6 +753,8 @@ void launch_epi(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const
     case 6: launch_variant<NP, SPLIT, 6>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
     case 7: launch_variant<NP, SPLIT, 7>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
     case 8: launch_variant<NP, SPLIT, 8>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 9: launch_variant<NP, SPLIT, 9>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
+    case 10: launch_variant<NP, SPLIT, 10>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, t0, cnt, up, so, xshift); return;
     default: break;
   }
 #endif

@@ -15,7 +15,7 @@ import torch
 sys.path.insert(0, os.environ.get("OICA_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2408_17118_b200 import oica  # noqa: E402
 
-shapes = {256: (4_000_000, 65536), 128: (1_000_000, 16384), 64: (250_000, 4096)}
+shapes = {256: (4_000_000, 65536), 128: (1_000_000, 16384), 64: (250_000, 4096), 32: (250_000, 4096)}
 Ns = [int(a) for a in sys.argv[2:]] or [256, 128]
 for N in Ns:
     M, L = shapes[N]
