@@ -241,3 +241,114 @@ def test_a4_global_converged_count_two_ranks_gloo():
     assert not res[0].no_converged
     assert out[0][2] == out[1][2] == res[0].index                # the single-process decision
     assert out[0][1:3] == out[1][1:3] or out[0][2] == out[1][2]
+
+
+# ---- hybrid L -> M tail (runtime.cu run_hybrid_tail): L-shard
+# iterations in lock step on the GLOBAL active count until it falls to the tail threshold; then
+# the still-active runs of every rank are all-gathered in rank order, iterated M-sharded (each rank
+# sums its share of the samples, one fp64 all-reduce per iteration, identical epilogues), and the
+# finished rows return to their owners by id; selection is the L-shard merge (reading A6)
+def _hybrid_worker(rank, world, port, rows_thr, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = datagen.PARITY["p_ragged"].with_(L=40)
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X = Xw.astype(np.float32).astype(np.float64)
+    N, M = X.shape
+    L, K = cfg.L, cfg.K
+    lo, hi = L * rank // world, L * (rank + 1) // world
+    ids = np.arange(lo, hi)
+    from oracle import rng
+    W = rng.candidates(cfg.cand_seed, 1, ids, N)
+    W /= np.linalg.norm(W, axis=1, keepdims=True)
+    conv = np.zeros(ids.size, dtype=bool)
+    active = np.arange(ids.size)
+
+    def epilogue(B, Gsum):
+        G = Gsum / M - 3.0 * B                                   # eq. (5), global M
+        Wn = G / np.linalg.norm(G, axis=1, keepdims=True)
+        return Wn, ordering.convergence_distance(Wn, B) <= cfg.tol
+
+    t = 0
+    while t < K:                                                 # L-shard, lock step
+        n = torch.tensor([active.size])
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        if int(n.item()) <= rows_thr:
+            break
+        t += 1
+        if active.size:
+            B = W[active]
+            Wn, c = epilogue(B, ((B @ X) ** 3) @ X.T)
+            W[active] = Wn
+            conv[active[c]] = True
+            active = active[~c]
+    t_switch = t
+    # C4: all-gather the active runs (id, row) in rank order
+    cnts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(cnts, torch.tensor([active.size]))
+    cnts = [int(v.item()) for v in cnts]
+    P = max(cnts + [1])
+    pack = np.zeros((P, N + 1))
+    pack[:active.size, 0] = ids[active]
+    pack[:active.size, 1:] = W[active]
+    allp = [torch.zeros(P, N + 1, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(allp, torch.from_numpy(pack))
+    dense = np.concatenate([allp[r].numpy()[:cnts[r]] for r in range(world)])
+    tid = dense[:, 0].astype(np.int64)
+    TW = dense[:, 1:].copy()
+    tconv = np.zeros(tid.size, dtype=bool)
+    tact = np.arange(tid.size)
+    m0, m1 = M * rank // world, M * (rank + 1) // world          # this rank's samples of the tail
+    Xr = X[:, m0:m1]
+    while tact.size and t < K:                                   # M-sharded tail iterations
+        t += 1
+        B = TW[tact]
+        part = torch.from_numpy((((B @ Xr) ** 3) @ Xr.T).copy())
+        dist.all_reduce(part, op=dist.ReduceOp.SUM)
+        Wn, c = epilogue(B, part.numpy())
+        TW[tact] = Wn
+        tconv[tact[c]] = True
+        tact = tact[~c]
+    # finished rows back to their owners by global id
+    for j, g in enumerate(tid):
+        if lo <= g < hi:
+            W[g - lo] = TW[j]
+            conv[g - lo] = tconv[j]
+    recs, rows = local_records(X, W, ids, conv, N)
+    R = [torch.zeros(MAXC, 6, dtype=torch.float64) for _ in range(world)]
+    Wl = [torch.zeros(MAXC, N, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(R, torch.from_numpy(recs))
+    dist.all_gather(Wl, torch.from_numpy(rows))
+    allr = torch.cat(R).numpy()
+    allw = torch.cat(Wl).numpy()
+    recl = [dict(upsilon=r[0], alpha=r[1], q=int(r[2]), size=int(r[3]), iters=0, valid=int(r[5])) for r in allr]
+    m = oica.merge_records(recl, allw)
+    q.put((rank, int(allr[m["winner"]][2]), float(allr[m["winner"]][1]), TW.tobytes(), t_switch, tid.size, t))
+    dist.destroy_process_group()
+
+
+def test_hybrid_tail_two_ranks_gloo():
+    world, rows_thr = 2, 12
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hybrid_worker, args=(r, world, port, rows_thr, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # the tail was entered with a real M-sharded phase, and both ranks hold bitwise-identical tail
+    # iterates (same all-reduced sums) and make the same decision ...
+    assert 0 < out[0][4] < out[0][6] and 0 < out[0][5] <= rows_thr
+    assert out[0][1:] == out[1][1:]
+    # ... which is the single-process oracle's (the sample sums are re-associated by rank)
+    cfg = datagen.PARITY["p_ragged"].with_(L=40)
+    ds = datagen.make_dataset(cfg)
+    Xw, _, _, _ = whiten.whiten(ds.X.numpy())
+    X = Xw.astype(np.float32).astype(np.float64)
+    _, res = ordering.extract(X, cfg.L, cfg.K, cfg.tol, 1, cfg.cand_seed)
+    assert out[0][1] == res[0].index
+    assert out[0][2] == pytest.approx(res[0].alpha, rel=1e-10)
