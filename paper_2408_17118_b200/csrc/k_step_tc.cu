@@ -141,6 +141,18 @@ __device__ __forceinline__ float2 cube2(uint32_t a0, uint32_t a1) {
   return make_float2(__uint_as_float((uint32_t)cu), __uint_as_float((uint32_t)(cu >> 32)));
 }
 
+// 8 consecutive floats (32-byte aligned) in one 256-bit store (sm_100)
+__device__ __forceinline__ void st_v8(float* p, const float (&g)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(g[0]), "f"(g[1]), "f"(g[2]), "f"(g[3]),
+               "f"(g[4]), "f"(g[5]), "f"(g[6]), "f"(g[7])
+               : "memory");
+}
+__device__ __forceinline__ void st_v8_cs(float* p, const float (&g)[8]) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(g[0]), "f"(g[1]), "f"(g[2]),
+               "f"(g[3]), "f"(g[4]), "f"(g[5]), "f"(g[6]), "f"(g[7])
+               : "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -486,18 +498,30 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         __trap();
       }
 #endif
-      const uint32_t* wh = (const uint32_t*)(Whi + id * NP);
-      const uint32_t* wl = (const uint32_t*)(Wlo + id * NP);
+      // 16-byte loads, up to 32 of them in flight per thread (one L2 round trip for NP <= 128)
+      const uint4* wh = (const uint4*)(Whi + id * NP);
+      const uint4* wl = (const uint4*)(Wlo + id * NP);
+      constexpr int CB = NP / 2 < 64 ? NP / 2 : 64;   // 32-bit columns per batch (a multiple of 8)
 #pragma unroll 1
-      for (int c = 8 * h; c < NP / 2; c += 8 * NH) {   // NP/2 is a multiple of 8 columns
-        uint32_t v[8];
+      for (int c0 = CB * h; c0 < NP / 2; c0 += CB * NH) {
+        uint4 a[CB / 4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = ok ? __ldg(wh + c + k) : 0u;
-        tmem_st8(tmem + lane_off + C::C_WHI + c, v);
+        for (int k = 0; k < CB / 4; ++k) a[k] = ok ? __ldg(wh + c0 / 4 + k) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int k = 0; k < CB / 8; ++k) {
+          const uint32_t v[8] = {a[2 * k].x, a[2 * k].y, a[2 * k].z, a[2 * k].w,
+                                 a[2 * k + 1].x, a[2 * k + 1].y, a[2 * k + 1].z, a[2 * k + 1].w};
+          tmem_st8(tmem + lane_off + C::C_WHI + c0 + 8 * k, v);
+        }
         if (C::WLO_TMEM && lo_pass) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) v[k] = ok ? __ldg(wl + c + k) : 0u;
-          tmem_st8(tmem + lane_off + C::C_WLO + c, v);
+          for (int k = 0; k < CB / 4; ++k) a[k] = ok ? __ldg(wl + c0 / 4 + k) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int k = 0; k < CB / 8; ++k) {
+            const uint32_t v[8] = {a[2 * k].x, a[2 * k].y, a[2 * k].z, a[2 * k].w,
+                                   a[2 * k + 1].x, a[2 * k + 1].y, a[2 * k + 1].z, a[2 * k + 1].w};
+            tmem_st8(tmem + lane_off + C::C_WLO + c0 + 8 * k, v);
+          }
         }
       }
       tmem_wait_st();
@@ -583,14 +607,20 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       tmem_ld32(tmem + lane_off + C::C_G + c, v);
       tmem_wait_ld();
       if (ok) {
+        // 32-byte vector stores (one full sector each: the thread's row is contiguous, the warp's
+        // 32 rows are not, so scalar stores cost a partial-sector write per element -- measured
+        // ~4 us per 128 x 64 partial, 20% of a cfg-2 unit).  Streaming (.cs: keep the X planes
+        // in L2), except the few rows of split parts, which the update reads next.
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (NP % 32 == 0 || c + k < NP) {   // streaming store (keep the X planes in L2), except
-            const float g = __uint_as_float(v[k]) * gsc;       // the few rows of split parts,
-            if (P > 1)                                          // which the epilogue reads next
-              out[c + k] = g;
+        for (int k = 0; k < 32; k += 8)
+          if (NP % 32 == 0 || c + k < NP) {   // (NP is a multiple of 16: groups of 8 are whole)
+            float g[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) g[e] = __uint_as_float(v[k + e]) * gsc;
+            if (P > 1)
+              st_v8(out + c + k, g);
             else
-              __stcs(out + c + k, g);
+              st_v8_cs(out + c + k, g);
           }
       }
     }
