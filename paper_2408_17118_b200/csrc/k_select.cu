@@ -26,23 +26,6 @@ __device__ __forceinline__ double dot_warp(const double* __restrict__ a, const d
   for (int n = lane; n < N; n += 32) d = fma(a[n], b[n], d);
   return warp_sum(d);
 }
-// The same value computed by ONE thread (few coordinates, many rows): the 32 lane partial sums,
-// then the butterfly's tree (lane 0 of xor 16, 8, 4, 2, 1 adds (v0 + v16) + (v8 + v24) + ...).
-__device__ __forceinline__ double dot_thread(const double* __restrict__ a, const double* __restrict__ b, int N) {
-  double v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    double d = 0.0;
-    for (int n = j; n < N; n += 32) d = fma(a[n], b[n], d);
-    v[j] = d;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int j = 0; j < o; ++j) v[j] = v[j] + v[j + o];
-  return v[0];
-}
-
 __device__ __forceinline__ bool eligible(uint8_t st, bool include_unconv, int n_conv) {
   return st == ST_CONVERGED || (st == ST_ACTIVE && (include_unconv || n_conv == 0));
 }
@@ -157,7 +140,9 @@ __global__ void k_assign(const double* __restrict__ W64, const double* __restric
 // k_argmax and k_assign: block reductions with the same tie rule, the same refine margin, the same
 // cluster test; q_c = min id and the sizes are order-independent (atomics).
 constexpr int kSelectSmallL = 2048;   // above: the multi-block assign is faster (cfg 2, L = 4096: 250 vs 350 us)
-constexpr int kSelectThreadN = 64;    // up to this N the single block assigns one candidate per thread
+constexpr int kSelectThreadN = 64;    // up to this N the single block takes ...
+// (cluster tests: one warp per candidate row, coalesced 8-byte lanes; one thread per row read 32
+// rows per load instruction -- ~225 us per selection at cfg 2 under ncu)
 constexpr int kSelectSmallLThread = 4096;   // ... and takes up to this many candidates
 __global__ void __launch_bounds__(1024) k_select_small(const double* __restrict__ W64,
                                                        const double* __restrict__ alpha,
@@ -169,7 +154,7 @@ __global__ void __launch_bounds__(1024) k_select_small(const double* __restrict_
   __shared__ int sl[32];
   __shared__ int s_p;
   __shared__ double s_um;
-  __shared__ double s_wp[kSelectThreadN];
+  __shared__ double s_wp[256];   // N <= 256 (oica_set_data)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const bool inc = flags & OICA_INCLUDE_UNCONVERGED;
   const bool raw = flags & OICA_RAW_ARGMAX;
@@ -243,28 +228,46 @@ __global__ void __launch_bounds__(1024) k_select_small(const double* __restrict_
       done = true;
       continue;
     }
-    if (N <= kSelectThreadN) {   // one thread per candidate row, w_p in shared memory
-      for (int n = tid; n < N; n += blockDim.x) s_wp[n] = W64[(int64_t)p * N + n];
-      __syncthreads();
-      for (int l = tid; l < L; l += blockDim.x) {
-        if (!eligible(state[l], inc, n_conv) || cluster[l] >= 0 || !(alpha[l] > kAlphaFloor)) continue;
-        if (raw && l != p) continue;
-        const double d = dot_thread(W64 + (int64_t)l * N, s_wp, N);
-        if (1.0 - fabs(d) <= kClusterDelta) {
-          cluster[l] = c;
-          atomicMin(&qc[c], l);
-          atomicAdd(&csize[c], 1);
+    // cluster test, one warp per candidate row (coalesced lanes, dot_warp's arithmetic: lane j
+    // sums coordinates j, j + 32, ... by an fma chain from 0, then the butterfly), up to kB rows
+    // of a warp's 32 in flight together (latency-bound otherwise)
+    for (int n = tid; n < N; n += blockDim.x) s_wp[n] = W64[(int64_t)p * N + n];
+    __syncthreads();
+    constexpr int kB = 8;
+    for (int base = w * 32; base < L; base += blockDim.x) {   // a warp takes 32 consecutive rows
+      const int l = base + lane;
+      const bool e = l < L && eligible(state[l], inc, n_conv) && cluster[l] < 0 && alpha[l] > kAlphaFloor &&
+                     !(raw && l != p);
+      unsigned mask = __ballot_sync(0xffffffffu, e);
+      while (mask) {
+        int rr[kB];
+        int nr = 0;
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+          rr[i] = mask ? base + __ffs(mask) - 1 : -1;
+          if (mask) {
+            mask &= mask - 1;
+            ++nr;
+          }
         }
-      }
-    } else {
-      for (int l = w; l < L; l += blockDim.x >> 5) {   // one warp per candidate row
-        if (!eligible(state[l], inc, n_conv) || cluster[l] >= 0 || !(alpha[l] > kAlphaFloor)) continue;
-        if (raw && l != p) continue;
-        const double d = dot_warp(W64 + (int64_t)l * N, W64 + (int64_t)p * N, N, lane);
-        if (1.0 - fabs(d) <= kClusterDelta && lane == 0) {
-          cluster[l] = c;
-          atomicMin(&qc[c], l);
-          atomicAdd(&csize[c], 1);
+        double d[kB];
+#pragma unroll
+        for (int i = 0; i < kB; ++i) d[i] = 0.0;
+        for (int n = lane; n < N; n += 32) {
+          const double b = s_wp[n];
+#pragma unroll
+          for (int i = 0; i < kB; ++i)
+            if (i < nr) d[i] = fma(W64[(int64_t)rr[i] * N + n], b, d[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+          if (i >= nr) break;
+          const double di = warp_sum(d[i]);
+          if (1.0 - fabs(di) <= kClusterDelta && lane == 0) {
+            cluster[rr[i]] = c;
+            atomicMin(&qc[c], rr[i]);
+            atomicAdd(&csize[c], 1);
+          }
         }
       }
     }
@@ -357,22 +360,16 @@ __global__ void __launch_bounds__(256) k_alpha_exact(const double* __restrict__ 
   }
 }
 
-__global__ void k_alpha_reduce(const double* __restrict__ part, int nblk, double* s4c) {
-  int c = threadIdx.x;
-  if (c >= kMaxClusters) return;
-  // fixed block order; 8 loads in flight (a serial chain of ~500 dependent loads otherwise)
+// one warp per cluster row: lane j sums blocks j, j + 32, ... in order, then the xor butterfly
+// (a fixed order; one thread per row was a ~1200-long chain of dependent adds, ~20 us)
+__global__ void __launch_bounds__(32 * kMaxClusters) k_alpha_reduce(const double* __restrict__ part, int nblk,
+                                                                    double* s4c) {
+  const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* p = part + (int64_t)c * nblk;
   double v = 0.0;
-  int b = 0;
-  for (; b + 8 <= nblk; b += 8) {
-    double t[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = p[b + u];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v += t[u];
-  }
-  for (; b < nblk; ++b) v += p[b];
-  s4c[c] = v;
+  for (int b = lane; b < nblk; b += 32) v += p[b];
+  v = warp_sum(v);
+  if (lane == 0) s4c[c] = v;
 }
 
 __global__ void k_finish(const double* __restrict__ W64, const int* __restrict__ iters, const int* __restrict__ counts,
@@ -505,7 +502,7 @@ int launch_select_local(cudaStream_t st, const double* W64, const double* alpha_
     }
   }
   k_alpha_exact<<<nblk, 256, 0, st>>>(W64, X, ld, M_local, N, pc, qc, flags, part, nblk);
-  k_alpha_reduce<<<1, 32, 0, st>>>(part, nblk, s4c);
+  k_alpha_reduce<<<1, 32 * kMaxClusters, 0, st>>>(part, nblk, s4c);
   return launches + 2;
 }
 
