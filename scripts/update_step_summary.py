@@ -52,8 +52,12 @@ def main():
             "algorithmic_bytes_note": f"X fp16 once (2 N M) + fp16 operand rows in (2 L NP) + fp32 slot partials out "
                                       f"(4 S L NP, S={S})",
             "source": p,
-            "tensor_pipe_active_pct": value(
-                d["TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"]),
+            # the SM-clock counter (the "realtime" triage counter reads low for short launches:
+            # cfg 2 17% against 60% on the SM clock)
+            "tensor_pipe_active_pct": value(d["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]
+                                            if "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed" in d
+                                            else d["TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime"
+                                                   ".avg.pct_of_peak_sustained_elapsed"]),
             "tensor_memory_active_pct": value(d["sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"])
             if "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed" in d else None,
         }
