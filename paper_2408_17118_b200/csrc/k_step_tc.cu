@@ -25,6 +25,11 @@
 // Layout (NP <= 128, MT = 128):  TMEM  [W_hi NP/2 | (W_lo NP/2) | G NP | Y0 128 | Y1 128]
 //                                 SMEM  X stages [NP][128] fp16, 128B-swizzled (2 TMA boxes)
 //   (variant RG = 0: 4 Y slots of 64 samples, [NP][64] stages; kept for A/B timing)
+// Layout (NP <= 64, MT = 64, release): TMEM [W_hi | (W_lo) | G | Y0 64 | Y1 64] in a 256-column
+//   allocation, [NP][64] stages, ~70 KB of SMEM: two CTAs per SM.
+// Every layout computes bitwise the same partials: split parts cut slots at multiples of 384
+// samples (whole chunks of every width), and a fine tile's GEMM2 runs its y^3 and residual
+// passes per 64-sample group, so the fp32 accumulation order does not depend on the chunk width.
 // Layout (NP > 128, MT = 64):    TMEM  [W_hi <=128 | G NP | Y0 64 | Y1 64]
 //                                 SMEM  (W_lo [128][NP], K-major SW128 boxes) + X stages [NP][64]
 // (W_lo parts only in the LO-capable instantiation, launched when the list has fine rows.)
@@ -241,6 +246,8 @@ struct Cfg {
   static constexpr bool WLO_SMEM = SPLIT && WIDE;                // W_lo as an SMEM A operand
   // RG = 3 (NP <= 64): 2 slots of 192 samples -- more tensor work per chunk hand-off where the
   // narrow MMAs are short (the hand-offs, not the MMAs, pace small NP)
+  // RG = 7 (NP <= 64): 2 slots of 64 samples in a 256-column TMEM allocation and ~70 KB of
+  // shared memory, so TWO CTAs share an SM (two hand-off chains interleave on the tensor pipe)
   static constexpr int MT = WIDE ? 64 : RG == 1 ? 128 : RG == 3 ? 192 : 64;   // samples per chunk (GEMM1 N)
   // epilogue warps (one per TMEM lane quadrant; the kernel also runs with two per quadrant, each
   // taking every other 32-column group)
@@ -258,12 +265,16 @@ struct Cfg {
   static constexpr int C_G = WLO_TMEM ? NP : (WIDE ? 128 : NP / 2);
   static constexpr int C_Y0 = C_G + NP;                          // slot b at C_Y0 + b * MT
   static_assert(C_Y0 + R * MT <= 512, "TMEM budget");
+  static constexpr int TCOLS = RG == 7 ? 256 : 512;             // TMEM columns allocated
+  static_assert(C_Y0 + R * MT <= TCOLS, "TMEM allocation");
   static constexpr int SMEM = 1024 + WLO_BYTES + STAGES * X_STAGE + 1024;
+  static constexpr int MINB = RG == 7 ? 2 : 1;                   // CTAs per SM
+  static_assert(MINB == 1 || SMEM * MINB <= 227 * 1024, "shared memory for MINB CTAs per SM");
 };
 
 // CL = cluster size sharing each X chunk (multicast); RG = Y-ring variant (Cfg)
 template <int NP, bool SPLIT, int EPI, int CL, int RG>
-__global__ void __launch_bounds__(Cfg<NP, SPLIT, RG>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg<NP, SPLIT, RG>::THREADS, Cfg<NP, SPLIT, RG>::MINB)
 k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWlo,
           const __half* __restrict__ Whi, const __half* __restrict__ Wlo, const int* __restrict__ act, int L_ub,
           int64_t M, int64_t slot_len,
@@ -312,8 +323,15 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   if ((tile - tile % CL) * 128 >= L_act) return;   // cluster-uniform: no barrier was touched
   const int row0 = tile * 128;
   const int64_t m_slot = (int64_t)s * slot_len;
-  const int nch_slot = (int)ceil_div(min(M, m_slot + slot_len) - m_slot, MT);
-  const int c_lo = (int)((int64_t)nch_slot * part / P), c_hi = (int)((int64_t)nch_slot * (part + 1) / P);
+  // parts split the slot at multiples of 384 samples (a multiple of every chunk width MT), so a
+  // part's samples -- and every fp32 partial -- are the same whichever layout runs the step
+  constexpr int kPartUnit = 384;
+  static_assert(kPartUnit % MT == 0, "part boundaries must be whole chunks");
+  const int len_slot = (int)(min(M, m_slot + slot_len) - m_slot);
+  const int nch_slot = (len_slot + MT - 1) / MT;
+  const int nu_slot = (len_slot + kPartUnit - 1) / kPartUnit;
+  const int c_lo = nu_slot * part / P * (kPartUnit / MT);
+  const int c_hi = part + 1 == P ? nch_slot : nu_slot * (part + 1) / P * (kPartUnit / MT);
   const int64_t m_begin = m_slot + (int64_t)c_lo * MT;
   const int nchunk = c_hi - c_lo;
   // idle: the empty partner tile of a cluster (rows >= L_act) only streams its share of the
@@ -340,7 +358,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512));
+                 "r"(C::TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -440,15 +458,24 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       if (elect_one()) {
         const uint64_t bk = dk0 + (uint64_t)((st * C::X_STAGE) >> 4);
         const uint32_t t_y3 = tmem + C::C_Y0 + b * MT;
+        // per 64-sample group: the y^3 pass, then (fine tile) the pass on its fp16 residual
+        // (columns 32g+16..) -- the accumulation order is then the same for every chunk width
 #pragma unroll
-        for (int kk = 0; kk < MT / 16; ++kk)
-          mma_ts(t_g, t_y3 + (kk >> 1) * 32 + (kk & 1) * 8, bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2,
-                 (j > 0 || kk > 0) ? 1u : 0u);
-        if (lo_pass) {   // fine tile: second GEMM2 pass on the y^3 residual (columns 32g+16..)
+        for (int g64 = 0; g64 < MT / 64; ++g64) {
 #pragma unroll
-          for (int kk = 0; kk < MT / 16; ++kk)
-            mma_ts(t_g, t_y3 + (kk >> 1) * 32 + 16 + (kk & 1) * 8,
-                   bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2, 1u);
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int kk = 4 * g64 + k4;
+            mma_ts(t_g, t_y3 + (kk >> 1) * 32 + (kk & 1) * 8,
+                   bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          if (lo_pass) {
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int kk = 4 * g64 + k4;
+              mma_ts(t_g, t_y3 + (kk >> 1) * 32 + 16 + (kk & 1) * 8,
+                     bk + (uint64_t)(((kk >> 2) * C::XB + (kk & 3) * 32) >> 4), id2, 1u);
+            }
+          }
         }
         if (CL > 1)
           tc_commit_mc(&empty[st], kMask);
@@ -633,7 +660,7 @@ k_step_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   else
     __syncthreads();
   tc_fence_after();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
 }
 
 // ------------------------------------------------------------------ host side
@@ -727,7 +754,8 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
 }
 
 // Release build: the measured-best layout per NP --
-//   NP <= 64        2 Y slots of 192 samples, no cluster (latency-bound chunk hand-offs);
+//   NP <= 64        2 Y slots of 192 samples, no cluster (latency-bound chunk hand-offs); few
+//                   units: 2 Y slots of 64 samples in 256 TMEM columns, two CTAs per SM;
 //   64 < NP <= 128  2 Y slots of 128 samples, 2-CTA multicast clusters;
 //   NP > 128        wide layout (2 Y slots of 64 samples), 2-CTA multicast clusters;
 // one remaining row tile (the tail of a component) launches without a cluster partner, whose
@@ -735,12 +763,22 @@ void launch_cl(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const 
 // -DOICA_EXPERIMENTS adds the timing variants of profiles/r01/tc_experiments (OICA_TC_EPI
 // modes 3-8 that skip work, OICA_TC_CL = 1|2|4 and OICA_TC_RING overrides); they are compiled
 // out of the product library so no environment variable can change what the timed step does.
+// NP <= 64: launches of at most this many (row tile, slot) units -- the tail of a component, small
+// L (cfg 1) -- take the two-CTAs-per-SM layout (RG 7); more units the 192-sample layout (RG 3).
+// Measured over eight components (scripts/ab_step.py, step TFLOP/s): cfg 1 80.8 (RG 3 always) ->
+// 90.8; cfg 2 995 -> 1009; RG 7 for every launch: cfg 1 90.3, cfg 2 1021 eager but 2% slower in
+// the device-side loop, and a full-L N = 32 launch 4% slower
+constexpr int kRg7Units = 2 * 296;
+
 template <int NP, bool SPLIT, int EPI>
 void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, const __half* Whi, const __half* Wlo,
                     const int* act, int L_act, int64_t slot_len, int S, float* Gp, int64_t cap, int n_coarse, const int* cnt,
                     const Upload& up, const SplitOut& so, const int8_t* xshift) {
   constexpr int CL2 = (NP / 2) % 8 == 0 ? 2 : 1;
-  constexpr int RGN = NP <= 64 ? 3 : NP <= 128 ? 1 : 0;   // release Y-ring layout for this NP
+  // release layout for this NP (bitwise the same arithmetic): NP <= 64 2 x 192-sample slots at
+  // one CTA per SM for launches of more than kRg7Units (row tile, slot) units, else 2 x 64 at two
+  // CTAs per SM; 64 < NP <= 128 2 x 128-sample slots; wide 2 x 64
+  constexpr int RGN = NP <= 64 ? 7 : NP <= 128 ? 1 : 0;
 #ifdef OICA_EXPERIMENTS
   static int cl_env = [] { const char* e = getenv("OICA_TC_CL"); return e ? atoi(e) : 0; }();
   static int ring = [] { const char* e = getenv("OICA_TC_RING"); return e ? atoi(e) : 0; }();
@@ -758,13 +796,28 @@ void launch_variant(cudaStream_t st, const __half* Xh, int64_t ldx, int64_t M, c
       launch_cl<NP, SPLIT, EPI, 1, 0>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
     return;
   }
+  if constexpr (NP <= 64) {   // two CTAs per SM (2 x 64-sample slots, 256 TMEM columns)
+    if (ring == 24) {
+      launch_cl<NP, SPLIT, EPI, 1, 7>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+      return;
+    }
+  }
   if (NP <= 64 && ring == 2) {   // small NP with 2 x 128-sample slots
     launch_cl<NP, SPLIT, EPI, 1, 1>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
     return;
   }
+  static int rg7_units = [] { const char* e = getenv("OICA_TC_RG7_UNITS"); return e ? atoi(e) : kRg7Units; }();
 #else
   const int cl = up.cl ? up.cl : (NP > 64 && L_act > 128 ? 2 : 1);
+  constexpr int rg7_units = kRg7Units;
 #endif
+  if constexpr (NP <= 64) {
+    // many work units (full L): 2 x 192-sample slots, one CTA per SM
+    if ((int64_t)ceil_div(L_act, 128) * S > rg7_units) {
+      launch_cl<NP, SPLIT, EPI, 1, 3>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
+      return;
+    }
+  }
   if (NP > 64 && cl == 2)
     launch_cl<NP, SPLIT, EPI, CL2, RGN>(st, Xh, ldx, M, Whi, Wlo, act, L_act, slot_len, S, Gp, cap, n_coarse, cnt, up, so, xshift);
   else
