@@ -105,6 +105,36 @@ __global__ void __launch_bounds__(512) k_update(UpdateArgs u) {
   if (threadIdx.x == 0) finish_iteration(u, r, L_in, t);
 }
 
+// K3 + K4 for few rows (L_ub <= kUpdateCoopRows, the tail of a component): one block of 16 warps
+// per row, the row's slot values loaded by all warps at once into shared memory and summed in slot
+// order (update_row_coop: bitwise k_update's G -- in k_update the row's NG warps walk the S
+// slots x P split parts themselves, a chain of S/2 dependent L2 round trips per row), then the
+// block that finishes last compacts.
+template <int NG>
+__global__ void __launch_bounds__(512) k_update_coop(UpdateArgs u) {
+  extern __shared__ double T[];   // [S][NG * 32]
+  __shared__ double gsh[1][NG * 32];
+  __shared__ double s4sh[1];
+  __shared__ int s_last;
+  const int t = u.ctl->t, k = u.ctl->k;
+  const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
+  upd::update_row_coop<NG>(u, blockIdx.x, L_in, t, k, T, gsh, s4sh);
+  if (threadIdx.x == 0) {   // completion ticket: the last block sees every row's keep / fine / state
+    __threadfence();
+    const unsigned tk = atomicAdd(&u.ctl->done, 1u);
+    s_last = tk == gridDim.x - 1 ? 1 : 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int2 r = compact_block(u.act_in, u.keep, u.pr.fine, L_in, u.act_out);   // K4
+  if (u.copy_back) {
+    int* dst = const_cast<int*>(u.act_in);
+    for (int j = threadIdx.x; j < r.x; j += blockDim.x) dst[j] = u.act_out[j];
+  }
+  if (threadIdx.x == 0) finish_iteration(u, r, L_in, t);
+}
+
 // K3 for many rows (L_ub > kUpdateCompactRows: the HBM-bound regime, where occupancy and not the
 // latency of one row matters): one warp per row with V coordinates per lane (slot sums in the same
 // sequential order as k_update), 8 rows per block; keep[] for k_compact_iter.
@@ -324,6 +354,32 @@ int launch_update(cudaStream_t st, const UpdateArgs& u, int NP) {
       f ? k_update_rows<4, true><<<nbr, 256, 0, st>>>(u) : k_update_rows<4, false><<<nbr, 256, 0, st>>>(u);
     else
       f ? k_update_rows<8, true><<<nbr, 256, 0, st>>>(u) : k_update_rows<8, false><<<nbr, 256, 0, st>>>(u);
+    return 1;
+  }
+  const size_t coop_smem = sizeof(double) * (size_t)u.S * (size_t)NG * 32;
+  if (u.L_ub <= kUpdateCoopRows && coop_smem <= kUpdateCoopSmem) {   // few rows: one block per row
+    static bool attr_set[9] = {};
+#define OICA_UPDC(g)                                                                             \
+  case g:                                                                                        \
+    if (!attr_set[g]) {                                                                          \
+      OICA_CUDA(cudaFuncSetAttribute(k_update_coop<g>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)kUpdateCoopSmem));                                     \
+      attr_set[g] = true;                                                                        \
+    }                                                                                            \
+    k_update_coop<g><<<(unsigned)u.L_ub, 512, coop_smem, st>>>(u);                              \
+    break;
+    switch (NG) {
+      OICA_UPDC(1)
+      OICA_UPDC(2)
+      OICA_UPDC(3)
+      OICA_UPDC(4)
+      OICA_UPDC(5)
+      OICA_UPDC(6)
+      OICA_UPDC(7)
+      OICA_UPDC(8)
+      default: throw Error(OICA_ERR_INVALID_ARGUMENT, "unsupported padded N for the update");
+    }
+#undef OICA_UPDC
     return 1;
   }
   const unsigned nb = (unsigned)update_blocks(u.L_ub, NP);

@@ -140,6 +140,12 @@ struct UpdateArgs {
 // launch_update compacts inside (last block) up to this many upper-bound rows; above, one warp per
 // row updates (the HBM-bound regime) and launch_compact_iter compacts
 constexpr int kUpdateCompactRows = 2048;
+// ... and up to this many upper-bound rows one block per row (k_update_coop) while the row's slot
+// values fit this much shared memory (S x NP x 8 bytes).  Measured: cfg 2 all components 136.7 ->
+// 127.0 ms, cfg 1 22.6 -> 20.6 ms; with 2048 rows cfg 1 takes 33 ms (512-thread blocks with large
+// shared memory for every mid-size iteration)
+constexpr int kUpdateCoopRows = 128;
+constexpr size_t kUpdateCoopSmem = 96 * 1024;
 int launch_update(cudaStream_t st, const UpdateArgs& u, int NP);
 // after launch_update with compact = 0: the compaction and the end of the iteration
 int launch_compact_iter(cudaStream_t st, const UpdateArgs& u);

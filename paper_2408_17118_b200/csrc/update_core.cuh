@@ -376,18 +376,18 @@ __device__ __forceinline__ void update_pass(const UpdateArgs& u, int a_base, int
   }
 }
 
-// One row a of the few-row update with the whole block (8 warps) on its slot partials (fp64
-// partials, no split parts; S * NP * 8 bytes of shared memory T): the warps load the S slots'
-// partials of the row into T in parallel, then warp g sums coordinates g*32 + lane over the slots
-// in slot order from T -- the same sequential association as slot_sum -- and warp 0 runs
-// epilogue_core.  Every thread of the block must call it.  keep[a] is written.
+// One row a of the few-row update with the whole block on its slot partials (S * NP * 8 bytes of
+// shared memory T): the warps load the S slots' values of the row into T in parallel (slot_part:
+// the fp64 or fp32 partial, or the fp64 sum of a slot's split parts in part order), then warp g
+// sums coordinates g*32 + lane over the slots in slot order from T -- the same sequential
+// association as slot_sum -- and warp 0 runs epilogue_core.  Every thread of the block must call
+// it.  keep[a] is written.
 template <int NG>
 __device__ __forceinline__ void update_row_coop(const UpdateArgs& u, int a, int L_in, int t, int k, double* T,
                                                 double (*gsh)[NG * 32], double* s4sh) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int NPd = NG * 32;
-  const double* G = (const double*)u.G.p;
-  const int64_t st = u.cap * u.ldg;
+  const int P = parts_of(u.G, u.S);
   int l = 0;
   double wo[NG], we[NG];
   if (a < L_in) {
@@ -397,7 +397,7 @@ __device__ __forceinline__ void update_row_coop(const UpdateArgs& u, int a, int 
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
         const int n = g * 32 + lane;
-        T[s * NPd + n] = n < u.N ? __ldg(G + s * st + (int64_t)a * u.ldg + n) : 0.0;
+        T[s * NPd + n] = n < u.N ? slot_part(u.G, P, s, u.cap, u.ldg, a, n) : 0.0;
       }
     }
   }
