@@ -279,6 +279,17 @@ def run_reference(args, cfg):
     print(json.dumps(out), flush=True)
 
 
+def fp32_peak():
+    """Best measured FFMA throughput (scripts/fp32_peak.cu) with its clock, or None."""
+    path = os.path.join(ROOT, "profiles", "r02", "microbench", "fp32_peak.jsonl")
+    try:
+        recs = [json.loads(l) for l in open(path) if l.strip()]
+        recs = [r for r in recs if r.get("max_sm_mhz")]
+        return max(recs, key=lambda r: r["tflops"]) if recs else None
+    except (OSError, ValueError):
+        return None
+
+
 def run_oica(args, cfg):
     import numpy as np
     import torch
@@ -478,8 +489,15 @@ def run_oica(args, cfg):
                                "issued_frac = issued (128-row tiles x padded N, all passes) / peak"}
     else:
         mhz = clocks.get("sm_mhz") or peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1357.0)
-        peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
-        roof = {"bound": "alu", "peak_source": f"148 SMs x 128 FP32 lanes x 2 flop x {mhz:.0f} MHz (median SM clock under load)"}
+        fp = fp32_peak()
+        if fp:   # measured FFMA throughput (scripts/fp32_peak.cu) scaled to the sampled clock
+            peak = fp["tflops"] * mhz / fp["max_sm_mhz"]
+            roof = {"bound": "alu", "peak_source": f"measured FP32 FFMA peak {fp['tflops']:.1f} TFLOP/s at "
+                                                   f"{fp['max_sm_mhz']:.0f} MHz (profiles/r02/microbench/fp32_peak.jsonl) "
+                                                   f"scaled to {mhz:.0f} MHz (median SM clock under load)"}
+        else:
+            peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+            roof = {"bound": "alu", "peak_source": f"148 SMs x 128 FP32 lanes x 2 flop x {mhz:.0f} MHz (median SM clock under load)"}
     tr = load_traffic(cfg.name, precision)
     roof.update({"achieved": kern_tflops, "peak": peak, "unit": "TFLOP/s",
                  "frac": (kern_tflops / peak) if kern_tflops else None,

@@ -1,5 +1,6 @@
 // Host runtime and C-ABI of liboica.so: context, memory planner, per-component driver loop,
 // NCCL exchange, whitening eigensolver.  Kernels live in k_*.cu (launch wrappers in kernels.cuh).
+#include <nvtx3/nvToolsExt.h>
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -773,11 +774,41 @@ void account_iteration(oica_ctx* c, int L_act, int n_coarse, int64_t M_work = -1
 void check_launch() { OICA_CUDA(cudaGetLastError()); }
 
 // OICA_TRACE=1: per-component host wall-clock phases on stderr (development aid)
+// Per-component phase trace: NVTX ranges (component i > a1 draw / a2-a6 iterate / a7 select /
+// accept; no-ops unless a profiler is attached) and, with OICA_TRACE, host timings on stderr.
 struct PhaseTrace {
   bool on = getenv("OICA_TRACE") != nullptr;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   std::string line;
+  int depth = 0;   // open NVTX ranges
+  void push(const char* name) {
+    nvtxRangePushA(name);
+    ++depth;
+  }
+  void pop() {
+    if (depth > 0) {
+      nvtxRangePop();
+      --depth;
+    }
+  }
+  void begin(int i) {
+    while (depth > 0) pop();
+    push(("oica component " + std::to_string(i)).c_str());
+    push("a1 draw (P:237-239)");
+  }
+  ~PhaseTrace() {
+    while (depth > 0) pop();
+  }
   void mark(const char* what) {
+    // `what` ended; the next phase's range opens
+    const std::string w(what);
+    pop();
+    if (w == "init")
+      push("a2-a6 iterate (P:241-256)");
+    else if (w == "iterate")
+      push("a7 select (P:257-259)");
+    else if (w == "select")
+      push("accept (P:264)");
     if (!on) return;
     auto t1 = std::chrono::steady_clock::now();
     line += std::string(" ") + what + "=" +
@@ -803,6 +834,7 @@ struct PhaseTrace {
     ++batches;
   }
   void flush(int i) {
+    while (depth > 0) pop();
     if (on)
       fprintf(stderr, "[oica] component %d:%s (iterate: %d batches, enqueue %.0fus, wait %.0fus)\n", i, line.c_str(),
               batches, enq_us, wait_us);
@@ -1310,6 +1342,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
   PhaseTrace trace;
   for (int k = k_prefix; k < N_out; ++k) {
     const int i = k + 1;  // 1-based component index
+    trace.begin(i);
     // Alg. 2 lines 4-12: iterate on X~ = G X in the d = N - k dimensional complement
     if (reduce && k > 0)
       use_reduced_view(c, N - k);
