@@ -133,6 +133,37 @@ def test_step_mixed_precision_tile_independent(name, boundary):
     assert ef < 0.5 * ec, (ef, ec)
 
 
+@pytest.mark.parametrize("N", [32, 64])
+def test_step_layouts_bitwise(N):
+    """NP <= 64 launches take one of two step layouts by their unit count (192-sample
+    chunks at one CTA per SM above 592 (row tile, slot) units, 64-sample chunks at two CTAs per SM
+    below); a row's partials are the same in both (same samples per slot, same accumulation order,
+    the fine passes per 64-sample group).  The first 640 rows of a 4096-row step (5 tiles x 29 slots
+    = 145 units: the small layout; no split parts, P = 1 in both) equal the same rows of the large
+    step bitwise, coarse and all-fine."""
+    M, Lb, Ls = 100_000, 4096, 640
+    g = np.random.default_rng(N)
+    X = torch.from_numpy((g.laplace(size=(N, M)) / np.sqrt(2.0)).astype(np.float32)).cuda()
+    W = rng.candidates(13, 1, np.arange(Lb), N)
+    W /= np.linalg.norm(W, axis=1, keepdims=True)
+    S = oica.slot_plan(M)[1]
+    assert ((Ls + 127) // 128) * S <= 592 < ((Lb + 127) // 128) * S   # the two layouts
+    assert oica.split_parts(Ls, S) == 1 and oica.split_parts(Lb, S) == 1
+    for fine_all in (False, True):
+        outs = []
+        for L in (Lb, Ls):
+            with oica.Context(0, oica.PREC_TC) as ctx:
+                ctx.set_data(X)
+                ctx.init_candidates(1, L)
+                G = torch.zeros(L, N, dtype=torch.float64, device="cuda")
+                s4 = torch.zeros(L, dtype=torch.float64, device="cuda")
+                ctx.fixed_point_step(torch.from_numpy(W[:L]).cuda(), G, s4,
+                                     fine=np.ones(L, np.uint8) if fine_all else None)
+                outs.append((G.cpu().numpy(), s4.cpu().numpy()))
+        assert np.array_equal(outs[0][0][:Ls], outs[1][0]), fine_all
+        assert np.array_equal(outs[0][1][:Ls], outs[1][1]), fine_all
+
+
 @pytest.mark.parametrize("name,flags", [("p_tc_n128", 0), ("p_n40", 0), ("p_tc_n128", oica.REDUCE_X),
                                         ("p_tc_n128", oica.EAGER), ("p_n40", oica.EAGER)])
 def test_iteration_log(name, flags):
