@@ -4,6 +4,8 @@
 
 #include <algorithm>
 
+#include <atomic>
+
 #include "kernels.cuh"
 #include "update_core.cuh"
 
@@ -358,13 +360,17 @@ int launch_update(cudaStream_t st, const UpdateArgs& u, int NP) {
   }
   const size_t coop_smem = sizeof(double) * (size_t)u.S * (size_t)NG * 32;
   if (u.L_ub <= kUpdateCoopRows && coop_smem <= kUpdateCoopSmem) {   // few rows: one block per row
-    static bool attr_set[9] = {};
+    // the shared-memory opt-in is a per-device function attribute: set once per (device, NG)
+    static std::atomic<uint64_t> attr_set[9];
+    int dev = 0;
+    OICA_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
 #define OICA_UPDC(g)                                                                             \
   case g:                                                                                        \
-    if (!attr_set[g]) {                                                                          \
+    if (!(attr_set[g].load() & bit)) {                                                           \
       OICA_CUDA(cudaFuncSetAttribute(k_update_coop<g>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      (int)kUpdateCoopSmem));                                     \
-      attr_set[g] = true;                                                                        \
+      attr_set[g].fetch_or(bit);                                                                 \
     }                                                                                            \
     k_update_coop<g><<<(unsigned)u.L_ub, 512, coop_smem, st>>>(u);                              \
     break;
