@@ -179,14 +179,20 @@ struct oica_ctx {
       valid = false;
     }
   } loop;
-  cudaEvent_t loop_ev0 = nullptr, loop_ev1 = nullptr;
+  // device-side loop timing, one pair per component slot (two components in flight, extract_impl)
+  cudaEvent_t loop_ev0[2] = {nullptr, nullptr}, loop_ev1[2] = {nullptr, nullptr};
+  int slot = 0;   // the component slot being enqueued
+  cudaEvent_t comp_ev[2] = {nullptr, nullptr};   // a component slot's record copied to the host
   bool loop_persistent = false;   // the last device-side loop was the persistent FP32 kernel
   // pinned read-back of a component's results (one host wait per component on the fast path):
   // [ComponentRecord | IterCtl | w (256 doubles) | hist (2 (K + 1) ints)]
   char* pin = nullptr;
   size_t pin_bytes = 0;
+  // two slots: the next component is enqueued before the host reads this one's record
+  size_t pin_slot = 0;
   void ensure_pin(int K) {
-    const size_t need = sizeof(ComponentRecord) + sizeof(IterCtl) + 256 * sizeof(double) + 2 * ((size_t)K + 1) * sizeof(int);
+    pin_slot = round_up(sizeof(ComponentRecord) + sizeof(IterCtl) + 256 * sizeof(double) + 2 * ((size_t)K + 1) * sizeof(int), 256);
+    const size_t need = 2 * pin_slot;
     if (need <= pin_bytes) return;
     if (pin) cudaFreeHost(pin);
     pin = nullptr;
@@ -194,10 +200,11 @@ struct oica_ctx {
     OICA_CUDA(cudaHostAlloc((void**)&pin, need, cudaHostAllocDefault));
     pin_bytes = need;
   }
-  ComponentRecord* pin_rec() { return (ComponentRecord*)pin; }
-  IterCtl* pin_ctl() { return (IterCtl*)(pin + sizeof(ComponentRecord)); }
-  double* pin_w() { return (double*)(pin + sizeof(ComponentRecord) + sizeof(IterCtl)); }
-  int* pin_hist() { return (int*)(pin + sizeof(ComponentRecord) + sizeof(IterCtl) + 256 * sizeof(double)); }
+  char* pin_at(int j) { return pin + (size_t)j * pin_slot; }
+  ComponentRecord* pin_rec(int j) { return (ComponentRecord*)pin_at(j); }
+  IterCtl* pin_ctl(int j) { return (IterCtl*)(pin_at(j) + sizeof(ComponentRecord)); }
+  double* pin_w(int j) { return (double*)(pin_at(j) + sizeof(ComponentRecord) + sizeof(IterCtl)); }
+  int* pin_hist(int j) { return (int*)(pin_at(j) + sizeof(ComponentRecord) + sizeof(IterCtl) + 256 * sizeof(double)); }
   // the data the current component iterates on (DESIGN.md §5 "reduced X"): the full whitened X,
   // or X~ = G X in the d = N-k dimensional complement of the accepted rows (OICA_REDUCE_X)
   const float* vX = nullptr;
@@ -780,7 +787,9 @@ struct PhaseTrace {
   bool on = getenv("OICA_TRACE") != nullptr;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   std::string line;
-  int depth = 0;   // open NVTX ranges
+  int depth = 0;        // open NVTX ranges
+  bool phases = true;   // phase ranges (false when components are enqueued one ahead: one range per
+                        // component's enqueue)
   void push(const char* name) {
     nvtxRangePushA(name);
     ++depth;
@@ -794,21 +803,26 @@ struct PhaseTrace {
   void begin(int i) {
     while (depth > 0) pop();
     push(("oica component " + std::to_string(i)).c_str());
-    push("a1 draw (P:237-239)");
+    if (phases) push("a1 draw (P:237-239)");
+  }
+  void end() {
+    while (depth > 0) pop();
   }
   ~PhaseTrace() {
     while (depth > 0) pop();
   }
   void mark(const char* what) {
     // `what` ended; the next phase's range opens
-    const std::string w(what);
-    pop();
-    if (w == "init")
-      push("a2-a6 iterate (P:241-256)");
-    else if (w == "iterate")
-      push("a7 select (P:257-259)");
-    else if (w == "select")
-      push("accept (P:264)");
+    if (phases) {
+      const std::string w(what);
+      pop();
+      if (w == "init")
+        push("a2-a6 iterate (P:241-256)");
+      else if (w == "iterate")
+        push("a7 select (P:257-259)");
+      else if (w == "select")
+        push("accept (P:264)");
+    }
     if (!on) return;
     auto t1 = std::chrono::steady_clock::now();
     line += std::string(" ") + what + "=" +
@@ -1164,6 +1178,19 @@ int64_t run_hybrid_tail(oica_ctx* c, const int* act, int L_local, const std::vec
 // host wait) per component instead of a host round trip per batch of iterations; the kernels are
 // those of the host-launched loop with the same upper-bound sizing, so results are bitwise equal
 // (tests/test_gpu_parity.py::test_device_loop_bitwise).  Enqueues only (no host wait).
+// Host wait for one event of the context's stream (single rank: no NCCL state to poll)
+void wait_event(oica_ctx* c, cudaEvent_t ev) {
+  (void)c;
+  OICA_CUDA(cudaEventSynchronize(ev));
+}
+
+void ensure_loop_events(oica_ctx* c) {
+  if (!c->loop_ev0[c->slot]) {
+    OICA_CUDA(cudaEventCreate(&c->loop_ev0[c->slot]));
+    OICA_CUDA(cudaEventCreate(&c->loop_ev1[c->slot]));
+  }
+}
+
 void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
   cudaStream_t st = c->st;
   c->loop_persistent = false;
@@ -1237,19 +1264,16 @@ void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
     c->loop.key = key;
     c->loop.valid = true;
   }
-  if (!c->loop_ev0) {
-    OICA_CUDA(cudaEventCreate(&c->loop_ev0));
-    OICA_CUDA(cudaEventCreate(&c->loop_ev1));
-  }
-  OICA_CUDA(cudaEventRecord(c->loop_ev0, st));
+  ensure_loop_events(c);
+  OICA_CUDA(cudaEventRecord(c->loop_ev0[c->slot], st));
   OICA_CUDA(cudaGraphLaunch(c->loop.x, st));
-  OICA_CUDA(cudaEventRecord(c->loop_ev1, st));
+  OICA_CUDA(cudaEventRecord(c->loop_ev1[c->slot], st));
 }
 
 // counters of a finished device-side loop of `iters` iterations (after the host wait)
-void finish_loop_graph(oica_ctx* c, int iters) {
+void finish_loop_graph(oica_ctx* c, int iters, int slot) {
   float ms = 0.f;
-  OICA_CUDA(cudaEventElapsedTime(&ms, c->loop_ev0, c->loop_ev1));
+  OICA_CUDA(cudaEventElapsedTime(&ms, c->loop_ev0[slot], c->loop_ev1[slot]));
   c->stats.graph_ms += ms;
   if (c->loop_persistent) {
     c->count(1);
@@ -1269,17 +1293,14 @@ bool persistent_loop_ok(const oica_ctx* c) {
 
 void enqueue_loop_simt(oica_ctx* c, int K, double tol) {
   cudaStream_t st = c->st;
-  if (!c->loop_ev0) {
-    OICA_CUDA(cudaEventCreate(&c->loop_ev0));
-    OICA_CUDA(cudaEventCreate(&c->loop_ev1));
-  }
+  ensure_loop_events(c);
   UpdateArgs u = update_args(c, SlotPartials{c->Gp.p, false}, c->s4p.p, c->S, c->Ll, c->act0.p, c->act1.p, (int)c->Ll,
                              tol, c->hist.p);
   u.copy_back = 1;
-  OICA_CUDA(cudaEventRecord(c->loop_ev0, st));
+  OICA_CUDA(cudaEventRecord(c->loop_ev0[c->slot], st));
   launch_loop_simt(st, c->vX, c->vld, c->M, c->slot_len, c->S, kFlush, K, u, c->vNP, c->num_sms);
   check_launch();
-  OICA_CUDA(cudaEventRecord(c->loop_ev1, st));
+  OICA_CUDA(cudaEventRecord(c->loop_ev1[c->slot], st));
   c->loop_persistent = true;
 }
 
@@ -1340,9 +1361,28 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
   use_full_view(c);
   c->iter_log.clear();
   PhaseTrace trace;
-  for (int k = k_prefix; k < N_out; ++k) {
+  // Components are enqueued one ahead where nothing the host computes feeds the next one (the
+  // device-side loop on one rank, no reduction, no Gaussianity stop): the GPU runs component k+1
+  // while the host reads component k's record from its pinned slot, instead of idling between
+  // components.  Elsewhere each component is finished before the next is enqueued.
+  struct Comp {
+    int k = 0, slot = 0;
+    bool fast = false;
+    int t = 0;
+    std::vector<std::pair<int, int>> rows_at;
+  };
+  const bool ahead = !reduce && !(flags & OICA_STOP_ON_GAUSSIANITY) && !c->collective() && !(flags & OICA_EAGER) &&
+                     (double)c->M * (double)c->vNP < kBatchMaxWork;
+  trace.phases = !ahead;
+  c->ensure_pin(K);
+  for (int j = 0; j < 2; ++j)
+    if (!c->comp_ev[j]) OICA_CUDA(cudaEventCreateWithFlags(&c->comp_ev[j], cudaEventDisableTiming));
+  auto enqueue = [&](int k, Comp& cp) {
     const int i = k + 1;  // 1-based component index
+    cp.k = k;
     trace.begin(i);
+    const int j = cp.slot;
+    c->slot = j;
     // Alg. 2 lines 4-12: iterate on X~ = G X in the d = N - k dimensional complement
     if (reduce && k > 0)
       use_reduced_view(c, N - k);
@@ -1362,6 +1402,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     // trip and its counters are read back once at the end (DESIGN.md §5 "iteration")
     const bool fast = !c->collective() && !c->reduced && !(flags & OICA_EAGER) &&
                       (double)c->M * (double)c->vNP < kBatchMaxWork;
+    cp.fast = fast;
     c->count(launch_compact(st, nullptr, c->keep.p, c->fine_flags(), (int)c->Ll, c->act0.p, c->Lact_dev.p,
                             c->Lact_host, nullptr, c->hist.p));   // hist[0..1]: runs entering iteration 1
     OICA_CUDA(cudaMemsetAsync(c->nonfinite.p, 0, sizeof(int), st));
@@ -1531,27 +1572,41 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
                                  c->reduced ? c->Wacc_scratch.p : c->Wacc.p, c->reduced ? 0 : k, c->rec.p,
                                  c->w_out.p));
     check_launch();
-    c->ensure_pin(K);
-    OICA_CUDA(cudaMemcpyAsync(c->pin_rec(), c->rec.p, sizeof(ComponentRecord), cudaMemcpyDeviceToHost, st));
-    OICA_CUDA(cudaMemcpyAsync(c->pin_w(), c->w_out.p, sizeof(double) * vN, cudaMemcpyDeviceToHost, st));
+    OICA_CUDA(cudaMemcpyAsync(c->pin_rec(j), c->rec.p, sizeof(ComponentRecord), cudaMemcpyDeviceToHost, st));
+    OICA_CUDA(cudaMemcpyAsync(c->pin_w(j), c->w_out.p, sizeof(double) * vN, cudaMemcpyDeviceToHost, st));
     if (fast) {
-      OICA_CUDA(cudaMemcpyAsync(c->pin_ctl(), c->ctl.p, sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
-      OICA_CUDA(cudaMemcpyAsync(c->pin_hist(), c->hist.p, sizeof(int) * 2 * ((size_t)K + 1), cudaMemcpyDeviceToHost,
+      OICA_CUDA(cudaMemcpyAsync(c->pin_ctl(j), c->ctl.p, sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
+      OICA_CUDA(cudaMemcpyAsync(c->pin_hist(j), c->hist.p, sizeof(int) * 2 * ((size_t)K + 1), cudaMemcpyDeviceToHost,
                                 st));
     }
-    c->harvest_events();   // the component's one host wait on the fast path
-    rec_h = *c->pin_rec();
-    std::copy(c->pin_w(), c->pin_w() + vN, b_host.begin());
+    OICA_CUDA(cudaEventRecord(c->comp_ev[j], st));   // this component's record is in the pinned slot
+    cp.t = t;
+    cp.rows_at = std::move(rows_at);
+    if (ahead) trace.end();
+  };
+  // returns true where the Gaussianity test stops the extraction
+  auto finish = [&](Comp& cp) -> bool {
+    const int k = cp.k, i = k + 1, j = cp.slot;
+    const bool fast = cp.fast;
+    const int vN = c->vN;
+    int t = cp.t;
+    std::vector<std::pair<int, int>>& rows_at = cp.rows_at;
+    if (ahead)
+      wait_event(c, c->comp_ev[j]);   // (step / exchange events are read once, after the last component)
+    else
+      c->harvest_events();   // the component's one host wait on the fast path
+    rec_h = *c->pin_rec(j);
+    std::copy(c->pin_w(j), c->pin_w(j) + vN, b_host.begin());
     if (fast) {   // counters of the device-side loop
-      t = c->pin_ctl()->t - 1;
-      const int* hh = c->pin_hist();
+      t = c->pin_ctl(j)->t - 1;
+      const int* hh = c->pin_hist(j);
       for (int tt = 1; tt <= t; ++tt) {
         const int Lin = hh[2 * (tt - 1)], ncin = hh[2 * (tt - 1) + 1];
         if (Lin <= 0) break;
         account_iteration(c, Lin, ncin, -1, false);
         rows_at[tt] = {Lin, ncin};
       }
-      finish_loop_graph(c, t);
+      finish_loop_graph(c, t, j);
     }
     // per-iteration log: every executed iteration; step_ms from its launch's events, or -1 for the
     // iterations of the device-side loop (not timed one by one)
@@ -1620,11 +1675,33 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
     if (out->dim) out->dim[k] = vN;
     if (stop) {
       out->stopped = 1;
-      break;
+      return true;
     }
     out->n_extracted = k + 1;
     trace.mark("accept");
     trace.flush(i);
+    return false;
+  };
+  if (ahead) {
+    Comp cur, nxt;
+    cur.slot = 0;
+    enqueue(k_prefix, cur);
+    for (int k = k_prefix; k < N_out; ++k) {
+      if (k + 1 < N_out) {
+        nxt = Comp{};
+        nxt.slot = 1 - cur.slot;
+        enqueue(k + 1, nxt);
+      }
+      if (finish(cur)) break;
+      std::swap(cur, nxt);
+    }
+    c->harvest_events();
+  } else {
+    for (int k = k_prefix; k < N_out; ++k) {
+      Comp cp;
+      enqueue(k, cp);
+      if (finish(cp)) break;
+    }
   }
   use_full_view(c);
 }
@@ -1754,8 +1831,11 @@ oica_status oica_destroy(oica_ctx* c) {
     cudaEventDestroy(e.second);
   }
   c->loop.reset();
-  if (c->loop_ev0) cudaEventDestroy(c->loop_ev0);
-  if (c->loop_ev1) cudaEventDestroy(c->loop_ev1);
+  for (int j = 0; j < 2; ++j) {
+    if (c->loop_ev0[j]) cudaEventDestroy(c->loop_ev0[j]);
+    if (c->loop_ev1[j]) cudaEventDestroy(c->loop_ev1[j]);
+    if (c->comp_ev[j]) cudaEventDestroy(c->comp_ev[j]);
+  }
   if (c->pin) cudaFreeHost(c->pin);
   if (c->Lact_host) cudaFreeHost(c->Lact_host);
   if (c->cst) {
