@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(512) k_update(UpdateArgs u) {
   __shared__ double s4sh[RPB];
   __shared__ int s_keep[RPB];
   __shared__ int s_last;
+  if (u.gate_in && u.gate_in[0] == 0) return;   // grid-uniform (the writer is this kernel's last block)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = u.ctl->t, k = u.ctl->k;
   const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(512) k_update_coop(UpdateArgs u) {
   __shared__ double gsh[1][NG * 32];
   __shared__ double s4sh[1];
   __shared__ int s_last;
+  if (u.gate_in && u.gate_in[0] == 0) return;   // grid-uniform (the writer is this kernel's last block)
   const int t = u.ctl->t, k = u.ctl->k;
   const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
   upd::update_row_coop<NG>(u, blockIdx.x, L_in, t, k, T, gsh, s4sh);
@@ -144,6 +146,7 @@ template <int V, bool F32>
 __global__ void __launch_bounds__(256) k_update_rows(UpdateArgs u) {
   const int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
+  if (u.gate_in && u.gate_in[0] == 0) return;
   const int t = u.ctl->t, k = u.ctl->k;
   const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
   if (a >= L_in) return;
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(256) k_update_rows(UpdateArgs u) {
 // K4 for many rows after launch_update with compact = 0: one 1024-thread block scans the list
 // (k_compact's arithmetic) and ends the iteration like the update's last block would.
 __global__ void __launch_bounds__(1024) k_compact_iter(UpdateArgs u) {
+  if (u.gate_in && u.gate_in[0] == 0) return;   // (read by every thread before the barrier below)
   const int t = u.ctl->t;
   const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
   __syncthreads();   // every thread read cnt_in (may alias cnt_out) before thread 0 writes it

@@ -133,6 +133,12 @@ struct UpdateArgs {
   cudaGraphConditionalHandle loop_next;
   int loop_thr;
   int K_loop;
+  // loop bodies unrolled U times (one WHILE re-launch per U iterations): gate_out [2] = this
+  // tier's loop goes on ? (L_act, n_coarse) : (0, 0), written with the condition; gate_in (the
+  // 2nd..U-th copies of the body) = the previous copy's gate_out -- 0: the loop ended inside
+  // this body and the kernel returns at once (the copy's step reads the same gate as its count)
+  const int* gate_in;
+  int* gate_out;
   // 0: no compaction here (many rows: the caller launches k_compact, whose 1024 threads scan the
   // list faster than one block of the update could); keep[] and the row state are written
   int compact;

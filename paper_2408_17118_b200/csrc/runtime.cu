@@ -59,6 +59,7 @@ constexpr double kPromoteRatio = 0.3;       // ... (d > this * d_prev: stagnatin
 constexpr int kPromoteT = 40;               // ... or t >= this
 constexpr int kBatchRows = 2048;            // below this many active rows, iterations are enqueued ...
 constexpr int kBatch = 8;                   // ... this many at a time without a host round trip
+constexpr int kLoopUnroll = 4;             // iterations per WHILE-body execution (device-side loop)
 constexpr double kBatchMaxWork = 1e8;       // ... when M x NP is below this (cfg 2: 1.6e7, cfg 3: 1.3e8)
 constexpr int kHybridRowsPerRank = 128;     // OICA_SHARD_HYBRID: tail once global L_act <= this x world
 constexpr int kTailMaxSlots = 1024;
@@ -171,6 +172,8 @@ struct oica_ctx {
     LoopKey key{};
     cudaGraph_t g = nullptr;
     cudaGraphExec_t x = nullptr;
+    std::vector<int> tiers;   // grid-size tiers (rows) of the WHILE nodes, in order
+    int unroll = 1;           // iterations per body execution
     void reset() {
       if (x) cudaGraphExecDestroy(x);
       if (g) cudaGraphDestroy(g);
@@ -495,7 +498,7 @@ void ensure_candidate_buffers(oica_ctx* c) {
   c->keep.ensure(Ll);
   c->act0.ensure(Ll);
   c->act1.ensure(Ll);
-  c->Lact_dev.ensure(2);
+  c->Lact_dev.ensure(4);   // [L_act, n_coarse] + the unrolled loop body's gate (2)
   c->Lg.ensure(1);
   c->fine.ensure(Ll);
   c->dprev.ensure(Ll);
@@ -1191,6 +1194,16 @@ void ensure_loop_events(oica_ctx* c) {
   }
 }
 
+// iterations per WHILE-body execution of the device-side loop
+int loop_unroll() {
+  static const int u = [] {
+    const char* e = getenv("OICA_LOOP_UNROLL");
+    const int v = e ? atoi(e) : kLoopUnroll;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+  }();
+  return u;
+}
+
 void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
   cudaStream_t st = c->st;
   c->loop_persistent = false;
@@ -1240,17 +1253,25 @@ void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
       OICA_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
       try {
         const int* cnt = c->Lact_dev.p;
+        int* gate = c->Lact_dev.p + 2;
         const int Lt = tiers[i];
-        run_step(c, c->act0.p, Lt, std::min(nc_ub, Lt), cnt, cnt, c->tc() && !c->split(), false);
-        UpdateArgs u = update_args(c, c->partials(cnt, Lt), c->tc() ? nullptr : c->s4p.p, c->S, c->Ll, c->act0.p,
-                                   c->act1.p, Lt, tol, c->hist.p);
-        u.copy_back = 1;
-        u.loop = hs[i];
-        u.loop_next = i + 1 < nt ? hs[i + 1] : 0;
-        u.loop_thr = i + 1 < nt ? tiers[i + 1] : 0;
-        u.K_loop = K;
-        run_update(c, u);
-        check_launch();
+        // the body holds kLoopUnroll iterations (a WHILE re-launch costs ~3 us, measured by
+        // scripts/while_overhead.cu); copies after the first run only while the gate is open
+        for (int j = 0; j < loop_unroll(); ++j) {
+          const int* cs = j == 0 ? cnt : gate;
+          run_step(c, c->act0.p, Lt, std::min(nc_ub, Lt), cs, cs, c->tc() && !c->split(), false);
+          UpdateArgs u = update_args(c, c->partials(cnt, Lt), c->tc() ? nullptr : c->s4p.p, c->S, c->Ll, c->act0.p,
+                                     c->act1.p, Lt, tol, c->hist.p);
+          u.copy_back = 1;
+          u.loop = hs[i];
+          u.loop_next = i + 1 < nt ? hs[i + 1] : 0;
+          u.loop_thr = i + 1 < nt ? tiers[i + 1] : 0;
+          u.K_loop = K;
+          u.gate_in = j == 0 ? nullptr : gate;
+          u.gate_out = gate;
+          run_update(c, u);
+          check_launch();
+        }
       } catch (...) {
         cudaGraph_t junk;
         cudaStreamEndCapture(st, &junk);
@@ -1261,6 +1282,8 @@ void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
       OICA_CUDA(cudaStreamEndCapture(st, &captured));
     }
     OICA_CUDA(cudaGraphInstantiate(&c->loop.x, c->loop.g, 0));
+    c->loop.tiers = tiers;
+    c->loop.unroll = loop_unroll();
     c->loop.key = key;
     c->loop.valid = true;
   }
@@ -1270,18 +1293,38 @@ void enqueue_loop_graph(oica_ctx* c, int L_ub, int nc_ub, int K, double tol) {
   OICA_CUDA(cudaEventRecord(c->loop_ev1[c->slot], st));
 }
 
-// counters of a finished device-side loop of `iters` iterations (after the host wait)
-void finish_loop_graph(oica_ctx* c, int iters, int slot) {
+// counters of a finished device-side loop of `iters` iterations (after the host wait); hh = the
+// per-iteration history (rows entering iteration t at hh[2 (t - 1)]).  Launches counted as the
+// graph ran them: the gate node, then per body execution of tier i `unroll` x (step + update
+// [+ k_compact_iter above kUpdateCompactRows rows]), gated copies included
+void finish_loop_graph(oica_ctx* c, int iters, int slot, const int* hh) {
   float ms = 0.f;
   OICA_CUDA(cudaEventElapsedTime(&ms, c->loop_ev0[slot], c->loop_ev1[slot]));
   c->stats.graph_ms += ms;
   if (c->loop_persistent) {
     c->count(1);
     c->stats.step_launches += 1;
-  } else {
-    c->count(2 * std::max(iters, 1));
-    c->stats.step_launches += std::max(iters, 1);
+    return;
   }
+  const std::vector<int>& tiers = c->loop.tiers;
+  const int nt = (int)tiers.size(), U = c->loop.unroll;
+  std::vector<int> n_in((size_t)std::max(nt, 1), 0);   // iterations run by each tier's loop
+  int ti = 0;
+  for (int tt = 1; tt <= iters; ++tt) {
+    ++n_in[(size_t)ti];
+    const int out = tt < iters ? hh[2 * tt] : 0;   // rows left after iteration tt
+    // hand-over: the next tier's loop runs at least one iteration before testing its threshold
+    if (ti + 1 < nt && out <= tiers[(size_t)ti + 1]) ++ti;
+  }
+  int64_t launches = 1, steps = 0;
+  for (int i = 0; i < nt; ++i) {
+    const int64_t bodies = (n_in[(size_t)i] + U - 1) / U;
+    const int per = 2 + (tiers[(size_t)i] > kUpdateCompactRows ? 1 : 0);
+    launches += bodies * U * per;
+    steps += bodies * U;
+  }
+  c->count((int)launches);
+  c->stats.step_launches += steps;
 }
 
 // Tiny FP32 problems (the paper's own experiment sizes): the persistent cooperative loop
@@ -1606,7 +1649,7 @@ void extract_impl(oica_ctx* c, int32_t N_out, int32_t K, double tol, uint32_t fl
         account_iteration(c, Lin, ncin, -1, false);
         rows_at[tt] = {Lin, ncin};
       }
-      finish_loop_graph(c, t, j);
+      finish_loop_graph(c, t, j, hh);
     }
     // per-iteration log: every executed iteration; step_ms from its launch's events, or -1 for the
     // iterations of the device-side loop (not timed one by one)

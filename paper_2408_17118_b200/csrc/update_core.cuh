@@ -328,7 +328,12 @@ __device__ __forceinline__ void finish_iteration(const UpdateArgs& u, int2 r, in
   // do ... while (t < K and B != {})
   const int t_next = L_in > 0 ? t + 1 : t;
   const bool more = r.x > 0 && t_next <= u.K_loop;
-  if (u.loop) cudaGraphSetConditional(u.loop, (L_in > 0 && more && r.x > u.loop_thr) ? 1u : 0u);
+  const bool run = L_in > 0 && more && r.x > u.loop_thr;
+  if (u.loop) cudaGraphSetConditional(u.loop, run ? 1u : 0u);
+  if (u.gate_out) {
+    u.gate_out[0] = run ? r.x : 0;
+    u.gate_out[1] = run ? r.y : 0;
+  }
   if (u.loop_next) cudaGraphSetConditional(u.loop_next, more ? 1u : 0u);
 }
 
