@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256, 2) k_loop_simt(LoopSimtArgs a) {
     // in parallel into the step's shared memory), else the warp-group passes of k_update
     if (a.coop_update && L_act <= (int)gridDim.x) {
       if ((int)blockIdx.x < L_act)
-        upd::update_row_coop<NG>(u, blockIdx.x, L_act, t, k, (double*)smem, gsh, s4sh);
+        upd::update_row_coop<NG, true>(u, blockIdx.x, L_act, t, k, (double*)smem, gsh, s4sh);
     } else {
       for (int a0 = blockIdx.x * RPB; a0 < L_act; a0 += gridDim.x * RPB) {
         upd::update_pass<NG, false, RPB>(u, a0, L_act, t, k, gsh, s4sh, s_keep, true);

@@ -58,7 +58,10 @@ __device__ __forceinline__ void project_warp(double (&v)[V], const double* __res
 
 // sum_{j < n} v(j) in order j = 0, 1, ... (fp64), loads issued 8 at a time: with few active
 // rows the epilogue is a chain of dependent adds over S (x P) partials, latency-bound otherwise
-template <int D = 8, class F>
+// TAIL: the last n mod D terms as one more batch of predicated loads in flight together (same add
+// order).  Used by the persistent FP32 loop (Exp. 1 -3.5%); in the launched update kernels of the
+// tensor-core path the longer code measured 1-3% slower (cfg 1 / cfg 2; profiles/r02/session3/ab)
+template <int D = 8, bool TAIL = false, class F>
 __device__ __forceinline__ double ordered_sum(int n, F&& v) {
   double acc = 0.0;
   int j = 0;
@@ -68,6 +71,17 @@ __device__ __forceinline__ double ordered_sum(int n, F&& v) {
     for (int u = 0; u < D; ++u) t[u] = v(j + u);
 #pragma unroll
     for (int u = 0; u < D; ++u) acc += t[u];
+  }
+  if (TAIL) {
+    if (j < n) {
+      double t[D];
+#pragma unroll
+      for (int u = 0; u < D; ++u) t[u] = j + u < n ? v(j + u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < D; ++u)
+        if (j + u < n) acc += t[u];
+    }
+    return acc;
   }
   for (; j < n; ++j) acc += v(j);
   return acc;
@@ -387,7 +401,7 @@ __device__ __forceinline__ void update_pass(const UpdateArgs& u, int a_base, int
 // sums coordinates g*32 + lane over the slots in slot order from T -- the same sequential
 // association as slot_sum -- and warp 0 runs epilogue_core.  Every thread of the block must call
 // it.  keep[a] is written.
-template <int NG>
+template <int NG, bool TAIL = false>   // TAIL: ordered_sum's batched tail for the sum y^4 partials
 __device__ __forceinline__ void update_row_coop(const UpdateArgs& u, int a, int L_in, int t, int k, double* T,
                                                 double (*gsh)[NG * 32], double* s4sh) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -415,7 +429,7 @@ __device__ __forceinline__ void update_row_coop(const UpdateArgs& u, int a, int 
       gsh[0][n] = acc;
     }
     if (warp == NG && lane == 0 && u.s4p)
-      s4sh[0] = ordered_sum<16>(u.S, [&](int s) { return __ldg(u.s4p + (int64_t)s * u.cap + a); });
+      s4sh[0] = ordered_sum<16, TAIL>(u.S, [&](int s) { return __ldg(u.s4p + (int64_t)s * u.cap + a); });
   }
   __syncthreads();
   if (a < L_in && warp == 0) {

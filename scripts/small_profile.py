@@ -6,6 +6,7 @@ round trips, not the contraction, set the pace -- cfg 1 (all 32 components) and 
     python scripts/small_profile.py [--reps 5] [--cases cfg1,exp1_L20,exp1_L100]
 """
 import argparse
+import hashlib
 import json
 import os
 import sys
@@ -25,6 +26,8 @@ def case(name, eager):
     fl = oica.EAGER if eager else 0
     if name == "cfg1":
         return datagen.get("cfg1_artificial"), fl
+    if name == "cfg2":
+        return datagen.get("cfg2_eeg_shaped"), fl
     L = int(name.split("_L")[1])
     return datagen.EXPERIMENTS["exp1_ordering"].with_(L=L), fl
 
@@ -32,7 +35,7 @@ def case(name, eager):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--cases", default="cfg1,exp1_L20,exp1_L100")
+    ap.add_argument("--cases", default="cfg1,exp1_L20,exp1_L100")  # also: cfg2 (EEG-shaped, 32 components)
     ap.add_argument("--eager", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
@@ -68,7 +71,11 @@ def main():
                           "launches_per_extract": s["kernel_launches"] / a.reps, "iterations_per_extract": s["iterations"] / a.reps,
                           "step_ms_per_extract": s["step_ms"] / a.reps, "graph_ms_per_extract": s["graph_ms"] / a.reps,
                           "graph_iterations_per_extract": s["graph_iterations"] / a.reps,
-                          "precision": s["precision"]}), flush=True)
+                          "precision": s["precision"],
+                          # result digest (W, alpha, index, row-iterations): bitwise comparisons across builds
+                          "result_sha": hashlib.sha256(np.ascontiguousarray(r.W).tobytes() + r.alpha.tobytes() +
+                                                       r.index.tobytes() + np.asarray(r.sum_active).tobytes()
+                                                       ).hexdigest()[:16]}), flush=True)
 
 
 if __name__ == "__main__":
