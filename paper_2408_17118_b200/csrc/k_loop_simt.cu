@@ -32,7 +32,7 @@ struct LoopSimtArgs {
   int S;
   int flush;
   int K;
-  int coop_update;   // block-per-row updates through shared memory (S * NP doubles <= 96 KB)
+  int coop_update;   // block-per-row updates through shared memory (S * (NP + 1) doubles <= 96 KB)
   UpdateArgs u;      // G = the fp64 slot partials (S x cap x NP), s4p, act_in (kept in place), ctl, ...
 };
 
@@ -125,7 +125,9 @@ template <int NP, int NG>
 int launch_np(cudaStream_t st, const LoopSimtArgs& a, int num_sms) {
   auto kern = k_loop_simt<NP, NG>;
   // the step unit's tiles, reused by the block-per-row update for the S x NP slot partials of a row
-  const size_t smem = std::max(simt::unit_smem_bytes<NP>(), a.coop_update ? (size_t)a.S * NP * sizeof(double) : 0);
+  // (+ S doubles: the row's sum-y^4 slot partials, update_row_coop<NG, true>)
+  const size_t smem =
+      std::max(simt::unit_smem_bytes<NP>(), a.coop_update ? (size_t)a.S * (NP + 1) * sizeof(double) : 0);
   static size_t attr = 0;
   if (smem > attr) {
     OICA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -151,10 +153,10 @@ int launch_loop_simt(cudaStream_t st, const float* X, int64_t ld, int64_t M, int
   LoopSimtArgs a{X, ld, M, slot_len, S, flush, K, 0, u};
   switch (NP) {
     case 32:
-      a.coop_update = (size_t)S * 32 * sizeof(double) <= 96 * 1024 ? 1 : 0;
+      a.coop_update = (size_t)S * (32 + 1) * sizeof(double) <= 96 * 1024 ? 1 : 0;
       return launch_np<32, 1>(st, a, num_sms);
     case 64:
-      a.coop_update = (size_t)S * 64 * sizeof(double) <= 96 * 1024 ? 1 : 0;
+      a.coop_update = (size_t)S * (64 + 1) * sizeof(double) <= 96 * 1024 ? 1 : 0;
       return launch_np<64, 2>(st, a, num_sms);
     default: throw Error(OICA_ERR_INVALID_ARGUMENT, "persistent FP32 loop: padded N must be 32 or 64");
   }

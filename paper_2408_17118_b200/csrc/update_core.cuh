@@ -58,10 +58,7 @@ __device__ __forceinline__ void project_warp(double (&v)[V], const double* __res
 
 // sum_{j < n} v(j) in order j = 0, 1, ... (fp64), loads issued 8 at a time: with few active
 // rows the epilogue is a chain of dependent adds over S (x P) partials, latency-bound otherwise
-// TAIL: the last n mod D terms as one more batch of predicated loads in flight together (same add
-// order).  Used by the persistent FP32 loop (Exp. 1 -3.5%); in the launched update kernels of the
-// tensor-core path the longer code measured 1-3% slower (cfg 1 / cfg 2; profiles/r02/session3/ab)
-template <int D = 8, bool TAIL = false, class F>
+template <int D = 8, class F>
 __device__ __forceinline__ double ordered_sum(int n, F&& v) {
   double acc = 0.0;
   int j = 0;
@@ -71,17 +68,6 @@ __device__ __forceinline__ double ordered_sum(int n, F&& v) {
     for (int u = 0; u < D; ++u) t[u] = v(j + u);
 #pragma unroll
     for (int u = 0; u < D; ++u) acc += t[u];
-  }
-  if (TAIL) {
-    if (j < n) {
-      double t[D];
-#pragma unroll
-      for (int u = 0; u < D; ++u) t[u] = j + u < n ? v(j + u) : 0.0;
-#pragma unroll
-      for (int u = 0; u < D; ++u)
-        if (j + u < n) acc += t[u];
-    }
-    return acc;
   }
   for (; j < n; ++j) acc += v(j);
   return acc;
@@ -401,7 +387,10 @@ __device__ __forceinline__ void update_pass(const UpdateArgs& u, int a_base, int
 // sums coordinates g*32 + lane over the slots in slot order from T -- the same sequential
 // association as slot_sum -- and warp 0 runs epilogue_core.  Every thread of the block must call
 // it.  keep[a] is written.
-template <int NG, bool TAIL = false>   // TAIL: ordered_sum's batched tail for the sum y^4 partials
+// S4SH (the persistent FP32 loop): the row's sum-y^4 slot partials are loaded with the G partials,
+// in parallel, into T[S * NP ...] (S more doubles of shared memory) and summed from there in slot
+// order -- one L2 round trip instead of a chain of S / 16 (Exp. 1: see DESIGN.md §5)
+template <int NG, bool S4SH = false>
 __device__ __forceinline__ void update_row_coop(const UpdateArgs& u, int a, int L_in, int t, int k, double* T,
                                                 double (*gsh)[NG * 32], double* s4sh) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -419,6 +408,8 @@ __device__ __forceinline__ void update_row_coop(const UpdateArgs& u, int a, int 
         T[s * NPd + n] = n < u.N ? slot_part(u.G, P, s, u.cap, u.ldg, a, n) : 0.0;
       }
     }
+    if (S4SH && u.s4p)
+      for (int s = threadIdx.x; s < u.S; s += blockDim.x) T[u.S * NPd + s] = __ldg(u.s4p + (int64_t)s * u.cap + a);
   }
   __syncthreads();
   if (a < L_in) {
@@ -428,8 +419,15 @@ __device__ __forceinline__ void update_row_coop(const UpdateArgs& u, int a, int 
       for (int s = 0; s < u.S; ++s) acc += T[s * NPd + n];   // slot order (slot_sum's association)
       gsh[0][n] = acc;
     }
-    if (warp == NG && lane == 0 && u.s4p)
-      s4sh[0] = ordered_sum<16, TAIL>(u.S, [&](int s) { return __ldg(u.s4p + (int64_t)s * u.cap + a); });
+    if (warp == NG && lane == 0 && u.s4p) {
+      if (S4SH) {
+        double acc = 0.0;
+        for (int s = 0; s < u.S; ++s) acc += T[u.S * NPd + s];   // slot order (ordered_sum's association)
+        s4sh[0] = acc;
+      } else {
+        s4sh[0] = ordered_sum<16>(u.S, [&](int s) { return __ldg(u.s4p + (int64_t)s * u.cap + a); });
+      }
+    }
   }
   __syncthreads();
   if (a < L_in && warp == 0) {
