@@ -401,11 +401,36 @@ __device__ __forceinline__ void update_row_coop(const UpdateArgs& u, int a, int 
   if (a < L_in) {
     l = u.act_in[a];
     if (warp == 0) load_row<NG>(u, l, lane, wo, we);
-    for (int s = warp; s < u.S; s += nw) {
+    if (S4SH) {
+      // a warp's slots (S / 8 of them at Exp. 1's S = 78) loaded into registers together, then
+      // stored: a load-store loop through the generic T pointer waits for each load in turn
+      constexpr int B = 8;
+      for (int s0 = warp; s0 < u.S; s0 += nw * B) {
+        double v[B][NG];
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        const int n = g * 32 + lane;
-        T[s * NPd + n] = n < u.N ? slot_part(u.G, P, s, u.cap, u.ldg, a, n) : 0.0;
+        for (int b = 0; b < B; ++b) {
+          const int s = s0 + b * nw;
+#pragma unroll
+          for (int g = 0; g < NG; ++g) {
+            const int n = g * 32 + lane;
+            v[b][g] = (s < u.S && n < u.N) ? slot_part(u.G, P, s, u.cap, u.ldg, a, n) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const int s = s0 + b * nw;
+          if (s < u.S)
+#pragma unroll
+            for (int g = 0; g < NG; ++g) T[s * NPd + g * 32 + lane] = v[b][g];
+        }
+      }
+    } else {
+      for (int s = warp; s < u.S; s += nw) {
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          const int n = g * 32 + lane;
+          T[s * NPd + n] = n < u.N ? slot_part(u.G, P, s, u.cap, u.ldg, a, n) : 0.0;
+        }
       }
     }
     if (S4SH && u.s4p)
