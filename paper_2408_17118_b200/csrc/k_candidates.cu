@@ -56,19 +56,26 @@ __global__ void k_cand_init(uint64_t seed, int i, int64_t id_base, int64_t L_loc
 // component): block 0 alone, compacting in shared memory; otherwise the block that finishes last
 // (ticket) compacts.
 template <int NG, bool F32>
-__global__ void __launch_bounds__(512) k_update(UpdateArgs u) {
+__global__ void __launch_bounds__(512, 1) k_update(UpdateArgs u) {
   constexpr int RPB = 16 / NG;
   __shared__ double gsh[RPB][NG * 32];
   __shared__ double s4sh[RPB];
   __shared__ int s_keep[RPB];
   __shared__ int s_last;
-  if (u.gate_in && u.gate_in[0] == 0) return;   // grid-uniform (the writer is this kernel's last block)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (u.gate_in && u.gate_in[0] == 0) return;   // grid-uniform (the writer is this kernel's last block)
   const int t = u.ctl->t, k = u.ctl->k;
   const int L_in = u.cnt_in ? min(u.L_ub, u.cnt_in[0]) : u.L_ub;
   const bool single = L_in <= RPB && u.compact;   // grid-uniform
   if (L_in <= RPB && blockIdx.x != 0) return;
+#ifdef OICA_EXPERIMENTS
+  long long stamp[8];
+  stamp[3] = clock64();
+  update_pass<NG, F32, RPB>(u, blockIdx.x * RPB, L_in, t, k, gsh, s4sh, s_keep, !single || !u.compact, stamp);
+  stamp[4] = clock64();
+#else
   update_pass<NG, F32, RPB>(u, blockIdx.x * RPB, L_in, t, k, gsh, s4sh, s_keep, !single || !u.compact);
+#endif
   if (!u.compact) return;   // (k_compact follows)
   int2 r;
   if (single) {   // K4 by one warp: kept coarse rows, then kept fine rows (k_compact's order)
@@ -98,14 +105,26 @@ __global__ void __launch_bounds__(512) k_update(UpdateArgs u) {
     }
     __syncthreads();
     if (!s_last) return;
+#ifdef OICA_EXPERIMENTS
+    stamp[5] = clock64();
+#endif
     __threadfence();
-    r = compact_block(u.act_in, u.keep, u.pr.fine, L_in, u.act_out);   // K4
-    if (u.copy_back) {
-      int* dst = const_cast<int*>(u.act_in);
-      for (int j = threadIdx.x; j < r.x; j += blockDim.x) dst[j] = u.act_out[j];
-    }
+    r = compact_block(u.act_in, u.keep, u.pr.fine, L_in, u.act_out,
+                      u.copy_back ? const_cast<int*>(u.act_in) : nullptr);   // K4
   }
+#ifdef OICA_EXPERIMENTS
+  if (threadIdx.x == 0 && !single) stamp[6] = clock64();
+#endif
   if (threadIdx.x == 0) finish_iteration(u, r, L_in, t);
+#ifdef OICA_EXPERIMENTS
+  // phase cycles of the block that finished last (its own SM clock): entry -> row loads landed ->
+  // slot sums stored -> barrier -> epilogue done -> ticket known -> compaction done -> finish
+  if (threadIdx.x == 0 && !single && t <= 3 && (k & 7) == 1)
+    printf("oica exp: k_update<%d> k %d t %d L_in %d grid %d block %d: rows %lld slots %lld barrier %lld epilogue %lld "
+           "ticket %lld compact %lld finish %lld cycles\n", NG, k, t, L_in, (int)gridDim.x, (int)blockIdx.x,
+           stamp[0] - stamp[3], stamp[1] - stamp[0], stamp[2] - stamp[1], stamp[4] - stamp[2], stamp[5] - stamp[4],
+           stamp[6] - stamp[5], clock64() - stamp[6]);
+#endif
 }
 
 // K3 + K4 for few rows (L_ub <= kUpdateCoopRows, the tail of a component): one block of 16 warps

@@ -11,6 +11,26 @@ namespace upd {
 
 constexpr int kMaxV = 8;  // 256 / 32 coordinates per lane
 
+// c[b] <- warp_sum(c[b]) for every b, the butterfly stages issued value-interleaved (up to 8 values
+// per stage): each value sees warp_sum's own sequence of adds (bitwise the same sums), but the
+// shuffles of different values overlap -- one value after the other is a chain of 5 shuffle + add
+// latencies per value (the compiler does not interleave them: measured)
+template <int RB>
+__device__ __forceinline__ void warp_sum_many(double (&c)[RB]) {
+  constexpr int G = RB < 8 ? RB : 8;
+#pragma unroll
+  for (int b0 = 0; b0 < RB; b0 += G) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double t[G];
+#pragma unroll
+      for (int b = 0; b < G; ++b) t[b] = __shfl_xor_sync(0xffffffffu, c[b0 + b], o);
+#pragma unroll
+      for (int b = 0; b < G; ++b) c[b0 + b] += t[b];
+    }
+  }
+}
+
 // v <- v - E v with E = Wacc^T Wacc: all coefficients w_k . v are
 // taken from the incoming v (one projection, as written in the paper).
 template <int V>
@@ -38,8 +58,7 @@ __device__ __forceinline__ void project_warp(double (&v)[V], const double* __res
         }
       }
     }
-#pragma unroll
-    for (int b = 0; b < RB; ++b) c[b] = warp_sum(c[b]);
+    warp_sum_many<RB>(c);
 #pragma unroll
     for (int b = 0; b < RB; ++b) {
       if (b < nb) {
@@ -69,7 +88,14 @@ __device__ __forceinline__ double ordered_sum(int n, F&& v) {
 #pragma unroll
     for (int u = 0; u < D; ++u) acc += t[u];
   }
-  for (; j < n; ++j) acc += v(j);
+  if (j < n) {   // the tail as one predicated batch (a rolled load-add loop waits for each load in turn)
+    double t[D];
+#pragma unroll
+    for (int u = 0; u < D; ++u) t[u] = j + u < n ? v(j + u) : 0.0;
+#pragma unroll
+    for (int u = 0; u < D; ++u)
+      if (j + u < n) acc += t[u];
+  }
   return acc;
 }
 
@@ -110,7 +136,7 @@ __device__ __forceinline__ double slot_sum(SlotPartials Gp, int S, int64_t cap, 
   }
   const int P = parts_of(Gp, S);
   // split parts: each slot's value already sums up to 8 partials (loads in flight); rolled loop
-  if (P > 1) return ordered_sum<2>(S, [&](int s) { return slot_part(Gp, P, s, cap, ldg, a, n); });
+  if (P > 1) return ordered_sum<(D >= 16 ? 4 : 2)>(S, [&](int s) { return slot_part(Gp, P, s, cap, ldg, a, n); });
   // one partial per slot (the common case; the loop the whole-L epilogue streams at HBM rate)
   if (KIND == 2 || Gp.f32) {
     const float* g = (const float*)Gp.p + (int64_t)a * ldg + n;
@@ -120,6 +146,13 @@ __device__ __forceinline__ double slot_sum(SlotPartials Gp, int S, int64_t cap, 
   const double* g = (const double*)Gp.p + (int64_t)a * ldg + n;
   const int64_t st = cap * ldg;
   return ordered_sum<D>(S, [&](int s) { return g[s * st]; });
+}
+
+// slot_sum kept out of line: in the few-row update the split-part / fp64-partial branch is the
+// cold one, and its unrolled loads would sit in the middle of the hot path's instruction stream
+template <int D, int KIND>
+__device__ __noinline__ double slot_sum_outlined(SlotPartials Gp, int S, int64_t cap, int ldg, int a, int n) {
+  return slot_sum<D, KIND>(Gp, S, cap, ldg, a, n);
 }
 
 // coordinate n of the point the contraction used for candidate l (master value w64 if none)
@@ -249,18 +282,47 @@ __device__ __forceinline__ bool epilogue_core(int l, int lane, const double (&ac
 // Order-preserving compaction by one block (deterministic), stably partitioned into coarse rows
 // followed by fine rows; act_in null: the identity list.  Each thread takes a contiguous run of
 // positions; counts are scanned with warp shuffles and one warp over the warp totals.  Returns
-// (n_coarse + n_fine, n_coarse) in every thread.
-__device__ __forceinline__ int2 compact_block(const int* __restrict__ act_in, const uint8_t* __restrict__ keep,
-                                              const uint8_t* __restrict__ fine, int L_in, int* __restrict__ act_out) {
+// (n_coarse + n_fine, n_coarse) in every thread.  copy_dst (may be act_in): the list is written
+// there too.
+__device__ __forceinline__ int2 compact_block(const int* act_in, const uint8_t* __restrict__ keep,
+                                              const uint8_t* __restrict__ fine, int L_in, int* act_out,
+                                              int* copy_dst = nullptr) {
   __shared__ int wc[32], wf[32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (blockDim.x + 31) >> 5;
   const int per = (L_in + blockDim.x - 1) / blockDim.x;
   const int b = t * per, e = min(L_in, b + per);
+  // few positions per thread (the latency-bound lists): a thread's flags and ids are loaded together
+  // and kept in registers for the second pass -- two load round trips instead of three per position
+  // and pass; the list written is the same
+  constexpr int R = 4;
+  const bool few = per <= R;   // block-uniform
+  int ids[R];
+  bool kp[R], fn[R];
   int cc = 0, cf = 0;
-  for (int a = b; a < e; ++a) {
-    if (!keep[a]) continue;
-    int id = act_in ? act_in[a] : a;
-    if (fine && fine[id]) ++cf; else ++cc;
+  if (few) {
+    uint8_t kq[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int a = b + r;
+      kq[r] = a < e ? keep[a] : (uint8_t)0;
+      ids[r] = a < e ? (act_in ? act_in[a] : a) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      kp[r] = kq[r] != 0;
+      fn[r] = kp[r] && fine && fine[ids[r]];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      cc += (kp[r] && !fn[r]) ? 1 : 0;
+      cf += fn[r] ? 1 : 0;
+    }
+  } else {
+    for (int a = b; a < e; ++a) {
+      if (!keep[a]) continue;
+      int id = act_in ? act_in[a] : a;
+      if (fine && fine[id]) ++cf; else ++cc;
+    }
   }
   int ic = cc, jf = cf;   // inclusive warp scans of (cc, cf)
 #pragma unroll
@@ -293,12 +355,25 @@ __device__ __forceinline__ int2 compact_block(const int* __restrict__ act_in, co
   const int n_coarse = wc[nw - 1], n_fine = wf[nw - 1];
   const int base_c = (w ? wc[w - 1] : 0) + ic - cc, base_f = (w ? wf[w - 1] : 0) + jf - cf;
   int pc = base_c, pf = n_coarse + base_f;
-  for (int a = b; a < e; ++a) {
-    if (!keep[a]) continue;
-    int id = act_in ? act_in[a] : a;
-    if (fine && fine[id]) act_out[pf++] = id; else act_out[pc++] = id;
+  if (few) {   // (every thread read its act_in entries before the barriers above: copy_dst may be act_in)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (kp[r]) {
+        const int p = fn[r] ? pf++ : pc++;
+        act_out[p] = ids[r];
+        if (copy_dst) copy_dst[p] = ids[r];
+      }
+    }
+  } else {
+    for (int a = b; a < e; ++a) {
+      if (!keep[a]) continue;
+      int id = act_in ? act_in[a] : a;
+      if (fine && fine[id]) act_out[pf++] = id; else act_out[pc++] = id;
+    }
   }
   __syncthreads();   // wc / wf are read above by every thread
+  if (!few && copy_dst)
+    for (int j = t; j < n_coarse + n_fine; j += blockDim.x) copy_dst[j] = act_out[j];
   return make_int2(n_coarse + n_fine, n_coarse);
 }
 
@@ -344,7 +419,8 @@ __device__ __forceinline__ void finish_iteration(const UpdateArgs& u, int2 r, in
 // the row stays active (and keep[a] when write_keep).
 template <int NG, bool F32, int RPB>
 __device__ __forceinline__ void update_pass(const UpdateArgs& u, int a_base, int L_in, int t, int k,
-                                            double (*gsh)[NG * 32], double* s4sh, int* keep_sh, bool write_keep) {
+                                            double (*gsh)[NG * 32], double* s4sh, int* keep_sh, bool write_keep,
+                                            long long* stamp = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = warp / NG, grp = warp - rb * NG;
   const int a = a_base + rb;
@@ -360,15 +436,49 @@ __device__ __forceinline__ void update_pass(const UpdateArgs& u, int a_base, int
       __trap();
     }
 #endif
-    if (grp == 0) load_row<NG>(u, l, lane, wo, we);   // (in flight with the slot sums below)
     const int n = grp * 32 + lane;
-    // (16 partials in flight per lane: with few active rows the slot chain is latency-bound; the
+    // (D partials in flight per lane: with few active rows the slot chain is latency-bound; the
     // association is the same sequential slot order whatever the depth)
-    gsh[rb][n] = n < u.N ? slot_sum<(NG >= 8 ? 8 : 16), (F32 ? 2 : 1)>(u.G, u.S, u.cap, u.ldg, a, n) : 0.0;
+    constexpr int D = NG >= 8 ? 8 : (NG == 1 ? 32 : 16);
+    if (F32 && parts_of(u.G, u.S) == 1) {
+      // one fp32 partial per slot: the first D slot loads (addresses from the row position a alone)
+      // are issued before the row's w_old / w_e loads, which wait for act_in[a] -- one L2 round
+      // trip for both instead of a chain (slot_sum's sum: acc = 0, += slot 0, 1, ... in order)
+      const float* g = (const float*)u.G.p + (int64_t)a * u.ldg + n;
+      const int64_t st = u.cap * u.ldg;
+      const bool nk = n < u.N;
+      float tb[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) tb[q] = (nk && q < u.S) ? g[q * st] : 0.f;
+      if (grp == 0) load_row<NG>(u, l, lane, wo, we);
+      if (stamp) stamp[0] = clock64() + (long long)(wo[0] * 0.0);   // (experiments build: after the row loads landed)
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q)
+        if (q < u.S) acc += (double)tb[q];
+      for (int j = D; j < u.S; j += D) {
+#pragma unroll
+        for (int q = 0; q < D; ++q) tb[q] = (nk && j + q < u.S) ? g[(int64_t)(j + q) * st] : 0.f;
+#pragma unroll
+        for (int q = 0; q < D; ++q)
+          if (j + q < u.S) acc += (double)tb[q];
+      }
+      gsh[rb][n] = nk ? acc : 0.0;
+    } else {
+      if (grp == 0) load_row<NG>(u, l, lane, wo, we);   // (in flight with the slot sums below)
+      // F32: only the split-part case gets here (the cold branch, out of line); fp64 partials (the
+      // FP32 step): this IS the row's slot sum, inline
+      if (F32)
+        gsh[rb][n] = n < u.N ? slot_sum_outlined<D, 2>(u.G, u.S, u.cap, u.ldg, a, n) : 0.0;
+      else
+        gsh[rb][n] = n < u.N ? slot_sum<D, 1>(u.G, u.S, u.cap, u.ldg, a, n) : 0.0;
+    }
     if (grp == 0 && lane == 0 && u.s4p)
       s4sh[rb] = ordered_sum<16>(u.S, [&](int s) { return __ldg(u.s4p + (int64_t)s * u.cap + a); });
   }
+  if (stamp) stamp[1] = clock64();
   __syncthreads();
+  if (stamp) stamp[2] = clock64();
   if (row_ok && grp == 0) {
     double acc[NG];
 #pragma unroll
