@@ -42,7 +42,7 @@ __device__ __forceinline__ void project_warp(double (&v)[V], const double* __res
   // rows in blocks of RB: their loads and warp reductions are independent (latency-bound
   // otherwise when few rows run); same operations in the same order per row (h accumulates the
   // rows in row order for any RB).  RB x V bounded (registers: 8 coordinates per lane fill them)
-  constexpr int RB = V >= 8 ? 1 : V == 1 ? 16 : 8 / V;
+  constexpr int RB = V >= 8 ? 1 : 8 / V;
   for (int r0 = 0; r0 < k; r0 += RB) {
     const int nb = min(RB, k - r0);
     double c[RB];
